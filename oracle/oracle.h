@@ -1,0 +1,143 @@
+/* oracle.h — CPU ORACLE for arXiv 2403.06648's hot path.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * leg may load this library.  It shares no code, header, constant table or helper with
+ * the CUDA path (paper_2403_06648_b200/csrc); both are written from PAPER.md and the
+ * readings R1-R32 listed in DESIGN.md.
+ *
+ * Coarse part (FP32, compiled with -ffp-contract=off, no fast-math): the plain
+ * definition of SURVEY §8(c) C.1 — at every segment the hit is the GLOBAL lexicographic
+ * argmin over ALL surfels of (t, id) under the HIT predicate (brute force; no grid).
+ * Refinement part (FP64, refine.c): damped Gauss-Newton on the stationarity residual
+ * of Eqs. 9-11 with the Eq. 1-4 MLS surface.
+ */
+#ifndef NRT_ORACLE_H
+#define NRT_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OR_MAX_INT 8
+
+typedef struct {
+    float a[3], b[3];   /* edge segment endpoints (m) */
+    float t0[3];        /* face-0 tangent, perpendicular to e, pointing into face 0 */
+    float n0[3];        /* face-0 outward normal */
+    float n1[3];        /* face-1 outward normal */
+    float n_exp;        /* exterior angle = n_exp * pi, 1 < n_exp < 2 */
+    int32_t label;      /* unique edge label */
+} or_edge;
+
+typedef struct {
+    const float* p;        /* n x 3 positions */
+    const float* nrm;      /* n x 3 normals (as given) */
+    const float* r;        /* n radii */
+    const int32_t* label;  /* n labels, 0 <= label < 4096 */
+    int64_t n;
+    const or_edge* edges;
+    int32_t n_edges;
+} or_scene;
+
+typedef struct {
+    float tx[3];
+    const float* rx;       /* n_rx x 3 */
+    int32_t n_rx;
+    int64_t n_rays;        /* N of the Fibonacci lattice (global) */
+    int32_t max_refl, max_diff;
+    int32_t kappa;
+    float tau;             /* departure-sheet noise tolerance (R8) */
+    float c_R;             /* reception-sphere scale (R12) */
+    float dphi_deg;        /* Keller fan step (R15) */
+    float theta_ex_deg;    /* departure-sheet angle (R8) */
+    float edge_bin;        /* event s-bin (R14) */
+    int32_t rank, world;   /* ray shard i == rank (mod world) */
+} or_launch_params;
+
+/* coarse path record (R17 key + representative) */
+typedef struct {
+    uint32_t rx;
+    uint8_t n_int, n_diff;
+    uint16_t kinds;                 /* bit k set <=> interaction k is a diffraction */
+    int32_t label[OR_MAX_INT];      /* surfel label or edge label; 0 beyond n_int */
+    uint32_t prim[OR_MAX_INT];      /* surfel id or edge id; 0 beyond n_int */
+    float v[OR_MAX_INT][3];         /* interaction points; 0 beyond n_int */
+    float s_edge;                   /* edge parameter of the diffraction (0 if none) */
+    float L;                        /* unfolded length at the RX closest approach */
+    uint64_t ray_id;
+} or_coarse;
+
+/* interaction history of a ray (internal state, also carried by events) */
+typedef struct {
+    int32_t n;                      /* interactions so far */
+    int32_t n_diff;
+    uint16_t kinds;
+    uint16_t pad_;
+    int32_t label[OR_MAX_INT];
+    uint32_t prim[OR_MAX_INT];
+    float v[OR_MAX_INT][3];
+    float s_edge;
+} or_hist;
+
+/* diffraction event (R13/R14) */
+typedef struct {
+    or_hist h;
+    uint32_t edge;
+    int32_t sbin;
+    float s;
+    float d[3];
+    float L;        /* unfolded length at the edge point */
+    float dist2;
+    uint64_t ray_id;
+} or_event;
+
+/* ---- building blocks exposed for the pin tests ---- */
+void or_sincos(double x, double* s, double* c);
+void or_fib_dir(uint64_t i, uint64_t n, float d[3]);
+float or_cos_ex(float theta_ex_deg);
+float or_cRw(float c_R, int64_t n_rays);
+/* HIT predicate R7-R8 for one surfel; returns 1 and writes *t on hit */
+int or_hit(const float o[3], const float d[3], const float p[3], const float n[3], float r,
+           const float* lam, int n_lam, float tau, float cos_ex, float* t);
+void or_reflect(const float d[3], const float n[3], float out[3]);
+/* brute-force nearest hit; returns surfel id or -1 (escape) */
+int64_t or_nearest(const or_scene* S, const float o[3], const float d[3], const float* lam,
+                   int n_lam, int64_t prev, float tau, float cos_ex, float* t_hit);
+
+/* R13 closest approach of ray (o,d) to edge E; 0 if parallel */
+int or_edge_closest(const float o[3], const float d[3], const or_edge* E, float* te, float* s,
+                    float* dist2);
+/* R15 Keller fan directions (Eq. 14) for incident d; returns M (writes min(M,cap)) */
+int or_fan_dirs(const or_edge* E, const float d[3], float dphi_deg, float* out, int cap);
+
+/* ---- the coarse operation ---- */
+/* Trace the rays of the shard (all diffraction handled inside), dedupe (R17).
+ * raw/out are caller buffers; returns 0 ok, 4 overflow (sizes still reported). */
+int or_launch(const or_scene* S, const or_launch_params* P, or_coarse* raw, int64_t raw_cap,
+              int64_t* n_raw, or_coarse* out, int64_t out_cap, int64_t* n_out,
+              uint64_t* n_bounces);
+/* The same operation in phases (so tests may run shards in parallel processes):
+ * primary rays i == P->rank (mod P->world) -> raw records + raw events;
+ * event dedupe (sorted by key, min (dist2, ray id) kept; returns count);
+ * fans of events r == part (mod parts), r = global event rank. */
+int or_trace_primary(const or_scene* S, const or_launch_params* P, or_coarse* raw,
+                     int64_t raw_cap, int64_t* n_raw, or_event* ev, int64_t ev_cap,
+                     int64_t* n_ev, uint64_t* n_bounces);
+int64_t or_event_dedupe(or_event* ev, int64_t n);
+int or_trace_fans(const or_scene* S, const or_launch_params* P, const or_event* ev, int64_t n_ev,
+                  int32_t part, int32_t parts, or_coarse* raw, int64_t raw_cap, int64_t* n_raw,
+                  uint64_t* n_bounces);
+/* Trace only primary rays with ids ray_ids[0..n) (sampled parity / cpu baseline).
+ * Emits raw (not deduped) records; hit_ids (n x (max_refl+1)) gets the per-segment surfel
+ * id or -1 (escape) or -2 (not traced).  Diffraction events are not followed. */
+int or_trace_rays(const or_scene* S, const or_launch_params* P, const uint64_t* ray_ids,
+                  int64_t n, or_coarse* raw, int64_t raw_cap, int64_t* n_raw, int64_t* hit_ids,
+                  uint64_t* n_bounces);
+/* R17 dedupe of an arbitrary record array (sort by key, L, ray id; keep first kappa) */
+int64_t or_dedupe(or_coarse* recs, int64_t n, int32_t kappa);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

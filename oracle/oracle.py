@@ -1,0 +1,362 @@
+"""ctypes wrapper of the CPU ORACLE (oracle/*.c).  TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+may import this module.  It never imports the CUDA product path and vice versa.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_SRCS = ["coarse.c", "refine.c"]
+
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+          "-Wall", "-Wno-unused-function"]
+
+
+def build(force: bool = False) -> str:
+    srcs = [os.path.join(_HERE, s) for s in _SRCS if os.path.exists(os.path.join(_HERE, s))]
+    if not force and os.path.exists(_LIB_PATH):
+        mt = os.path.getmtime(_LIB_PATH)
+        deps = srcs + [os.path.join(_HERE, "oracle.h")]
+        if all(os.path.getmtime(s) <= mt for s in deps):
+            return _LIB_PATH
+    cmd = ["gcc", *CFLAGS, "-o", _LIB_PATH, *srcs, "-lm"]
+    subprocess.run(cmd, check=True)
+    return _LIB_PATH
+
+
+COARSE_DTYPE = np.dtype([
+    ("rx", "<u4"), ("n_int", "u1"), ("n_diff", "u1"), ("kinds", "<u2"),
+    ("label", "<i4", (8,)), ("prim", "<u4", (8,)), ("v", "<f4", (8, 3)),
+    ("s_edge", "<f4"), ("L", "<f4"), ("ray_id", "<u8")], align=True)
+assert COARSE_DTYPE.itemsize == 184
+
+
+HIST_FIELDS = [("n", "<i4"), ("n_diff", "<i4"), ("kinds", "<u2"), ("pad_", "<u2"),
+               ("label", "<i4", (8,)), ("prim", "<u4", (8,)), ("v", "<f4", (8, 3)),
+               ("s_edge", "<f4")]
+EVENT_DTYPE = np.dtype([("h", np.dtype(HIST_FIELDS, align=True)), ("edge", "<u4"),
+                        ("sbin", "<i4"), ("s", "<f4"), ("d", "<f4", (3,)), ("L", "<f4"),
+                        ("dist2", "<f4"), ("ray_id", "<u8")], align=True)
+assert EVENT_DTYPE.itemsize == 216
+
+
+class _Edge(C.Structure):
+    _fields_ = [("a", C.c_float * 3), ("b", C.c_float * 3), ("t0", C.c_float * 3),
+                ("n0", C.c_float * 3), ("n1", C.c_float * 3), ("n_exp", C.c_float),
+                ("label", C.c_int32)]
+
+
+class _Scene(C.Structure):
+    _fields_ = [("p", C.c_void_p), ("nrm", C.c_void_p), ("r", C.c_void_p), ("label", C.c_void_p),
+                ("n", C.c_int64), ("edges", C.c_void_p), ("n_edges", C.c_int32)]
+
+
+class _Params(C.Structure):
+    _fields_ = [("tx", C.c_float * 3), ("rx", C.c_void_p), ("n_rx", C.c_int32),
+                ("n_rays", C.c_int64), ("max_refl", C.c_int32), ("max_diff", C.c_int32),
+                ("kappa", C.c_int32), ("tau", C.c_float), ("c_R", C.c_float),
+                ("dphi_deg", C.c_float), ("theta_ex_deg", C.c_float), ("edge_bin", C.c_float),
+                ("rank", C.c_int32), ("world", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(_LIB_PATH)
+        L.or_sincos.argtypes = [C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.or_fib_dir.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p]
+        L.or_cos_ex.argtypes = [C.c_float]
+        L.or_cos_ex.restype = C.c_float
+        L.or_cRw.argtypes = [C.c_float, C.c_int64]
+        L.or_cRw.restype = C.c_float
+        L.or_hit.argtypes = [C.c_void_p] * 4 + [C.c_float, C.c_void_p, C.c_int, C.c_float,
+                                                 C.c_float, C.POINTER(C.c_float)]
+        L.or_reflect.argtypes = [C.c_void_p] * 3
+        L.or_nearest.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                 C.c_int64, C.c_float, C.c_float, C.POINTER(C.c_float)]
+        L.or_nearest.restype = C.c_int64
+        L.or_launch.argtypes = [C.POINTER(_Scene), C.POINTER(_Params), C.c_void_p, C.c_int64,
+                                C.POINTER(C.c_int64), C.c_void_p, C.c_int64,
+                                C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
+        L.or_trace_rays.argtypes = [C.POINTER(_Scene), C.POINTER(_Params), C.c_void_p, C.c_int64,
+                                    C.c_void_p, C.c_int64, C.POINTER(C.c_int64), C.c_void_p,
+                                    C.POINTER(C.c_uint64)]
+        L.or_trace_primary.argtypes = [C.POINTER(_Scene), C.POINTER(_Params), C.c_void_p,
+                                       C.c_int64, C.POINTER(C.c_int64), C.c_void_p, C.c_int64,
+                                       C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
+        L.or_event_dedupe.argtypes = [C.c_void_p, C.c_int64]
+        L.or_event_dedupe.restype = C.c_int64
+        L.or_trace_fans.argtypes = [C.POINTER(_Scene), C.POINTER(_Params), C.c_void_p, C.c_int64,
+                                    C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
+                                    C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
+        L.or_dedupe.argtypes = [C.c_void_p, C.c_int64, C.c_int32]
+        L.or_dedupe.restype = C.c_int64
+        L.or_edge_closest.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Edge),
+                                      C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                      C.POINTER(C.c_float)]
+        L.or_fan_dirs.argtypes = [C.POINTER(_Edge), C.c_void_p, C.c_float, C.c_void_p, C.c_int]
+        _lib = L
+    return _lib
+
+
+def _f32(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if shape is not None:
+        a = a.reshape(shape)
+    return a
+
+
+class OracleScene:
+    """Keeps the numpy arrays alive and the C view of them."""
+
+    def __init__(self, scene):
+        self.p = _f32(scene.points, (-1, 3))
+        self.nrm = _f32(scene.normals, (-1, 3))
+        self.r = _f32(scene.radii, (-1,))
+        self.label = np.ascontiguousarray(scene.labels, dtype=np.int32)
+        E = scene.edges
+        self.n_edges = len(E)
+        self.edges = (_Edge * max(1, self.n_edges))()
+        for j in range(self.n_edges):
+            e = self.edges[j]
+            e.a[:] = [float(x) for x in E.a[j]]
+            e.b[:] = [float(x) for x in E.b[j]]
+            e.t0[:] = [float(x) for x in E.t0[j]]
+            e.n0[:] = [float(x) for x in E.n0[j]]
+            e.n1[:] = [float(x) for x in E.n1[j]]
+            e.n_exp = float(E.n_exp[j])
+            e.label = int(E.label[j])
+        self.c = _Scene(self.p.ctypes.data, self.nrm.ctypes.data, self.r.ctypes.data,
+                        self.label.ctypes.data, self.p.shape[0],
+                        C.cast(self.edges, C.c_void_p), self.n_edges)
+
+
+def _params(case, rx=None, max_diff=None):
+    rxa = _f32(case.rx if rx is None else rx, (-1, 3))
+    p = _Params()
+    p.tx[:] = [float(x) for x in np.asarray(case.tx, np.float32)]
+    p.rx = rxa.ctypes.data
+    p.n_rx = rxa.shape[0]
+    p.n_rays = int(case.n_rays)
+    p.max_refl = int(case.max_refl)
+    p.max_diff = int(case.max_diff if max_diff is None else max_diff)
+    p.kappa = int(case.kappa)
+    p.tau = float(case.tau)
+    p.c_R = float(case.c_R)
+    p.dphi_deg = float(case.dphi_deg)
+    p.theta_ex_deg = float(case.theta_ex_deg)
+    p.edge_bin = float(case.edge_bin)
+    p.rank = 0
+    p.world = 1
+    return p, rxa
+
+
+def sincos(x: float):
+    s, c = C.c_double(), C.c_double()
+    lib().or_sincos(float(x), C.byref(s), C.byref(c))
+    return s.value, c.value
+
+
+def fib_dir(i: int, n: int) -> np.ndarray:
+    d = np.zeros(3, np.float32)
+    lib().or_fib_dir(int(i), int(n), d.ctypes.data)
+    return d
+
+
+def fib_dirs(n: int, ids=None) -> np.ndarray:
+    ids = range(n) if ids is None else ids
+    return np.stack([fib_dir(i, n) for i in ids]) if len(ids) else np.zeros((0, 3), np.float32)
+
+
+def cos_ex(theta_deg: float) -> float:
+    return lib().or_cos_ex(float(theta_deg))
+
+
+def cRw(c_R: float, n_rays: int) -> float:
+    return lib().or_cRw(float(c_R), int(n_rays))
+
+
+def hit(o, d, p, n, r, lam=(), tau=0.0015, cosex=None):
+    """R7-R8 predicate for one surfel -> t or None."""
+    o, d, p, n = (_f32(x, (3,)) for x in (o, d, p, n))
+    lam = np.ascontiguousarray(np.asarray(lam, np.float32).reshape(-1, 3))
+    nl = lam.shape[0]
+    if nl == 0:
+        lam = np.zeros((1, 3), np.float32)
+    t = C.c_float()
+    ce = cos_ex(25.0) if cosex is None else cosex
+    ok = lib().or_hit(o.ctypes.data, d.ctypes.data, p.ctypes.data, n.ctypes.data, float(r),
+                      lam.ctypes.data, nl, float(tau), float(ce), C.byref(t))
+    return t.value if ok else None
+
+
+def reflect(d, n):
+    d, n = _f32(d, (3,)), _f32(n, (3,))
+    out = np.zeros(3, np.float32)
+    lib().or_reflect(d.ctypes.data, n.ctypes.data, out.ctypes.data)
+    return out
+
+
+def nearest(scene: OracleScene, o, d, lam=(), prev=-1, tau=0.0015, cosex=None):
+    o, d = _f32(o, (3,)), _f32(d, (3,))
+    lama = np.ascontiguousarray(np.asarray(lam, np.float32).reshape(-1, 3))
+    nl = lama.shape[0]
+    if nl == 0:
+        lama = np.zeros((1, 3), np.float32)
+    t = C.c_float()
+    ce = cos_ex(25.0) if cosex is None else cosex
+    s = lib().or_nearest(C.byref(scene.c), o.ctypes.data, d.ctypes.data, lama.ctypes.data,
+                         nl, int(prev), float(tau), float(ce),
+                         C.byref(t))
+    return int(s), float(t.value)
+
+
+_FORK = {}
+
+
+def _primary_worker(args):
+    rank, world = args
+    case, max_diff = _FORK["case"], _FORK["max_diff"]
+    sc = OracleScene(case.scene)
+    p, rxa = _params(case, max_diff=max_diff)
+    p.rank, p.world = rank, world
+    rc, ec = 1 << 16, 1 << 16
+    while True:
+        raw = np.zeros(rc, COARSE_DTYPE)
+        ev = np.zeros(ec, EVENT_DTYPE)
+        nr, ne, nb = C.c_int64(), C.c_int64(), C.c_uint64()
+        lib().or_trace_primary(C.byref(sc.c), C.byref(p), raw.ctypes.data, rc, C.byref(nr),
+                               ev.ctypes.data, ec, C.byref(ne), C.byref(nb))
+        if nr.value <= rc and ne.value <= ec:
+            return raw[:nr.value].copy(), ev[:ne.value].copy(), int(nb.value)
+        rc, ec = max(rc, nr.value), max(ec, ne.value)
+
+
+def _fan_worker(args):
+    part, parts = args
+    case, max_diff, ev = _FORK["case"], _FORK["max_diff"], _FORK["events"]
+    sc = OracleScene(case.scene)
+    p, rxa = _params(case, max_diff=max_diff)
+    rc = 1 << 16
+    while True:
+        raw = np.zeros(rc, COARSE_DTYPE)
+        nr, nb = C.c_int64(), C.c_uint64()
+        lib().or_trace_fans(C.byref(sc.c), C.byref(p), ev.ctypes.data, ev.shape[0], part, parts,
+                            raw.ctypes.data, rc, C.byref(nr), C.byref(nb))
+        if nr.value <= rc:
+            return raw[:nr.value].copy(), int(nb.value)
+        rc = nr.value
+
+
+def event_dedupe(ev):
+    a = np.ascontiguousarray(ev.copy())
+    m = lib().or_event_dedupe(a.ctypes.data, a.shape[0])
+    return a[:m].copy()
+
+
+def launch_phased(case, procs=1, max_diff=None, return_events=False):
+    """The same coarse operation run in phases over `procs` forked single-threaded
+    processes (ray shards, then event shards); the merged set is identical (per-ray
+    results are independent; the event set is global).  Returns (records, n_raw, bounces)."""
+    import multiprocessing as mp
+    lib()
+    _FORK["case"], _FORK["max_diff"] = case, max_diff
+    ctx = mp.get_context("fork")
+    if procs > 1:
+        with ctx.Pool(procs) as pool:
+            parts = pool.map(_primary_worker, [(r, procs) for r in range(procs)])
+    else:
+        parts = [_primary_worker((0, 1))]
+    raw = np.concatenate([x[0] for x in parts])
+    ev = event_dedupe(np.concatenate([x[1] for x in parts]))
+    nb = sum(x[2] for x in parts)
+    _FORK["events"] = ev
+    if ev.shape[0]:
+        if procs > 1:
+            with ctx.Pool(procs) as pool:
+                fparts = pool.map(_fan_worker, [(r, procs) for r in range(procs)])
+        else:
+            fparts = [_fan_worker((0, 1))]
+        raw = np.concatenate([raw] + [x[0] for x in fparts])
+        nb += sum(x[1] for x in fparts)
+    recs = dedupe(raw, case.kappa)
+    if return_events:
+        return recs, raw.shape[0], nb, ev
+    return recs, raw.shape[0], nb
+
+
+def launch(case, scene: OracleScene | None = None, raw_cap=1 << 20, max_diff=None):
+    """The coarse operation (C.1): returns (deduped records, n_raw, n_bounces)."""
+    sc = scene or OracleScene(case.scene)
+    p, rxa = _params(case, max_diff=max_diff)
+    while True:
+        raw = np.zeros(raw_cap, COARSE_DTYPE)
+        out = np.zeros(raw_cap, COARSE_DTYPE)
+        n_raw, n_out, nb = C.c_int64(), C.c_int64(), C.c_uint64()
+        st = lib().or_launch(C.byref(sc.c), C.byref(p), raw.ctypes.data, raw_cap, C.byref(n_raw),
+                             out.ctypes.data, raw_cap, C.byref(n_out), C.byref(nb))
+        if st == 0:
+            return out[:n_out.value].copy(), int(n_raw.value), int(nb.value)
+        raw_cap = int(n_raw.value) + 1
+
+
+def trace_rays(case, ray_ids, scene: OracleScene | None = None, raw_cap=1 << 16):
+    """Primary rays only (no fans): raw records, per-segment hit ids, bounce count."""
+    sc = scene or OracleScene(case.scene)
+    p, rxa = _params(case)
+    ids = np.ascontiguousarray(ray_ids, dtype=np.uint64)
+    nseg = case.max_refl + 1
+    while True:
+        raw = np.zeros(raw_cap, COARSE_DTYPE)
+        hits = np.zeros((ids.shape[0], nseg), np.int64)
+        n_raw, nb = C.c_int64(), C.c_uint64()
+        st = lib().or_trace_rays(C.byref(sc.c), C.byref(p), ids.ctypes.data, ids.shape[0],
+                                 raw.ctypes.data, raw_cap, C.byref(n_raw), hits.ctypes.data,
+                                 C.byref(nb))
+        if st == 0:
+            return raw[:n_raw.value].copy(), hits, int(nb.value)
+        raw_cap = int(n_raw.value) + 1
+
+
+def dedupe(recs: np.ndarray, kappa: int = 1) -> np.ndarray:
+    a = np.ascontiguousarray(recs.copy())
+    m = lib().or_dedupe(a.ctypes.data, a.shape[0], int(kappa))
+    return a[:m].copy()
+
+
+def make_edge(a, b, t0, n0, n1, n_exp=1.5, label=100):
+    e = _Edge()
+    e.a[:] = [float(x) for x in a]
+    e.b[:] = [float(x) for x in b]
+    e.t0[:] = [float(x) for x in t0]
+    e.n0[:] = [float(x) for x in n0]
+    e.n1[:] = [float(x) for x in n1]
+    e.n_exp = float(n_exp)
+    e.label = int(label)
+    return e
+
+
+def edge_closest(o, d, edge):
+    o, d = _f32(o, (3,)), _f32(d, (3,))
+    te, s, d2 = C.c_float(), C.c_float(), C.c_float()
+    ok = lib().or_edge_closest(o.ctypes.data, d.ctypes.data, C.byref(edge), C.byref(te),
+                               C.byref(s), C.byref(d2))
+    return (te.value, s.value, d2.value) if ok else None
+
+
+def fan_dirs(edge, d, dphi_deg=2.5):
+    d = _f32(d, (3,))
+    out = np.zeros((512, 3), np.float32)
+    M = lib().or_fan_dirs(C.byref(edge), d.ctypes.data, float(dphi_deg), out.ctypes.data, 512)
+    return out[:M].copy()
