@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""bench.py — one JSON line for the driver (see DESIGN.md §7 "Measurement").
+
+Step = one pass of the whole hot path over the workload (BASELINE.json configs[1], "C2": SR
+room, 1e6 surfels, sigma = 10 mm, 1 TX / 1 RX, 1e6 rays, <= 3 reflections + 1 diffraction):
+  A1 scene build -> A2-A7 launch (primary rays, events, Keller fans) -> A8 dedupe
+  -> A9-A10 refinement (when built).
+Multi-GPU (torchrun): scene replicated, rays i == rank (mod N), NCCL all-gather of events and of
+coarse records, global merge on every rank, refinement sharded by path.
+
+`value` = ray-bounces per second of the whole job (device time, inputs resident in HBM).
+`--impl reference` times the CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ray-bounces/sec and refined paths/sec at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "ray-bounces/s"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def peaks():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.path = os.path.join("/tmp", f"nrt_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def allgather_bytes(t, world):
+    """All-gather variable-length uint8 cuda tensors (count exchange, then padded gather)."""
+    import torch
+    import torch.distributed as dist
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n)
+    ns = [int(x.item()) for x in ns]
+    m = max(ns) if ns else 0
+    if m == 0:
+        return torch.zeros(0, dtype=torch.uint8, device=t.device)
+    pad = torch.zeros(m, dtype=torch.uint8, device=t.device)
+    pad[: t.numel()] = t
+    out = torch.zeros(world * m, dtype=torch.uint8, device=t.device)
+    dist.all_gather_into_tensor(out, pad)
+    return torch.cat([out[r * m: r * m + ns[r]] for r in range(world)])
+
+
+class Runner:
+    """One hot-path step on this rank, device-resident inputs."""
+
+    def __init__(self, N, case, world, rank, stream, refine_on):
+        import torch
+        self.N, self.case, self.world, self.rank, self.stream = N, case, world, rank, stream
+        s = case.scene
+        dev = torch.device("cuda", torch.cuda.current_device())
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        self.pts, self.nrm, self.rad, self.lab = t(s.points), t(s.normals), t(s.radii), t(s.labels)
+        self.tx = t(case.tx)
+        self.rx = t(case.rx.reshape(-1, 3))
+        self.refine_on = refine_on
+        self.desc = dict(kappa=case.kappa, tau=case.tau, c_R=case.c_R, dphi_deg=case.dphi_deg,
+                         theta_ex_deg=case.theta_ex_deg, edge_bin=case.edge_bin)
+
+    def step(self, counters=0):
+        N, c = self.N, self.case
+        sc = N.nrt_scene_build_ex(self.pts, self.nrm, c.voxel, radii=self.rad, labels=self.lab,
+                                  edges=c.scene.edges, stream=self.stream)
+        if self.world == 1:
+            coarse = N.nrt_launch_ex(sc, self.tx, self.rx, c.n_rays, c.max_refl, c.max_diff,
+                                     counters=counters, stream=self.stream, **self.desc)
+            merged = coarse
+            parts = [coarse]
+        else:
+            import torch
+            has_diff = c.max_diff > 0 and len(c.scene.edges) > 0
+            coarse = N.nrt_launch_ex(sc, self.tx, self.rx, c.n_rays, c.max_refl, c.max_diff,
+                                     rank=self.rank, world=self.world, stage=1 if has_diff else 0,
+                                     counters=counters, stream=self.stream, **self.desc)
+            if has_diff:
+                ev = torch.from_numpy(coarse.export_events().view(np.uint8)).cuda()
+                evall = allgather_bytes(ev, self.world)
+                N.nrt_launch_fans(sc, coarse, evall, rank=self.rank, world=self.world,
+                                  stream=self.stream, **self.desc)
+            rs = coarse.record_size()
+            buf = torch.zeros(coarse.count() * rs, dtype=torch.uint8, device="cuda")
+            coarse.export(buf)
+            allr = allgather_bytes(buf, self.world)
+            merged = N.nrt_paths_import(allr, N.PATHS_COARSE, c.tx, c.rx)
+            merged = N.nrt_paths_merge([merged], c.kappa)
+            parts = [coarse]
+        refined = None
+        if self.refine_on:
+            refined = N.nrt_refine_ex(sc, merged, xi=c.xi, r_s=c.r_s, tau=c.tau + 0.0,
+                                      rank=self.rank, world=self.world, stream=self.stream)
+        infos = [p.info() for p in parts]
+        out = {
+            "bounces": sum(i["bounces"] for i in infos),
+            "coarse": merged.count(),
+            "refined": refined.count() if refined is not None else 0,
+            "ms_trace": sum(i["ms_trace"] for i in infos),
+            "ms_fans": sum(i["ms_fans"] for i in infos),
+            "tests": sum(i["surfel_tests"] for i in infos),
+            "cells": sum(i["cells_visited"] for i in infos),
+            "nonempty": sum(i["cells_nonempty"] for i in infos),
+            "n_events": infos[0]["n_events"],
+            "n_fan_rays": infos[0]["n_fan_rays"],
+            "scene": sc.info(),
+            "refined_info": refined.info() if refined is not None else None,
+        }
+        return out
+
+
+def e2e_step(N, case, host, stream, refine_on):
+    """The public API with HOST buffers: H2D of the cloud inside the build, D2H of results."""
+    sc = N.nrt_scene_build_ex(host["p"], host["n"], case.voxel, radii=host["r"],
+                              labels=host["l"], edges=case.scene.edges, stream=stream)
+    coarse = N.launch_case(sc, case, stream=stream)
+    rec = coarse.export()
+    out_b = rec.nbytes
+    if refine_on:
+        ref = N.nrt_refine_ex(sc, coarse, xi=case.xi, r_s=case.r_s, tau=case.tau, stream=stream)
+        out_b += ref.export().nbytes
+    return coarse.info()["bounces"], out_b
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_baseline(case, seconds=15.0):
+    """The oracle as it stands, on this host's cores (processes over a ray sample)."""
+    import multiprocessing as mp
+    from oracle import oracle as O
+    O.lib()
+    P = os.cpu_count() or 1
+    # calibrate: rays per second per core on a handful of rays
+    ids = np.arange(0, case.n_rays, max(1, case.n_rays // 997), dtype=np.uint64)
+    t0 = time.perf_counter()
+    _, _, nb = O.trace_rays(case, ids[:2])
+    dt = max(1e-3, time.perf_counter() - t0)
+    per_ray = dt / 2
+    n_per = max(1, int(seconds / per_ray))
+    sample = np.linspace(0, case.n_rays - 1, n_per * P).astype(np.uint64)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(P) as pool:
+        res = pool.map(_oracle_chunk, [(case, sample[k::P]) for k in range(P)])
+    wall = time.perf_counter() - t0
+    bounces = sum(r for r in res)
+    return {"value": bounces / wall, "unit": UNIT, "cores": P, "kind": "oracle",
+            "sample": f"{len(sample)} primary rays of {case.name} (evenly spaced lattice ids, "
+                      f"brute force over {case.scene.n} surfels, no fans), {wall:.1f} s wall on "
+                      f"{P} processes"}
+
+
+def _oracle_chunk(args):
+    case, ids = args
+    from oracle import oracle as O
+    _, _, nb = O.trace_rays(case, ids)
+    return nb
+
+
+def run_reference(args, case):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.lib()
+    import multiprocessing as mp
+    P = os.cpu_count() or 1
+    rays_per_step = 8 * P
+    times, bounces = [], []
+    ctx = mp.get_context("fork")
+    with ctx.Pool(P) as pool:
+        for k in range(args.warmup + args.steps):
+            sample = (np.arange(rays_per_step, dtype=np.uint64) * (case.n_rays // rays_per_step)
+                      + k).astype(np.uint64)
+            t0 = time.perf_counter()
+            res = pool.map(_oracle_chunk, [(case, sample[j::P]) for j in range(P)])
+            dt = time.perf_counter() - t0
+            if k >= args.warmup:
+                times.append(dt)
+                bounces.append(sum(res))
+    value = sum(bounces) / sum(times)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": case.name, "sample": f"{rays_per_step} primary rays per step"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "oracle",
+                             "sample": f"{rays_per_step} primary rays per step of {case.name}, "
+                                       f"brute force over {case.scene.n} surfels"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="nrt", choices=["nrt", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--sigma", type=float, default=0.010)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    import nrt_gen as G
+    case = G.case(args.config, sigma=args.sigma) if args.config.startswith("C2") else G.case(args.config)
+    if args.impl == "reference":
+        run_reference(args, case)
+        return
+
+    import torch
+    import paper_2403_06648_b200 as N
+    N.lib()
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    refine_on = False
+    try:
+        refine_on = os.environ.get("NRT_BENCH_REFINE", "1") == "1" and N_has_refine(N)
+    except Exception:
+        refine_on = False
+    R = Runner(N, case, world, rank, stream, refine_on)
+
+    for _ in range(args.warmup):
+        R.step()
+    torch.cuda.synchronize()
+    cnt = R.step(counters=1)  # instrumented (untimed): algorithmic byte counts
+    torch.cuda.synchronize()
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    outs = []
+    launches0 = N.nrt_kernel_launches()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))          # L2 flush between steps (outside the event pair)
+            ev[k][0].record(stream)
+            outs.append(R.step())
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches = (N.nrt_kernel_launches() - launches0) / args.steps
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    bounces = outs[-1]["bounces"]
+    refined = outs[-1]["refined"]
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms, float(bounces)], dtype=torch.float64, device="cuda")
+        tl = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(tl, t)
+        total_ms = max(float(x[0]) for x in tl)
+        bounces = sum(int(x[1]) for x in tl)
+    value = bounces * args.steps / (total_ms / 1000.0)
+
+    # ---- roofline of the dominant kernel (primary traversal k_primary)
+    hbm, src = peaks()
+    prim_bytes = 32 * cnt["tests"] + 8 * cnt["cells"]
+    ms_trace = statistics.mean(o["ms_trace"] for o in outs)
+    ms_fans = statistics.mean(o["ms_fans"] for o in outs)
+    # counters cover primary + fans together; split by kernel time share is not exact, so the
+    # primary kernel's bytes come from a primary-only instrumented launch below
+    prim_only = prim_counts(N, R, case)
+    pb = 32 * prim_only["tests"] + 8 * prim_only["cells"]
+    achieved = pb / (ms_trace / 1000.0) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "kernel": "k_primary",
+            "peak_source": src,
+            "bytes_per_launch": pb, "bytes_per_bounce": pb / max(1, prim_only["bounces"]),
+            "ms_per_launch": ms_trace}
+
+    # ---- e2e through the public API with host (pinned) buffers
+    e2e = None
+    if not args.no_e2e and world == 1:
+        s = case.scene
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        host = {"p": pin(s.points), "n": pin(s.normals), "r": pin(s.radii), "l": pin(s.labels)}
+        h2d = sum(v.nbytes for v in host.values()) + case.rx.nbytes + case.tx.nbytes
+        e2e_step(N, case, host, stream, refine_on)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tot_b, d2h = 0, 0
+        for _ in range(args.steps):
+            b, ob = e2e_step(N, case, host, stream, refine_on)
+            tot_b += b
+            d2h = ob
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        e2e = {"value": tot_b / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000 * dt / args.steps}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{case.name}: SR room {case.scene.n} surfels sigma={args.sigma} m, "
+                               f"1 TX/{len(case.rx)} RX, {case.n_rays} rays/GPU-shard-set, "
+                               f"max_refl {case.max_refl}, max_diff {case.max_diff}",
+                   "voxel_m": case.voxel, "n_rays": case.n_rays, "l2": "512 MiB write between steps",
+                   "parallelism": f"dp{world} (rays i == rank mod {world})"},
+        "refined_paths_per_s": (refined * args.steps / (total_ms / 1000.0)) if refine_on else None,
+        "coarse_paths": outs[-1]["coarse"], "refined_paths": refined,
+        "breakdown_ms": {"trace": ms_trace, "fans": ms_fans,
+                         "refine": (outs[-1]["refined_info"] or {}).get("ms_refine")},
+        "n_events": outs[-1]["n_events"], "n_fan_rays": outs[-1]["n_fan_rays"],
+        "bounces_per_step": bounces,
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(case)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def N_has_refine(N):
+    return os.path.exists(os.path.join(ROOT, "paper_2403_06648_b200", "REFINE_READY"))
+
+
+def prim_counts(N, R, case):
+    """Instrumented primary-only launch (stage 1: no fans) for the k_primary byte count."""
+    sc = N.nrt_scene_build_ex(R.pts, R.nrm, case.voxel, radii=R.rad, labels=R.lab,
+                              edges=case.scene.edges, stream=R.stream)
+    p = N.nrt_launch_ex(sc, R.tx, R.rx, case.n_rays, case.max_refl, case.max_diff, counters=1,
+                        stage=1, rank=R.rank, world=R.world, stream=R.stream, **R.desc)
+    i = p.info()
+    return {"tests": i["surfel_tests"], "cells": i["cells_visited"], "bounces": i["bounces"]}
+
+
+if __name__ == "__main__":
+    main()

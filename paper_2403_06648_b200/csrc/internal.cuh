@@ -1,0 +1,186 @@
+// internal.cuh — shared internals of libnrt (CUDA path).  Independent of oracle/.
+//
+// Compiled with -fmad=false (no FMA contraction) and IEEE div/sqrt so that every FP32
+// quantity on the coarse path is the exact value the definition (DESIGN.md §2 R1-R17)
+// prescribes, whatever the grid or launch configuration.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/nrt.h"
+
+namespace nrt {
+
+// ------------------------------------------------------------------------------------
+// error plumbing
+// ------------------------------------------------------------------------------------
+nrt_status set_error(nrt_status st, const char* fmt, ...);
+void clear_error();
+void count_launch();  // every kernel launch of the library increments a process-wide counter
+
+#define NRT_CUDA(call)                                                                    \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            return ::nrt::set_error(e_ == cudaErrorMemoryAllocation ? NRT_E_NOMEM         \
+                                                                    : NRT_E_CUDA,         \
+                                    "%s:%d %s: %s", __FILE__, __LINE__, #call,            \
+                                    cudaGetErrorString(e_));                              \
+        }                                                                                 \
+    } while (0)
+
+#define NRT_TRY(call)                                                                     \
+    do {                                                                                  \
+        nrt_status s_ = (call);                                                           \
+        if (s_ != NRT_OK) return s_;                                                      \
+    } while (0)
+
+// ------------------------------------------------------------------------------------
+// R2: FP64 sincos, pi/2 Cody-Waite (2 parts) + minimax kernels, fixed order, no FMA.
+// Used on the device (ray generation, fan angles) and on the host (cos theta_ex).
+// ------------------------------------------------------------------------------------
+__host__ __device__ inline double k_sin(double x) {
+    const double S1 = -1.66666666666666324348e-01, S2 = 8.33333333332248946124e-03,
+                 S3 = -1.98412698298579493134e-04, S4 = 2.75573137070700676789e-06,
+                 S5 = -2.50507602534068634195e-08, S6 = 1.58969099521155010221e-10;
+    double z = x * x;
+    double v = z * x;
+    double r = S2 + z * (S3 + z * (S4 + z * (S5 + z * S6)));
+    return x + v * (S1 + z * r);
+}
+__host__ __device__ inline double k_cos(double x) {
+    const double C1 = 4.16666666666666019037e-02, C2 = -1.38888888888741095749e-03,
+                 C3 = 2.48015872894767294178e-05, C4 = -2.75573143513906633035e-07,
+                 C5 = 2.08757232129817482790e-09, C6 = -1.13596475577881948265e-11;
+    double z = x * x;
+    double r = z * (C1 + z * (C2 + z * (C3 + z * (C4 + z * (C5 + z * C6)))));
+    return 1.0 - (0.5 * z - z * r);
+}
+constexpr double kPi = 3.14159265358979311600e+00;
+__host__ __device__ inline void nrt_sincos(double x, double* s, double* c) {
+    const double PIO2_1 = 1.57079632673412561417e+00, PIO2_1T = 6.07710050650619224932e-11,
+                 INVPIO2 = 6.36619772367581382433e-01;
+    double kf = floor(x * INVPIO2 + 0.5);
+    double y = (x - kf * PIO2_1) - kf * PIO2_1T;
+    long long k = (long long)kf;
+    double sy = k_sin(y), cy = k_cos(y);
+    switch (k & 3) {
+        case 0: *s = sy; *c = cy; break;
+        case 1: *s = cy; *c = -sy; break;
+        case 2: *s = -sy; *c = -cy; break;
+        default: *s = -cy; *c = sy; break;
+    }
+}
+
+// R1: spherical Fibonacci lattice direction i of n (FP64, rounded to f32, not renormalised)
+__host__ __device__ inline float3 fib_dir(uint64_t i, uint64_t n) {
+    const double g = 0.3819660112501051;
+    double z = 1.0 - (2.0 * (double)i + 1.0) / (double)n;
+    double x = (double)i * g;
+    double fr = x - floor(x);
+    double phi = (2.0 * kPi) * fr;
+    double s, c;
+    nrt_sincos(phi, &s, &c);
+    double rr = sqrt(1.0 - z * z);
+    return make_float3((float)(rr * c), (float)(rr * s), (float)z);
+}
+
+__host__ __device__ inline float dot3(float3 a, float3 b) {
+    return (a.x * b.x + a.y * b.y) + a.z * b.z;
+}
+
+// ------------------------------------------------------------------------------------
+// device-side tables
+// ------------------------------------------------------------------------------------
+struct DevEdge {
+    float a[3], e[3], len;
+    float t0[3], n0[3], n1[3];
+    float n_exp;
+    int32_t label;
+};
+
+struct Hist {
+    int32_t n, n_diff;
+    uint32_t kinds;
+    int32_t label[NRT_MAX_INT];
+    uint32_t prim[NRT_MAX_INT];
+    float v[NRT_MAX_INT][3];
+    float s_edge;
+};
+
+}  // namespace nrt
+
+// ------------------------------------------------------------------------------------
+// handles
+// ------------------------------------------------------------------------------------
+struct nrt_scene_s {
+    int device = 0;
+    int64_t n = 0, nref = 0, ncell = 0;
+    int dims[3] = {0, 0, 0};
+    float org[3] = {0, 0, 0};
+    float v = 0, inv_v = 0, pad = 0, r_max = 0;
+    uint2* cell = nullptr;     // [ncell] (start, end) into rec
+    float4* rec = nullptr;     // [2*nref] AoS: (p, r^2), (n, id bits)
+    float4* sp = nullptr;      // [n] (p, r)
+    float4* sn = nullptr;      // [n] (n, label bits)
+    int32_t* label = nullptr;  // [n]
+    nrt::DevEdge* edges = nullptr;
+    int n_edges = 0;
+    std::vector<nrt::DevEdge> h_edges;
+};
+
+struct nrt_paths_s {
+    int kind = NRT_PATHS_COARSE;
+    int device = 0;
+    int64_t n = 0;
+    void* d_rec = nullptr;  // device records
+    int64_t n_ev = 0;
+    void* d_ev = nullptr;   // stage-1 events (nrt_event_rec, deduped locally, key order)
+    float tx[3] = {0, 0, 0};
+    std::vector<float> rx;
+    nrt_paths_info info{};
+    // launch parameters (for stage-2 fans)
+    int64_t n_rays = 0;
+    int32_t max_refl = 0, max_diff = 0;
+};
+
+namespace nrt {
+// scene.cu
+nrt_status scene_build(const nrt_scene_desc* d, nrt_scene* out);
+// dedupe.cu
+nrt_status dedupe_coarse(const nrt_coarse_rec* in, int64_t n, int32_t kappa, nrt_coarse_rec* out,
+                         int64_t* n_out, cudaStream_t st);
+nrt_status dedupe_events(const nrt_event_rec* in, int64_t n, nrt_event_rec* out, int64_t* n_out,
+                         cudaStream_t st);
+nrt_status dedupe_refined(const nrt_refined_rec* in, int64_t n, nrt_refined_rec* out,
+                          int64_t* n_out, cudaStream_t st);
+// launch.cu
+struct LaunchArgs {
+    float tx[3];
+    const float* d_rx;  // device
+    int32_t n_rx;
+    int64_t n_rays;
+    int32_t max_refl, max_diff;
+    nrt_launch_desc desc;
+};
+struct KernelStats {
+    float ms_kernel = 0;  // device time of the traversal kernel alone
+    unsigned long long tests = 0, cells = 0, nonempty = 0;  // counters build only
+};
+nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw, int64_t* n_raw,
+                          nrt_event_rec** ev, int64_t* n_ev, uint64_t* bounces, KernelStats* ks,
+                          cudaStream_t st);
+nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev, int64_t n_ev,
+                       nrt_coarse_rec** raw, int64_t* n_raw, int64_t* n_fan_rays,
+                       uint64_t* bounces, KernelStats* ks, cudaStream_t st);
+nrt_status debug_trace(nrt_scene s, const LaunchArgs& a, const uint64_t* ids, int64_t n,
+                       int64_t* hit_ids, cudaStream_t st);
+float cos_ex_of(float theta_deg);
+float cRw_of(float c_R, int64_t n_rays);
+// refine.cu
+nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
+                  cudaStream_t st);
+}  // namespace nrt

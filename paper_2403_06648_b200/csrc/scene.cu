@@ -1,0 +1,433 @@
+// scene.cu — A1: GPU voxelisation of the oriented-surfel cloud.
+//
+// The paper forms a three-level voxel/subvoxel/AABB hierarchy for OptiX; B200
+// has no RT cores, so the B200 build is one uniform fine grid walked by a 3D-DDA:
+//   1. validate + pack surfels (p, r), (n, label); bounds by block reduction;
+//   2. per surfel, the exact disk AABB half extent r*sqrt(1 - n_a^2/|n|^2) + pad gives the
+//      overlapped cell box; counts -> CUB exclusive scan -> (Morton u64, id u32) pairs;
+//   3. CUB radix sort by Morton code (stable: ids ascend within a cell);
+//   4. records duplicated per cell, AoS 32 B {p, r^2 | n, id} in Morton order, plus a
+//      dense (start, end) table indexed by the linear cell index (8 B per cell).
+// Registering a surfel in every cell its padded AABB overlaps is what makes the DDA's
+// nearest hit equal the brute-force global argmin.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstring>
+
+#include "internal.cuh"
+
+namespace nrt {
+
+namespace {
+
+__device__ __forceinline__ unsigned int f2ord(float f) {
+    unsigned int u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ inline float ord2f(unsigned int u) {
+    unsigned int b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+    float f;
+    memcpy(&f, &b, 4);
+    return f;
+}
+
+struct BuildIn {
+    const float* p;
+    const float* n;
+    const float* r;
+    float radius;
+    const int32_t* label;
+    int64_t count;
+};
+
+// validate + pack; bounds (ordered-int atomics); first bad index (atomicMin)
+__global__ void k_pack(BuildIn in, float4* sp, float4* sn, unsigned int* bounds,
+                       unsigned long long* bad, int* bad_kind, unsigned int* rmax) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    float rm = 0.0f;
+    if (i < in.count) {
+        float px = in.p[3 * i], py = in.p[3 * i + 1], pz = in.p[3 * i + 2];
+        float nx = in.n[3 * i], ny = in.n[3 * i + 1], nz = in.n[3 * i + 2];
+        float r = in.r ? in.r[i] : in.radius;
+        int32_t lab = in.label ? in.label[i] : 0;
+        int kind = 0;
+        if (!(isfinite(px) && isfinite(py) && isfinite(pz))) kind = 1;
+        float nn = sqrtf((nx * nx + ny * ny) + nz * nz);
+        if (!kind && !(fabsf(nn - 1.0f) <= 1e-3f)) kind = 2;
+        if (!kind && !(r > 0.0f && isfinite(r))) kind = 3;
+        if (!kind && (lab < 0 || lab >= 4096)) kind = 4;
+        if (kind) {
+            unsigned long long old = atomicMin(bad, (unsigned long long)i);
+            if ((unsigned long long)i < old) atomicExch(bad_kind, kind);
+        }
+        sp[i] = make_float4(px, py, pz, r);
+        sn[i] = make_float4(nx, ny, nz, __int_as_float(lab));
+        mn[0] = mx[0] = px;
+        mn[1] = mx[1] = py;
+        mn[2] = mx[2] = pz;
+        rm = r;
+    }
+    typedef cub::BlockReduce<float, 256> BR;
+    __shared__ typename BR::TempStorage tmp;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float v = BR(tmp).Reduce(mn[a], cub::Min());
+        if (threadIdx.x == 0) atomicMin(&bounds[a], f2ord(v));
+        __syncthreads();
+        v = BR(tmp).Reduce(mx[a], cub::Max());
+        if (threadIdx.x == 0) atomicMax(&bounds[3 + a], f2ord(v));
+        __syncthreads();
+    }
+    float v = BR(tmp).Reduce(rm, cub::Max());
+    if (threadIdx.x == 0) atomicMax(rmax, __float_as_uint(v));
+}
+
+// R6: pseudo-label = linear index of the 0.5 m cell of p relative to the bounds minimum
+__global__ void k_pseudo_label(float4* sn, const float4* sp, int64_t n, float bx, float by,
+                               float bz, int lx, int ly, unsigned long long* bad) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 p = sp[i];
+    int ix = (int)floorf((p.x - bx) / 0.5f), iy = (int)floorf((p.y - by) / 0.5f),
+        iz = (int)floorf((p.z - bz) / 0.5f);
+    long long lab = (long long)ix + (long long)lx * ((long long)iy + (long long)ly * iz);
+    if (lab < 0 || lab >= 4096) atomicMin(bad, (unsigned long long)i);
+    sn[i].w = __int_as_float((int)lab);
+}
+
+struct Grid {
+    float ox, oy, oz, v, inv_v, pad;
+    int nx, ny, nz;
+};
+
+__device__ __forceinline__ void cell_box(const Grid& g, float4 p, float4 n, int lo[3], int hi[3]) {
+    float nn = (n.x * n.x + n.y * n.y) + n.z * n.z;
+    float c[3] = {p.x, p.y, p.z};
+    float o[3] = {g.ox, g.oy, g.oz};
+    float na[3] = {n.x, n.y, n.z};
+    int dim[3] = {g.nx, g.ny, g.nz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float h = p.w * sqrtf(fmaxf(0.0f, 1.0f - (na[a] * na[a]) / nn)) * 1.0001f + g.pad;
+        int l = (int)floorf((c[a] - h - o[a]) * g.inv_v);
+        int u = (int)floorf((c[a] + h - o[a]) * g.inv_v);
+        lo[a] = max(0, min(dim[a] - 1, l));
+        hi[a] = max(0, min(dim[a] - 1, u));
+    }
+}
+
+__global__ void k_count(Grid g, const float4* sp, const float4* sn, int64_t n, unsigned int* cnt) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int lo[3], hi[3];
+    cell_box(g, sp[i], sn[i], lo, hi);
+    cnt[i] = (unsigned)((hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1));
+}
+
+__device__ __forceinline__ uint64_t spread3(uint64_t x) {
+    x &= 0x1fffff;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+__device__ __forceinline__ uint64_t morton3(int x, int y, int z) {
+    return spread3(x) | (spread3(y) << 1) | (spread3(z) << 2);
+}
+__device__ __forceinline__ int compact3(uint64_t x) {
+    x &= 0x1249249249249249ull;
+    x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ull;
+    x = (x ^ (x >> 4)) & 0x100f00f00f00f00full;
+    x = (x ^ (x >> 8)) & 0x1f0000ff0000ffull;
+    x = (x ^ (x >> 16)) & 0x1f00000000ffffull;
+    x = (x ^ (x >> 32)) & 0x1fffffull;
+    return (int)x;
+}
+
+__global__ void k_emit(Grid g, const float4* sp, const float4* sn, int64_t n,
+                       const unsigned int* off, uint64_t* keys, unsigned int* vals) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int lo[3], hi[3];
+    cell_box(g, sp[i], sn[i], lo, hi);
+    unsigned int k = off[i];
+    for (int z = lo[2]; z <= hi[2]; ++z)
+        for (int y = lo[1]; y <= hi[1]; ++y)
+            for (int x = lo[0]; x <= hi[0]; ++x) {
+                keys[k] = morton3(x, y, z);
+                vals[k] = (unsigned)i;
+                ++k;
+            }
+}
+
+__global__ void k_records(Grid g, const uint64_t* keys, const unsigned int* ids, int64_t nref,
+                          const float4* sp, const float4* sn, float4* rec, uint2* cell) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nref) return;
+    unsigned id = ids[k];
+    float4 p = sp[id], nv = sn[id];
+    rec[2 * k] = make_float4(p.x, p.y, p.z, p.w * p.w);
+    rec[2 * k + 1] = make_float4(nv.x, nv.y, nv.z, __uint_as_float(id));
+    uint64_t key = keys[k];
+    bool first = (k == 0) || keys[k - 1] != key;
+    bool last = (k == nref - 1) || keys[k + 1] != key;
+    if (first || last) {
+        int x = compact3(key), y = compact3(key >> 1), z = compact3(key >> 2);
+        int64_t lin = (int64_t)x + (int64_t)g.nx * ((int64_t)y + (int64_t)g.ny * z);
+        if (first) cell[lin].x = (unsigned)k;
+        if (last) cell[lin].y = (unsigned)(k + 1);
+    }
+}
+
+template <class T>
+nrt_status dmalloc(T** p, size_t count, cudaStream_t st) {
+    if (count == 0) count = 1;
+    NRT_CUDA(cudaMallocAsync((void**)p, count * sizeof(T), st));
+    return NRT_OK;
+}
+
+}  // namespace
+
+static nrt_status build_impl(const nrt_scene_desc* D, nrt_scene S, cudaStream_t st) {
+    const int64_t n = D->n;
+    const unsigned nb = (unsigned)((n + 255) / 256);
+    // ---- stage inputs on the device
+    const float *dp = D->points, *dn = D->normals, *dr = D->radii;
+    const int32_t* dl = D->labels;
+    float *tp = nullptr, *tn = nullptr, *tr = nullptr;
+    int32_t* tl = nullptr;
+    if (D->mem == NRT_MEM_HOST) {
+        NRT_TRY(dmalloc(&tp, 3 * n, st));
+        NRT_TRY(dmalloc(&tn, 3 * n, st));
+        NRT_CUDA(cudaMemcpyAsync(tp, D->points, 12 * n, cudaMemcpyHostToDevice, st));
+        NRT_CUDA(cudaMemcpyAsync(tn, D->normals, 12 * n, cudaMemcpyHostToDevice, st));
+        dp = tp;
+        dn = tn;
+        if (D->radii) {
+            NRT_TRY(dmalloc(&tr, n, st));
+            NRT_CUDA(cudaMemcpyAsync(tr, D->radii, 4 * n, cudaMemcpyHostToDevice, st));
+            dr = tr;
+        }
+        if (D->labels) {
+            NRT_TRY(dmalloc(&tl, n, st));
+            NRT_CUDA(cudaMemcpyAsync(tl, D->labels, 4 * n, cudaMemcpyHostToDevice, st));
+            dl = tl;
+        }
+    }
+    NRT_TRY(dmalloc(&S->sp, n, st));
+    NRT_TRY(dmalloc(&S->sn, n, st));
+    NRT_TRY(dmalloc(&S->label, n, st));
+    // scratch: bounds[6], rmax, bad, bad_kind
+    struct Scratch {
+        unsigned int bounds[6];
+        unsigned int rmax;
+        int bad_kind;
+        unsigned long long bad;
+    };
+    Scratch h{}, *ds = nullptr;
+    for (int a = 0; a < 3; ++a) {
+        h.bounds[a] = 0xffffffffu;
+        h.bounds[3 + a] = 0u;
+    }
+    h.rmax = 0;
+    h.bad_kind = 0;
+    h.bad = ~0ull;
+    NRT_TRY(dmalloc(&ds, 1, st));
+    NRT_CUDA(cudaMemcpyAsync(ds, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+    BuildIn in{dp, dn, dr, D->radius, dl, n};
+    k_pack<<<nb, 256, 0, st>>>(in, S->sp, S->sn, ds->bounds, &ds->bad, &ds->bad_kind, &ds->rmax); ::nrt::count_launch();
+    NRT_CUDA(cudaGetLastError());
+    NRT_CUDA(cudaMemcpyAsync(&h, ds, sizeof(h), cudaMemcpyDeviceToHost, st));
+    NRT_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(tp, st);
+    cudaFreeAsync(tn, st);
+    cudaFreeAsync(tr, st);
+    cudaFreeAsync(tl, st);
+    if (h.bad != ~0ull) {
+        static const char* what[] = {"", "non-finite position", "normal not unit (|n|-1 > 1e-3)",
+                                     "radius <= 0 or non-finite", "label outside [0,4096)"};
+        cudaFreeAsync(ds, st);
+        return set_error(NRT_E_INVALID, "surfel %llu: %s", h.bad, what[h.bad_kind & 7]);
+    }
+    float bmin[3], bmax[3];
+    for (int a = 0; a < 3; ++a) {
+        bmin[a] = ord2f(h.bounds[a]);
+        bmax[a] = ord2f(h.bounds[3 + a]);
+    }
+    memcpy(&S->r_max, &h.rmax, 4);
+    if (!dl) {  // R6 pseudo-labels
+        int lx = (int)floorf((bmax[0] - bmin[0]) / 0.5f) + 1;
+        int ly = (int)floorf((bmax[1] - bmin[1]) / 0.5f) + 1;
+        h.bad = ~0ull;
+        NRT_CUDA(cudaMemcpyAsync(&ds->bad, &h.bad, 8, cudaMemcpyHostToDevice, st));
+        k_pseudo_label<<<nb, 256, 0, st>>>(S->sn, S->sp, n, bmin[0], bmin[1], bmin[2], lx, ly,
+                                           &ds->bad); ::nrt::count_launch();
+        NRT_CUDA(cudaMemcpyAsync(&h.bad, &ds->bad, 8, cudaMemcpyDeviceToHost, st));
+        NRT_CUDA(cudaStreamSynchronize(st));
+        if (h.bad != ~0ull) {
+            cudaFreeAsync(ds, st);
+            return set_error(NRT_E_INVALID, "pseudo-label of surfel %llu exceeds 4095 (scene too "
+                             "large for 0.5 m pseudo-labels; pass labels)", h.bad);
+        }
+    }
+    cudaFreeAsync(ds, st);
+    // ---- grid: origin = bmin - (ceil(r_max/v) + 1.5) v so every disk lies inside the grid
+    // and axis-aligned walls sit mid-cell; covers bmax + the same margin.
+    const float v = D->voxel_size;
+    Grid g;
+    g.v = v;
+    g.inv_v = 1.0f / v;
+    g.pad = fmaxf(1e-3f * v, 2e-5f);
+    const float margin = (ceilf(S->r_max / v) + 1.5f) * v;
+    g.ox = bmin[0] - margin;
+    g.oy = bmin[1] - margin;
+    g.oz = bmin[2] - margin;
+    float o3[3] = {g.ox, g.oy, g.oz};
+    int dims[3];
+    for (int a = 0; a < 3; ++a) {
+        double ext = ((double)bmax[a] + (double)margin - (double)o3[a]) / v;
+        dims[a] = (int)ceil(ext) + 1;
+        if (dims[a] < 1) dims[a] = 1;
+        if (dims[a] > (1 << 20)) return set_error(NRT_E_INVALID, "grid too large: voxel too small");
+    }
+    g.nx = dims[0];
+    g.ny = dims[1];
+    g.nz = dims[2];
+    const int64_t ncell = (int64_t)dims[0] * dims[1] * dims[2];
+    if (ncell > (int64_t)1 << 31) return set_error(NRT_E_INVALID, "grid has > 2^31 cells");
+    S->ncell = ncell;
+    memcpy(S->dims, dims, sizeof(dims));
+    memcpy(S->org, o3, sizeof(o3));
+    S->v = v;
+    S->inv_v = g.inv_v;
+    S->pad = g.pad;
+    // ---- counts, offsets
+    unsigned int *cnt = nullptr, *off = nullptr;
+    NRT_TRY(dmalloc(&cnt, n + 1, st));
+    NRT_TRY(dmalloc(&off, n + 1, st));
+    k_count<<<nb, 256, 0, st>>>(g, S->sp, S->sn, n, cnt); ::nrt::count_launch();
+    NRT_CUDA(cudaGetLastError());
+    NRT_CUDA(cudaMemsetAsync(cnt + n, 0, 4, st));
+    size_t tb = 0;
+    void* tmp = nullptr;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, n + 1, st);
+    NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, n + 1, st);
+    cudaFreeAsync(tmp, st);
+    unsigned int nref32 = 0;
+    NRT_CUDA(cudaMemcpyAsync(&nref32, off + n, 4, cudaMemcpyDeviceToHost, st));
+    NRT_CUDA(cudaStreamSynchronize(st));
+    const int64_t nref = nref32;
+    S->nref = nref;
+    // ---- pairs, sort
+    uint64_t *k0 = nullptr, *k1 = nullptr;
+    unsigned int *v0 = nullptr, *v1 = nullptr;
+    NRT_TRY(dmalloc(&k0, nref, st));
+    NRT_TRY(dmalloc(&k1, nref, st));
+    NRT_TRY(dmalloc(&v0, nref, st));
+    NRT_TRY(dmalloc(&v1, nref, st));
+    k_emit<<<nb, 256, 0, st>>>(g, S->sp, S->sn, n, off, k0, v0); ::nrt::count_launch();
+    NRT_CUDA(cudaGetLastError());
+    int maxd = dims[0] > dims[1] ? dims[0] : dims[1];
+    maxd = maxd > dims[2] ? maxd : dims[2];
+    int bits = 1;
+    while ((1 << bits) < maxd) ++bits;
+    cub::DoubleBuffer<uint64_t> kb(k0, k1);
+    cub::DoubleBuffer<unsigned int> vb(v0, v1);
+    tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, (int)nref, 0, 3 * bits, st);
+    NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+    cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, (int)nref, 0, 3 * bits, st);
+    cudaFreeAsync(tmp, st);
+    // ---- records + cell table
+    NRT_TRY(dmalloc(&S->rec, 2 * nref, st));
+    NRT_TRY(dmalloc(&S->cell, ncell, st));
+    NRT_CUDA(cudaMemsetAsync(S->cell, 0, ncell * sizeof(uint2), st));
+    k_records<<<(unsigned)((nref + 255) / 256), 256, 0, st>>>(g, kb.Current(), vb.Current(), nref,
+                                                             S->sp, S->sn, S->rec, S->cell); ::nrt::count_launch();
+    NRT_CUDA(cudaGetLastError());
+    cudaFreeAsync(k0, st);
+    cudaFreeAsync(k1, st);
+    cudaFreeAsync(v0, st);
+    cudaFreeAsync(v1, st);
+    cudaFreeAsync(cnt, st);
+    cudaFreeAsync(off, st);
+    // labels array (int) for the history
+    {
+        // sn.w holds the label bits; extract with a tiny kernel-free trick: copy strided
+        NRT_CUDA(cudaMemcpy2DAsync(S->label, 4, (const char*)S->sn + 12, 16, 4, n,
+                                   cudaMemcpyDeviceToDevice, st));
+    }
+    NRT_CUDA(cudaStreamSynchronize(st));
+    return NRT_OK;
+}
+
+nrt_status scene_build(const nrt_scene_desc* D, nrt_scene* out) {
+    if (!D || !out) return set_error(NRT_E_INVALID, "null argument");
+    *out = nullptr;
+    if (D->n <= 0) return set_error(NRT_E_EMPTY, "scene has no points");
+    if (D->n >= ((int64_t)1 << 31)) return set_error(NRT_E_INVALID, "n >= 2^31");
+    if (!D->points || !D->normals) return set_error(NRT_E_INVALID, "points/normals are NULL");
+    if (!(D->voxel_size > 0.0f) || !std::isfinite(D->voxel_size))
+        return set_error(NRT_E_INVALID, "voxel_size must be > 0");
+    if (!D->radii && !(D->radius > 0.0f)) return set_error(NRT_E_INVALID, "radius must be > 0");
+    if (D->n_edges < 0 || (D->n_edges > 0 && !D->edges))
+        return set_error(NRT_E_INVALID, "bad edge array");
+    NRT_CUDA(cudaSetDevice(D->device));
+    cudaStream_t st = (cudaStream_t)D->stream;
+    nrt_scene S = new nrt_scene_s();
+    S->device = D->device;
+    S->n = D->n;
+    // edges (host): validate, precompute e and len with the definition's FP32 formula
+    for (int j = 0; j < D->n_edges; ++j) {
+        const nrt_edge& E = D->edges[j];
+        DevEdge g{};
+        if (!(E.n_exp > 1.0f && E.n_exp < 2.0f)) {
+            delete S;
+            return set_error(NRT_E_INVALID, "edge %d: exterior angle n_exp=%g outside (1,2) "
+                             "(only exterior edges are supported, P:73)", j, (double)E.n_exp);
+        }
+        if (E.label < 0 || E.label >= 4096) {
+            delete S;
+            return set_error(NRT_E_INVALID, "edge %d: label outside [0,4096)", j);
+        }
+        float ev[3] = {E.b[0] - E.a[0], E.b[1] - E.a[1], E.b[2] - E.a[2]};
+        float len = sqrtf((ev[0] * ev[0] + ev[1] * ev[1]) + ev[2] * ev[2]);
+        if (!(len > 0.0f) || !std::isfinite(len)) {
+            delete S;
+            return set_error(NRT_E_INVALID, "edge %d: zero or non-finite length", j);
+        }
+        for (int k = 0; k < 3; ++k) {
+            g.a[k] = E.a[k];
+            g.e[k] = ev[k] / len;
+            g.t0[k] = E.t0[k];
+            g.n0[k] = E.n0[k];
+            g.n1[k] = E.n1[k];
+        }
+        g.len = len;
+        g.n_exp = E.n_exp;
+        g.label = E.label;
+        S->h_edges.push_back(g);
+    }
+    S->n_edges = D->n_edges;
+    nrt_status rc = build_impl(D, S, st);
+    if (rc == NRT_OK && S->n_edges > 0) {
+        cudaError_t e = cudaMalloc(&S->edges, sizeof(DevEdge) * S->n_edges);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(S->edges, S->h_edges.data(), sizeof(DevEdge) * S->n_edges,
+                           cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) rc = set_error(NRT_E_CUDA, "edge upload: %s", cudaGetErrorString(e));
+    }
+    if (rc != NRT_OK) {
+        nrt_scene_free(S);
+        return rc;
+    }
+    *out = S;
+    return NRT_OK;
+}
+
+}  // namespace nrt
