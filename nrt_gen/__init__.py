@@ -325,12 +325,12 @@ def case(name: str, **over) -> LaunchCase:
         lc = LaunchCase("C1", box_room(), C1_TX, C1_RX, 10_000, 2, 0, 0.125, r_s=0.03)
     elif name == "C2":
         sig = over.pop("sigma", 0.010)
-        lc = LaunchCase("C2", synth_room(1_000_000, sig), SR_TX, SR_RX, 1_000_000, 3, 1, 0.0625,
+        lc = LaunchCase("C2", synth_room(1_000_000, sig), SR_TX, SR_RX, 1_000_000, 3, 1, 0.03125,
                         tau=0.0015 + 3 * sig, r_s=0.01 if sig > 0 else 0.003, sigma_noise=sig)
     elif name == "C3":
         sig = over.pop("sigma", 0.010)
         lc = LaunchCase("C3", synth_room(1_000_000, sig, normals="pca"), SR_TX, SR_RX, 10_000_000, 4,
-                        0, 0.0625, tau=0.0015 + 3 * sig, r_s=0.01, sigma_noise=sig)
+                        0, 0.03125, tau=0.0015 + 3 * sig, r_s=0.01, sigma_noise=sig)
     elif name == "C2s":
         # small SR for brute-force parity: 40k surfels, 2e4 rays
         sig = over.pop("sigma", 0.010)

@@ -137,6 +137,46 @@ int or_trace_rays(const or_scene* S, const or_launch_params* P, const uint64_t* 
 /* R17 dedupe of an arbitrary record array (sort by key, L, ray id; keep first kappa) */
 int64_t or_dedupe(or_coarse* recs, int64_t n, int32_t kappa);
 
+/* ---- refinement (refine.c, FP64) ---- */
+enum { NRT_OR_OK = 0, NRT_OR_NO_CONVERGE = 1, NRT_OR_OFF_EDGE = 2, NRT_OR_NO_SUPPORT = 3,
+       NRT_OR_WRONG_SIDE = 4, NRT_OR_OCCLUDED = 5, NRT_OR_DEGENERATE = 6 };
+
+typedef struct {
+    double xi, r_s;        /* sigma = xi * r_s */
+    double tol_m;          /* converged when the GN step |D|_inf < tol_m */
+    int32_t max_iter;
+    double alpha, beta;    /* Eq. 12 backtracking */
+    double tau;            /* support / sheet tolerance (R25) */
+    double theta_ex_deg;   /* sheet angle for the shadow rays */
+    float tx[3];
+    const float* rx;       /* RX table indexed by the record's rx */
+} or_refine_params;
+
+typedef struct {
+    uint32_t rx;
+    uint8_t n_int, n_diff;
+    uint16_t kinds;
+    int32_t label[OR_MAX_INT];
+    uint32_t prim[OR_MAX_INT];
+    double v[OR_MAX_INT][3];
+    double L, delay;
+    float aod_az, aod_el, aoa_az, aoa_el;
+    float inc[OR_MAX_INT];
+    int32_t status, iters;
+    double resid, gradsq;
+    uint64_t ray_id;
+} or_refined;
+
+/* refine every coarse record (out[q] for in[q], no dedupe; status per path) */
+int or_refine(const or_scene* S, const or_refine_params* R, const or_coarse* in, int64_t n,
+              or_refined* out);
+/* residual of record c at its seed (z_in NULL) or at z_in; returns dim or -1 (pin helper) */
+int or_path_residual(const or_scene* S, const or_refine_params* R, const or_coarse* c,
+                     const double* z_in, double* r_out, double* z_out);
+/* Eqs. 1-4 at x over the label's surfels within 4 sigma (pin helper); 0 if empty */
+int or_mls(const or_scene* S, const or_refine_params* R, int32_t label, const double nseed[3],
+           const double x[3], double pbar[3], double nbar[3], double* f);
+
 #ifdef __cplusplus
 }
 #endif

@@ -360,3 +360,104 @@ def fan_dirs(edge, d, dphi_deg=2.5):
     out = np.zeros((512, 3), np.float32)
     M = lib().or_fan_dirs(C.byref(edge), d.ctypes.data, float(dphi_deg), out.ctypes.data, 512)
     return out[:M].copy()
+
+
+# ------------------------------------------------------------------------------------------
+# refinement (refine.c)
+# ------------------------------------------------------------------------------------------
+REFINED_DTYPE = np.dtype([
+    ("rx", "<u4"), ("n_int", "u1"), ("n_diff", "u1"), ("kinds", "<u2"),
+    ("label", "<i4", (8,)), ("prim", "<u4", (8,)), ("v", "<f8", (8, 3)),
+    ("L", "<f8"), ("delay", "<f8"),
+    ("aod_az", "<f4"), ("aod_el", "<f4"), ("aoa_az", "<f4"), ("aoa_el", "<f4"),
+    ("inc", "<f4", (8,)), ("status", "<i4"), ("iters", "<i4"),
+    ("resid", "<f8"), ("gradsq", "<f8"), ("ray_id", "<u8")], align=True)
+STATUS = {0: "OK", 1: "NO_CONVERGE", 2: "OFF_EDGE", 3: "NO_SUPPORT", 4: "WRONG_SIDE",
+          5: "OCCLUDED", 6: "DEGENERATE"}
+
+
+class _RefParams(C.Structure):
+    _fields_ = [("xi", C.c_double), ("r_s", C.c_double), ("tol_m", C.c_double),
+                ("max_iter", C.c_int32), ("alpha", C.c_double), ("beta", C.c_double),
+                ("tau", C.c_double), ("theta_ex_deg", C.c_double), ("tx", C.c_float * 3),
+                ("rx", C.c_void_p)]
+
+
+def _ref_params(case, rx=None, **over):
+    rxa = _f32(case.rx if rx is None else rx, (-1, 3))
+    p = _RefParams()
+    p.xi = float(over.get("xi", case.xi))
+    p.r_s = float(over.get("r_s", case.r_s))
+    p.tol_m = float(over.get("tol_m", 1e-10))
+    p.max_iter = int(over.get("max_iter", 100))
+    p.alpha = float(over.get("alpha", 0.4))
+    p.beta = float(over.get("beta", 0.4))
+    p.tau = float(over.get("tau", case.tau))
+    p.theta_ex_deg = float(over.get("theta_ex_deg", case.theta_ex_deg))
+    p.tx[:] = [float(x) for x in np.asarray(case.tx, np.float32)]
+    p.rx = rxa.ctypes.data
+    return p, rxa
+
+
+def refine(case, coarse, scene: OracleScene | None = None, **over):
+    """Refine every coarse record (no dedupe): one or_refined per input, with status."""
+    L = lib()
+    if not hasattr(L, "_ref_setup"):
+        L.or_refine.argtypes = [C.POINTER(_Scene), C.POINTER(_RefParams), C.c_void_p, C.c_int64,
+                                C.c_void_p]
+        L.or_mls.argtypes = [C.POINTER(_Scene), C.POINTER(_RefParams), C.c_int32, C.c_void_p,
+                             C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
+        L._ref_setup = True
+    sc = scene or OracleScene(case.scene)
+    p, rxa = _ref_params(case, **over)
+    cin = np.ascontiguousarray(coarse, dtype=COARSE_DTYPE)
+    out = np.zeros(cin.shape[0], REFINED_DTYPE)
+    L.or_refine(C.byref(sc.c), C.byref(p), cin.ctypes.data, cin.shape[0], out.ctypes.data)
+    return out
+
+
+def mls(case, label, nseed, x, scene: OracleScene | None = None, **over):
+    refine(case, np.zeros(0, COARSE_DTYPE), scene)  # argtypes
+    sc = scene or OracleScene(case.scene)
+    p, rxa = _ref_params(case, **over)
+    ns = np.ascontiguousarray(nseed, np.float64)
+    xx = np.ascontiguousarray(x, np.float64)
+    pb, nb = np.zeros(3), np.zeros(3)
+    f = C.c_double()
+    ok = lib().or_mls(C.byref(sc.c), C.byref(p), int(label), ns.ctypes.data, xx.ctypes.data,
+                      pb.ctypes.data, nb.ctypes.data, C.byref(f))
+    return (pb, nb, f.value) if ok else None
+
+
+def refine_dedupe(ref):
+    """R28: among OK paths keep the shortest per key (then lowest ray id), key order."""
+    ok = ref[ref["status"] == 0]
+    best = {}
+    for r in ok:
+        k = (int(r["rx"]), int(r["n_int"]), int(r["kinds"]), tuple(int(x) for x in r["label"]))
+        cur = best.get(k)
+        if cur is None or (float(r["L"]), int(r["ray_id"])) < (float(cur["L"]), int(cur["ray_id"])):
+            best[k] = r
+    keys = sorted(best)
+    return np.array([best[k] for k in keys], dtype=REFINED_DTYPE) if keys else np.zeros(0, REFINED_DTYPE)
+
+
+def path_residual(case, rec, z=None, scene: OracleScene | None = None, **over):
+    """Residual r(z) of one coarse record (at its seed when z is None) -> (r, z_seed)."""
+    refine(case, np.zeros(0, COARSE_DTYPE), scene)
+    L = lib()
+    if not hasattr(L, "_res_setup"):
+        L.or_path_residual.argtypes = [C.POINTER(_Scene), C.POINTER(_RefParams), C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]
+        L._res_setup = True
+    sc = scene or OracleScene(case.scene)
+    p, rxa = _ref_params(case, **over)
+    c = np.ascontiguousarray(np.asarray(rec, dtype=COARSE_DTYPE).reshape(1))
+    r = np.zeros(32)
+    zs = np.zeros(32)
+    zin = None if z is None else np.ascontiguousarray(z, np.float64)
+    m = L.or_path_residual(C.byref(sc.c), C.byref(p), c.ctypes.data,
+                           None if zin is None else zin.ctypes.data, r.ctypes.data, zs.ctypes.data)
+    if m < 0:
+        return None, None
+    return r[:m].copy(), zs[:m].copy()

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 
 #include <cmath>
 #include <cstdarg>
@@ -25,6 +27,42 @@ void clear_error() { g_err[0] = 0; }
 
 static std::atomic<unsigned long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// Stream-ordered allocations come from the device's default pool; keep freed blocks cached
+// (release threshold = max) so that repeated launches do not return memory to the driver.
+void ensure_pool(int dev) {
+    static std::atomic<unsigned long long> done{0};
+    if (dev < 0 || dev >= 64) return;
+    const unsigned long long bit = 1ull << dev;
+    if (done.load() & bit) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done.fetch_or(bit);
+}
+
+// NRT_PHASES=1: synchronise and print host wall time per phase (diagnostics only)
+struct PhaseLog {
+    bool on;
+    cudaStream_t st;
+    std::chrono::steady_clock::time_point t;
+    explicit PhaseLog(cudaStream_t s) : on(getenv("NRT_PHASES") != nullptr), st(s) {
+        if (on) {
+            cudaStreamSynchronize(st);
+            t = std::chrono::steady_clock::now();
+        }
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "[nrt] %-16s %8.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
 
 static bool finite3(const float* x) {
     return std::isfinite(x[0]) && std::isfinite(x[1]) && std::isfinite(x[2]);
@@ -190,6 +228,7 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
     else nrt_launch_desc_default(&d);
     NRT_TRY(check_launch(s, tx, rx, n_rx, n_rays, max_refl, max_diff, d));
     NRT_CUDA(cudaSetDevice(s->device));
+    ensure_pool(s->device);
     cudaStream_t st = (cudaStream_t)d.stream;
     LaunchArgs a{};
     float htx[3];
@@ -228,6 +267,7 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
     P->info.kind = NRT_PATHS_COARSE;
 
     EventTimer total(st);
+    PhaseLog ph(st);
     nrt_coarse_rec* raw = nullptr;
     nrt_event_rec* ev = nullptr;
     int64_t n_raw = 0, n_ev = 0;
@@ -236,6 +276,7 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
     {
         KernelStats ks;
         rc = launch_primary(s, a, &raw, &n_raw, &ev, &n_ev, &b1, &ks, st);
+        ph.mark("primary");
         P->info.ms_trace = ks.ms_kernel;
         P->info.surfel_tests = ks.tests;
         P->info.cells_visited = ks.cells;
@@ -256,6 +297,7 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
                  ? dedupe_events(ev, n_ev, evu, &n_evu, st)
                  : set_error(NRT_E_NOMEM, "event buffer");
         P->info.ms_dedupe += t.stop();
+        ph.mark("event dedupe");
     }
     cudaFreeAsync(ev, st);
     if (rc != NRT_OK) {
@@ -277,6 +319,7 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
             P->info.surfel_tests += ks.tests;
             P->info.cells_visited += ks.cells;
             P->info.cells_nonempty += ks.nonempty;
+            ph.mark("fans");
         }
         if (rc == NRT_OK && nf > 0) {
             nrt_coarse_rec* both = nullptr;
@@ -300,7 +343,9 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
     P->d_ev = evu;
     cudaFreeAsync(d_rx, st);
     P->info.n_raw = n_raw;
+    ph.mark("append");
     if (rc == NRT_OK) rc = finish_coarse(P, raw, n_raw, d.kappa, st);
+    ph.mark("record dedupe");
     cudaFreeAsync(raw, st);
     if (rc != NRT_OK) {
         nrt_paths_free(P);
@@ -318,6 +363,7 @@ nrt_status nrt_launch_fans(nrt_scene s, nrt_paths coarse, const void* events, in
     if (coarse->kind != NRT_PATHS_COARSE) return set_error(NRT_E_STATE, "not a coarse set");
     if (n_events < 0 || (n_events > 0 && !events)) return set_error(NRT_E_INVALID, "bad events");
     NRT_CUDA(cudaSetDevice(s->device));
+    ensure_pool(s->device);
     cudaStream_t st = (cudaStream_t)desc->stream;
     nrt_launch_desc d = *desc;
     LaunchArgs a{};
@@ -414,6 +460,7 @@ nrt_status nrt_refine_ex(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d
     if (d.world < 1 || d.rank < 0 || d.rank >= d.world)
         return set_error(NRT_E_INVALID, "need 0 <= rank < world");
     NRT_CUDA(cudaSetDevice(s->device));
+    ensure_pool(s->device);
     nrt_paths P = new nrt_paths_s();
     P->kind = NRT_PATHS_REFINED;
     P->device = s->device;
@@ -588,6 +635,7 @@ nrt_status nrt_debug_trace_rays(nrt_scene s, const float tx[3], int64_t n_rays, 
     NRT_TRY(check_launch(s, tx, dummy, 0, n_rays, max_refl, 0, d));
     if (n < 0 || (n > 0 && (!ray_ids || !hit_ids))) return set_error(NRT_E_INVALID, "bad arrays");
     NRT_CUDA(cudaSetDevice(s->device));
+    ensure_pool(s->device);
     LaunchArgs a{};
     memcpy(a.tx, tx, 12);
     a.d_rx = nullptr;

@@ -20,6 +20,7 @@ namespace nrt {
 nrt_status set_error(nrt_status st, const char* fmt, ...);
 void clear_error();
 void count_launch();  // every kernel launch of the library increments a process-wide counter
+void ensure_pool(int dev);  // default mempool keeps freed memory cached
 
 #define NRT_CUDA(call)                                                                    \
     do {                                                                                  \
@@ -100,6 +101,7 @@ struct DevEdge {
     float t0[3], n0[3], n1[3];
     float n_exp;
     int32_t label;
+    float c[3], hl;  // bounding sphere (centre, half length) for conservative culling
 };
 
 struct Hist {
@@ -122,6 +124,7 @@ struct nrt_scene_s {
     int dims[3] = {0, 0, 0};
     float org[3] = {0, 0, 0};
     float v = 0, inv_v = 0, pad = 0, r_max = 0;
+    float slack = 1e-4f;  // absolute slack (m) of the traversal's division-free disk prefilter
     uint2* cell = nullptr;     // [ncell] (start, end) into rec
     float4* rec = nullptr;     // [2*nref] AoS: (p, r^2), (n, id bits)
     float4* sp = nullptr;      // [n] (p, r)
@@ -130,6 +133,8 @@ struct nrt_scene_s {
     nrt::DevEdge* edges = nullptr;
     int n_edges = 0;
     std::vector<nrt::DevEdge> h_edges;
+    // output-buffer size hints (largest counts seen by launches on this scene)
+    unsigned long long hint_raw = 1 << 16, hint_ev = 1 << 14, hint_fan = 1 << 16;
 };
 
 struct nrt_paths_s {

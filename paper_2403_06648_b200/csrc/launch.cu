@@ -6,12 +6,22 @@
 // cells its padded disk AABB overlaps, and the walk stops only once best_t < t_exit - pad
 // (DESIGN.md §6), so the result equals the brute-force definition for any voxel size.
 // All FP32 arithmetic of the definition is done in the order DESIGN.md R3 fixes; the
-// library is compiled with -fmad=false so no FMA contraction alters a rounding.
+// library is compiled with -fmad=false so no FMA contraction alters a rounding (explicit
+// __fmaf_rn appears only in the prefilter and grid walk, which never decide a result).
+//
+// Execution model (wavefront): per bounce, one persistent TRACE kernel finds
+// the nearest hit of every live ray segment (tight loop: record tests + grid moves, lanes
+// refill from a device counter), then one SHADE kernel does the per-segment work uniformly
+// across threads (RX captures, edge captures, reflection, history) and compacts the live
+// list for the next bounce.  Counts stay on the device: no host round trip between bounces.
 #include <cooperative_groups.h>
 
 #include <cub/cub.cuh>
 
+#include <atomic>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.cuh"
@@ -31,6 +41,29 @@ float cRw_of(float c_R, int64_t n_rays) {
 
 namespace {
 
+constexpr int kMaxIter = NRT_MAX_INT + 1;  // bounce iterations per wavefront launch
+
+// per-ray state that only the shade kernel touches
+struct RayCold {
+    float L, Ls, kR, R0;
+    int32_t seg, budget, flags;  // flags: bit0 edge captures on, bit1 after a diffraction
+    int32_t pad_;
+    uint64_t rid;
+    Hist h;
+};
+
+struct Wave {
+    float4* o;       // [cap] origin xyz, prev surfel id (int bits)
+    float4* d;       // [cap] direction
+    float4* l0;      // [cap] departure-sheet normal 0
+    float4* l1;      // [cap] departure-sheet normal 1
+    float2* hit;     // [cap] (best_t, best id bits)
+    RayCold* cold;   // [cap]
+    unsigned* alive[2];       // ping-pong live lists
+    unsigned long long* n_alive;  // [kMaxIter + 1]
+    unsigned long long* ctr;      // [kMaxIter] trace work counters
+};
+
 struct TP {  // trace parameters (by value into the kernels)
     // grid
     const uint2* cell;
@@ -47,6 +80,7 @@ struct TP {  // trace parameters (by value into the kernels)
     int rank, world;
     int max_refl, max_diff;
     float tau, cos_ex, cRw, b_e, edge_bin, c_R, dphi_deg;
+    float slack;  // absolute slack of the division-free disk prefilter (m)
     const DevEdge* edges;
     int n_edges;
     // outputs
@@ -58,7 +92,7 @@ struct TP {  // trace parameters (by value into the kernels)
     unsigned long long* ev_n;
     unsigned long long* bounces;
     unsigned long long* counters;  // [tests, cells, nonempty cells] (instrumented build)
-    int64_t* hit_out;  // debug: per-segment hit ids
+    int64_t* hit_out;              // debug: per-segment hit ids
 };
 
 __device__ __forceinline__ unsigned long long agg_inc(unsigned long long* ctr) {
@@ -69,17 +103,15 @@ __device__ __forceinline__ unsigned long long agg_inc(unsigned long long* ctr) {
     return base + g.thread_rank();
 }
 
-// ---- A3: nearest surfel along (o, d) by 3D-DDA over the fine grid -----------------------
 struct Cnt {
     unsigned long long tests = 0, cells = 0, nonempty = 0;
 };
 
-template <bool CNT>
+// ---- A3 reference walk (debug path): nearest surfel along (o, d) by plain 3D-DDA --------
 __device__ int nearest(const TP& P, float3 o, float3 d, float3 l0, float3 l1, int prev,
-                       float& t_out, Cnt& cnt) {
+                       float& t_out) {
     float best_t = INFINITY;
     int best = -1;
-    // grid entry (slab test); the walk only needs a conservative start
     const float gx1 = P.ox + P.nx * P.v, gy1 = P.oy + P.ny * P.v, gz1 = P.oz + P.nz * P.v;
     float ix_ = 1.0f / d.x, iy_ = 1.0f / d.y, iz_ = 1.0f / d.z;
     float t0 = 0.0f, t1 = INFINITY;
@@ -106,14 +138,8 @@ __device__ int nearest(const TP& P, float3 o, float3 d, float3 l0, float3 l1, in
     float tmx = d.x != 0.0f ? ((P.ox + (float)(ix + (stx > 0)) * P.v) - o.x) * ix_ : INFINITY;
     float tmy = d.y != 0.0f ? ((P.oy + (float)(iy + (sty > 0)) * P.v) - o.y) * iy_ : INFINITY;
     float tmz = d.z != 0.0f ? ((P.oz + (float)(iz + (stz > 0)) * P.v) - o.z) * iz_ : INFINITY;
-    const float tau = P.tau, cex = P.cos_ex;
     for (;;) {
         const uint2 rg = __ldg(&P.cell[ix + P.nx * (iy + P.ny * iz)]);
-        if (CNT) {
-            cnt.cells++;
-            cnt.tests += rg.y - rg.x;
-            cnt.nonempty += rg.y > rg.x;
-        }
         for (unsigned k = rg.x; k < rg.y; ++k) {
             const float4 A = __ldg(&P.rec[2 * k]);
             const float4 B = __ldg(&P.rec[2 * k + 1]);
@@ -122,17 +148,17 @@ __device__ int nearest(const TP& P, float3 o, float3 d, float3 l0, float3 l1, in
             const float f0 = (wx * B.x + wy * B.y) + wz * B.z;
             const float dn = (d.x * B.x + d.y * B.y) + d.z * B.z;
             if (!(f0 * dn < 0.0f) || id == prev) continue;
-            if (fabsf(f0) <= tau) {
+            if (fabsf(f0) <= P.tau) {
                 const float c0 = (B.x * l0.x + B.y * l0.y) + B.z * l0.z;
                 const float c1 = (B.x * l1.x + B.y * l1.y) + B.z * l1.z;
-                if (fabsf(c0) >= cex || fabsf(c1) >= cex) continue;
+                if (fabsf(c0) >= P.cos_ex || fabsf(c1) >= P.cos_ex) continue;
             }
             const float t = (-f0) / dn;
             if (t > best_t) continue;
             const float hx = o.x + t * d.x, hy = o.y + t * d.y, hz = o.z + t * d.z;
             const float qx = hx - A.x, qy = hy - A.y, qz = hz - A.z;
             const float qq = (qx * qx + qy * qy) + qz * qz;
-            if (qq <= A.w && (t < best_t || id < best)) {
+            if (qq <= A.w * A.w && (t < best_t || id < best)) {
                 best_t = t;
                 best = id;
             }
@@ -199,8 +225,19 @@ __device__ void rx_captures(const TP& P, const Hist& h, float3 o, float3 d, floa
 // ---- A6: edge capture -> diffraction events (R13) --------------------------------------
 __device__ void edge_captures(const TP& P, const Hist& h, float3 o, float3 d, float t_hit,
                               float L, uint64_t ray_id) {
+    // conservative cull: a capture needs a ray point at t < t_hit + b_e within
+    // R(L + t) <= Rmax of an edge point, hence within hl + Rmax of the edge centre
+    const float T = fminf(t_hit + P.b_e, 1e4f);
+    const float Rmax = P.cRw * (L + T) * 1.001f + 1e-4f;
     for (int j = 0; j < P.n_edges; ++j) {
         const DevEdge& E = P.edges[j];
+        {
+            const float cx = E.c[0] - o.x, cy = E.c[1] - o.y, cz = E.c[2] - o.z;
+            const float tc = fminf(fmaxf(cx * d.x + cy * d.y + cz * d.z, 0.0f), T);
+            const float ux = cx - tc * d.x, uy = cy - tc * d.y, uz = cz - tc * d.z;
+            const float lim = E.hl + Rmax;
+            if (ux * ux + uy * uy + uz * uz > lim * lim) continue;
+        }
         const float b = (d.x * E.e[0] + d.y * E.e[1]) + d.z * E.e[2];
         const float w0x = o.x - E.a[0], w0y = o.y - E.a[1], w0z = o.z - E.a[2];
         const float den = 1.0f - b * b;
@@ -247,100 +284,32 @@ __device__ void edge_captures(const TP& P, const Hist& h, float3 o, float3 d, fl
     }
 }
 
-// ---- C.1 step 2: one ray (primary or fan) --------------------------------------------
-template <bool CNT>
-__device__ void trace(const TP& P, Hist& h, float3 o, float3 d, float L, int budget,
-                      bool allow_edges, float3 l0, float3 l1, bool after_diff, float kR, float R0,
-                      uint64_t ray_id, unsigned long long& bounces, int64_t* hit_out, Cnt& cnt) {
-    float Ls = 0.0f;
-    int prev = -1;
-    for (int seg = 0; seg <= budget; ++seg) {
-        float th;
-        const int s = nearest<CNT>(P, o, d, l0, l1, prev, th, cnt);
-        ++bounces;
-        if (hit_out) hit_out[seg] = s;
-        rx_captures(P, h, o, d, th, L, Ls, kR, R0, after_diff, ray_id);
-        if (allow_edges && h.n_diff < P.max_diff && h.n < NRT_MAX_INT)
-            edge_captures(P, h, o, d, th, L, ray_id);
-        if (s < 0 || seg == budget) break;
-        // A4: reflect (d' = d - (2 d.n) n, normalised)
-        const float3 hp = make_float3(o.x + th * d.x, o.y + th * d.y, o.z + th * d.z);
-        const float4 nv = __ldg(&P.sn[s]);
-        const float3 n = make_float3(nv.x, nv.y, nv.z);
-        h.label[h.n] = __ldg(&P.label[s]);
-        h.prim[h.n] = (uint32_t)s;
-        h.v[h.n][0] = hp.x;
-        h.v[h.n][1] = hp.y;
-        h.v[h.n][2] = hp.z;
-        h.n++;
-        const float k2 = 2.0f * dot3(d, n);
-        const float3 x = make_float3(d.x - k2 * n.x, d.y - k2 * n.y, d.z - k2 * n.z);
-        const float l = sqrtf(dot3(x, x));
-        d = make_float3(x.x / l, x.y / l, x.z / l);
-        o = hp;
-        L = L + th;
-        Ls = Ls + th;
-        l0 = n;
-        l1 = n;
-        prev = s;
-    }
-}
-
-__device__ __forceinline__ void flush_counts(const TP& P, unsigned long long bounces, const Cnt& c,
-                                             bool cnt_on) {
-    for (int off = 16; off > 0; off >>= 1) bounces += __shfl_down_sync(0xffffffffu, bounces, off);
-    if ((threadIdx.x & 31) == 0) atomicAdd(P.bounces, bounces);
-    if (cnt_on) {
-        unsigned long long t = c.tests, ce = c.cells, ne = c.nonempty;
-        for (int off = 16; off > 0; off >>= 1) {
-            t += __shfl_down_sync(0xffffffffu, t, off);
-            ce += __shfl_down_sync(0xffffffffu, ce, off);
-            ne += __shfl_down_sync(0xffffffffu, ne, off);
-        }
-        if ((threadIdx.x & 31) == 0) {
-            atomicAdd(P.counters, t);
-            atomicAdd(P.counters + 1, ce);
-            atomicAdd(P.counters + 2, ne);
-        }
-    }
-}
-
-template <bool CNT>
-__global__ void __launch_bounds__(128) k_primary(TP P, uint64_t n_shard) {
-    unsigned long long bounces = 0;
-    Cnt cnt;
-    const float3 z3 = make_float3(0.0f, 0.0f, 0.0f);
-    const bool edges_on = P.n_edges > 0 && P.max_diff > 0;
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_shard;
-         j += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = (uint64_t)P.rank + j * (uint64_t)P.world;
-        Hist h;
-        h.n = 0;
-        h.n_diff = 0;
-        h.kinds = 0;
-        h.s_edge = 0.0f;
-        const float3 d = fib_dir(i, P.n_rays);
-        trace<CNT>(P, h, make_float3(P.tx, P.ty, P.tz), d, 0.0f, P.max_refl, edges_on, z3, z3,
-                   false, P.cRw, 0.0f, i, bounces, nullptr, cnt);
-    }
-    flush_counts(P, bounces, cnt, CNT);
-}
-
+// ---- debug: C.1 step 2 for one primary ray, sequentially, with the reference walk -------
 __global__ void k_debug(TP P, const uint64_t* ids, int64_t n) {
     int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n) return;
-    unsigned long long b = 0;
-    Hist h;
-    h.n = 0;
-    h.n_diff = 0;
-    h.kinds = 0;
-    h.s_edge = 0.0f;
-    const float3 z3 = make_float3(0.0f, 0.0f, 0.0f);
     int64_t* out = P.hit_out + q * (P.max_refl + 1);
     for (int k = 0; k <= P.max_refl; ++k) out[k] = -2;
-    Cnt cnt;
-    trace<false>(P, h, make_float3(P.tx, P.ty, P.tz), fib_dir(ids[q], P.n_rays), 0.0f, P.max_refl,
-                 false, z3, z3, false, P.cRw, 0.0f, ids[q], b, out, cnt);
+    float3 o = make_float3(P.tx, P.ty, P.tz);
+    float3 d = fib_dir(ids[q], P.n_rays);
+    float3 l0 = make_float3(0.0f, 0.0f, 0.0f), l1 = l0;
+    int prev = -1;
+    for (int seg = 0; seg <= P.max_refl; ++seg) {
+        float th;
+        const int s = nearest(P, o, d, l0, l1, prev, th);
+        out[seg] = s;
+        if (s < 0 || seg == P.max_refl) break;
+        const float3 hp = make_float3(o.x + th * d.x, o.y + th * d.y, o.z + th * d.z);
+        const float4 nv = __ldg(&P.sn[s]);
+        const float3 nn = make_float3(nv.x, nv.y, nv.z);
+        const float k2 = 2.0f * dot3(d, nn);
+        const float3 x = make_float3(d.x - k2 * nn.x, d.y - k2 * nn.y, d.z - k2 * nn.z);
+        const float l = sqrtf(dot3(x, x));
+        d = make_float3(x.x / l, x.y / l, x.z / l);
+        o = hp;
+        l0 = l1 = nn;
+        prev = s;
+    }
 }
 
 // ---- A7: fans -------------------------------------------------------------------------
@@ -370,17 +339,308 @@ __global__ void k_fan_count(TP P, const nrt_event_rec* ev, int64_t n_ev, unsigne
     cnt[r] = mine ? (unsigned)fan_geo(P, ev[r]).M : 0u;
 }
 
+// =======================================================================================
+// Wavefront engine
+// =======================================================================================
+struct Seg {  // trace-kernel lane state for one segment
+    float3 o, d, inv, l0, l1;
+    int prev;
+    float best_t, tmx, tmy, tmz;
+    int best, ix, iy, iz, cellD;
+    unsigned k, kend;
+};
+
 template <bool CNT>
-__global__ void __launch_bounds__(128) k_fans(TP P, const nrt_event_rec* ev, int64_t n_ev,
-                                              const unsigned int* off, unsigned int total) {
+__device__ __forceinline__ void load_cell(const TP& P, Seg& s, Cnt& cnt) {
+    const uint2 rg = __ldg(&P.cell[s.ix + P.nx * (s.iy + P.ny * s.iz)]);
+    if (CNT) cnt.cells++;
+    if (rg.y > rg.x) {
+        s.k = rg.x;
+        s.kend = rg.y;
+        s.cellD = 1;
+        if (CNT) {
+            cnt.nonempty++;
+            cnt.tests += rg.y - rg.x;
+        }
+    } else {
+        s.cellD = (int)rg.x;
+    }
+}
+
+// grid entry, first cell, first header load; false when the ray misses the grid
+template <bool CNT>
+__device__ __forceinline__ bool seg_begin(const TP& P, Seg& s, Cnt& cnt) {
+    s.best_t = INFINITY;
+    s.best = -1;
+    s.k = s.kend = 0;
+    const float3 o = s.o, d = s.d;
+    s.inv = make_float3(__frcp_rn(d.x), __frcp_rn(d.y), __frcp_rn(d.z));
+    const float gx1 = P.ox + P.nx * P.v, gy1 = P.oy + P.ny * P.v, gz1 = P.oz + P.nz * P.v;
+    float t0 = 0.0f, t1 = INFINITY;
+    {
+        float a = (P.ox - o.x) * s.inv.x, b = (gx1 - o.x) * s.inv.x;
+        if (d.x != 0.0f) { t0 = fmaxf(t0, fminf(a, b)); t1 = fminf(t1, fmaxf(a, b)); }
+        else if (o.x < P.ox || o.x > gx1) t1 = -1.0f;
+        a = (P.oy - o.y) * s.inv.y; b = (gy1 - o.y) * s.inv.y;
+        if (d.y != 0.0f) { t0 = fmaxf(t0, fminf(a, b)); t1 = fminf(t1, fmaxf(a, b)); }
+        else if (o.y < P.oy || o.y > gy1) t1 = -1.0f;
+        a = (P.oz - o.z) * s.inv.z; b = (gz1 - o.z) * s.inv.z;
+        if (d.z != 0.0f) { t0 = fmaxf(t0, fminf(a, b)); t1 = fminf(t1, fmaxf(a, b)); }
+        else if (o.z < P.oz || o.z > gz1) t1 = -1.0f;
+    }
+    if (t0 > t1) return false;
+    const float sx = o.x + t0 * d.x, sy = o.y + t0 * d.y, sz = o.z + t0 * d.z;
+    s.ix = min(P.nx - 1, max(0, (int)floorf((sx - P.ox) * P.inv_v)));
+    s.iy = min(P.ny - 1, max(0, (int)floorf((sy - P.oy) * P.inv_v)));
+    s.iz = min(P.nz - 1, max(0, (int)floorf((sz - P.oz) * P.inv_v)));
+    s.tmx = d.x != 0.0f ? ((P.ox + (float)(s.ix + (d.x > 0.0f)) * P.v) - o.x) * s.inv.x : INFINITY;
+    s.tmy = d.y != 0.0f ? ((P.oy + (float)(s.iy + (d.y > 0.0f)) * P.v) - o.y) * s.inv.y : INFINITY;
+    s.tmz = d.z != 0.0f ? ((P.oz + (float)(s.iz + (d.z > 0.0f)) * P.v) - o.z) * s.inv.z : INFINITY;
+    load_cell<CNT>(P, s, cnt);
+    return true;
+}
+
+// one grid move out of the current (exhausted) cell: a DDA step, or, from an empty cell
+// whose Chebyshev distance to the nearest non-empty cell is D >= 2, a jump across the empty
+// box [c-(D-1), c+(D-1)] (the paper's march distance, P:154 / P:281).  false = left the grid.
+template <bool CNT>
+__device__ __forceinline__ bool grid_move(const TP& P, Seg& s, Cnt& cnt) {
+    const float3 o = s.o, d = s.d;
+    const int D = s.cellD;
+    if (D <= 1) {
+        if (s.tmx <= s.tmy && s.tmx <= s.tmz) {
+            s.ix += d.x > 0.0f ? 1 : -1;
+            if (s.ix < 0 || s.ix >= P.nx) return false;
+            s.tmx = ((P.ox + (float)(s.ix + (d.x > 0.0f)) * P.v) - o.x) * s.inv.x;
+        } else if (s.tmy <= s.tmz) {
+            s.iy += d.y > 0.0f ? 1 : -1;
+            if (s.iy < 0 || s.iy >= P.ny) return false;
+            s.tmy = ((P.oy + (float)(s.iy + (d.y > 0.0f)) * P.v) - o.y) * s.inv.y;
+        } else {
+            s.iz += d.z > 0.0f ? 1 : -1;
+            if (s.iz < 0 || s.iz >= P.nz) return false;
+            s.tmz = ((P.oz + (float)(s.iz + (d.z > 0.0f)) * P.v) - o.z) * s.inv.z;
+        }
+    } else {
+        const int r = D - 1;
+        const int fx = d.x > 0.0f ? s.ix + r + 1 : s.ix - r;
+        const int fy = d.y > 0.0f ? s.iy + r + 1 : s.iy - r;
+        const int fz = d.z > 0.0f ? s.iz + r + 1 : s.iz - r;
+        const float Tx = d.x != 0.0f ? ((P.ox + (float)fx * P.v) - o.x) * s.inv.x : INFINITY;
+        const float Ty = d.y != 0.0f ? ((P.oy + (float)fy * P.v) - o.y) * s.inv.y : INFINITY;
+        const float Tz = d.z != 0.0f ? ((P.oz + (float)fz * P.v) - o.z) * s.inv.z : INFINITY;
+        const float T = fminf(Tx, fminf(Ty, Tz));
+        const float px = o.x + T * d.x, py = o.y + T * d.y, pz = o.z + T * d.z;
+        int nx = (int)floorf((px - P.ox) * P.inv_v), ny = (int)floorf((py - P.oy) * P.inv_v),
+            nz = (int)floorf((pz - P.oz) * P.inv_v);
+        nx = min(s.ix + r, max(s.ix - r, nx));
+        ny = min(s.iy + r, max(s.iy - r, ny));
+        nz = min(s.iz + r, max(s.iz - r, nz));
+        if (Tx <= Ty && Tx <= Tz) nx = d.x > 0.0f ? s.ix + r + 1 : s.ix - r - 1;
+        else if (Ty <= Tz) ny = d.y > 0.0f ? s.iy + r + 1 : s.iy - r - 1;
+        else nz = d.z > 0.0f ? s.iz + r + 1 : s.iz - r - 1;
+        if (nx < 0 || nx >= P.nx || ny < 0 || ny >= P.ny || nz < 0 || nz >= P.nz) return false;
+        s.ix = nx;
+        s.iy = ny;
+        s.iz = nz;
+        s.tmx = d.x != 0.0f ? ((P.ox + (float)(nx + (d.x > 0.0f)) * P.v) - o.x) * s.inv.x : INFINITY;
+        s.tmy = d.y != 0.0f ? ((P.oy + (float)(ny + (d.y > 0.0f)) * P.v) - o.y) * s.inv.y : INFINITY;
+        s.tmz = d.z != 0.0f ? ((P.oz + (float)(nz + (d.z > 0.0f)) * P.v) - o.z) * s.inv.z : INFINITY;
+    }
+    load_cell<CNT>(P, s, cnt);
+    return true;
+}
+
+// HIT predicate (R7-R9) on one loaded record, keeping the lexicographic min (t, id).
+// A division-free prefilter rejects records whose disk the ray clearly misses:
+// q * dn = w * dn - f0 * d (w = o - p), so |q| > r  <=>  |w dn - f0 d|^2 > r^2 dn^2; the
+// reject threshold carries an absolute slack P.slack (>> the FP32 error of either form), so
+// only records that might pass reach the exact, definition-ordered arithmetic.
+__device__ __forceinline__ void test_record(const TP& P, Seg& s, const float4 A, const float4 B) {
+    const int id = __float_as_int(B.w);
+    const float wx = s.o.x - A.x, wy = s.o.y - A.y, wz = s.o.z - A.z;
+    const float f0 = (wx * B.x + wy * B.y) + wz * B.z;
+    const float dn = (s.d.x * B.x + s.d.y * B.y) + s.d.z * B.z;
+    if (!(f0 * dn < 0.0f)) return;
+    {
+        const float ex = __fmaf_rn(-f0, s.d.x, wx * dn), ey = __fmaf_rn(-f0, s.d.y, wy * dn),
+                    ez = __fmaf_rn(-f0, s.d.z, wz * dn);
+        const float rs = A.w + P.slack;
+        if (__fmaf_rn(ex, ex, __fmaf_rn(ey, ey, ez * ez)) > rs * rs * (dn * dn)) return;
+    }
+    if (id == s.prev) return;
+    if (fabsf(f0) <= P.tau) {
+        const float c0 = (B.x * s.l0.x + B.y * s.l0.y) + B.z * s.l0.z;
+        const float c1 = (B.x * s.l1.x + B.y * s.l1.y) + B.z * s.l1.z;
+        if (fabsf(c0) >= P.cos_ex || fabsf(c1) >= P.cos_ex) return;
+    }
+    const float t = (-f0) / dn;
+    if (t > s.best_t) return;
+    const float hx = s.o.x + t * s.d.x, hy = s.o.y + t * s.d.y, hz = s.o.z + t * s.d.z;
+    const float qx = hx - A.x, qy = hy - A.y, qz = hz - A.z;
+    const float qq = (qx * qx + qy * qy) + qz * qz;
+    if (qq <= A.w * A.w && (t < s.best_t || id < s.best)) {
+        s.best_t = t;
+        s.best = id;
+    }
+}
+
+__device__ __forceinline__ void flush_counts(const TP& P, unsigned long long bounces, const Cnt& c,
+                                             bool cnt_on) {
+    for (int off = 16; off > 0; off >>= 1) bounces += __shfl_down_sync(0xffffffffu, bounces, off);
+    if ((threadIdx.x & 31) == 0 && bounces) atomicAdd(P.bounces, bounces);
+    if (cnt_on) {
+        unsigned long long t = c.tests, ce = c.cells, ne = c.nonempty;
+        for (int off = 16; off > 0; off >>= 1) {
+            t += __shfl_down_sync(0xffffffffu, t, off);
+            ce += __shfl_down_sync(0xffffffffu, ce, off);
+            ne += __shfl_down_sync(0xffffffffu, ne, off);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(P.counters, t);
+            atomicAdd(P.counters + 1, ce);
+            atomicAdd(P.counters + 2, ne);
+        }
+    }
+}
+
+// TRACE: nearest hit of every live segment of bounce b (persistent, dynamic refill)
+template <bool CNT>
+__global__ void __launch_bounds__(128) k_trace(TP P, Wave W, int b) {
+    const unsigned long long n = W.n_alive[b];
+    const unsigned* alive = W.alive[b & 1];
     unsigned long long bounces = 0;
     Cnt cnt;
+    Seg s;
+    unsigned ray = 0;
+    bool have = false;
+    for (;;) {
+        if (!have) {
+            const unsigned long long j = agg_inc(&W.ctr[b]);
+            if (j >= n) break;
+            ray = alive[j];
+            const float4 o = W.o[ray], d = W.d[ray], a = W.l0[ray], c = W.l1[ray];
+            s.o = make_float3(o.x, o.y, o.z);
+            s.prev = __float_as_int(o.w);
+            s.d = make_float3(d.x, d.y, d.z);
+            s.l0 = make_float3(a.x, a.y, a.z);
+            s.l1 = make_float3(c.x, c.y, c.z);
+            ++bounces;
+            if (!seg_begin<CNT>(P, s, cnt)) {
+                W.hit[ray] = make_float2(INFINITY, __int_as_float(-1));
+                continue;
+            }
+            have = true;
+        }
+        if (s.k < s.kend) {
+            // four records per iteration, all loads issued before any test; indices past the
+            // cell end repeat the last record (the (t, id) argmin is idempotent)
+            const unsigned last = s.kend - 1;
+            const unsigned k0 = s.k, k1 = min(k0 + 1, last), k2 = min(k0 + 2, last),
+                           k3 = min(k0 + 3, last);
+            const float4 A0 = __ldg(&P.rec[2 * k0]), B0 = __ldg(&P.rec[2 * k0 + 1]);
+            const float4 A1 = __ldg(&P.rec[2 * k1]), B1 = __ldg(&P.rec[2 * k1 + 1]);
+            const float4 A2 = __ldg(&P.rec[2 * k2]), B2 = __ldg(&P.rec[2 * k2 + 1]);
+            const float4 A3 = __ldg(&P.rec[2 * k3]), B3 = __ldg(&P.rec[2 * k3 + 1]);
+            test_record(P, s, A0, B0);
+            test_record(P, s, A1, B1);
+            test_record(P, s, A2, B2);
+            test_record(P, s, A3, B3);
+            s.k = min(k0 + 4, s.kend);
+            continue;
+        }
+        const float te = fminf(s.tmx, fminf(s.tmy, s.tmz));
+        if (s.best_t < te - P.pad || !grid_move<CNT>(P, s, cnt)) {
+            W.hit[ray] = make_float2(s.best_t, __int_as_float(s.best));
+            have = false;
+        }
+    }
+    flush_counts(P, bounces, cnt, CNT);
+}
+
+// SHADE: captures, edge events, reflection; compacts the live list for bounce b+1
+__global__ void __launch_bounds__(128) k_shade(TP P, Wave W, int b) {
+    const unsigned long long n = W.n_alive[b];
+    const unsigned* alive = W.alive[b & 1];
+    unsigned* next = W.alive[(b + 1) & 1];
+    for (unsigned long long j = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned ray = alive[j];
+        const float4 o4 = W.o[ray], d4 = W.d[ray];
+        const float2 hit = W.hit[ray];
+        const float3 o = make_float3(o4.x, o4.y, o4.z), d = make_float3(d4.x, d4.y, d4.z);
+        const float th = hit.x;
+        const int sid = __float_as_int(hit.y);
+        RayCold& c = W.cold[ray];
+        const int flags = c.flags;
+        const float L = c.L, Ls = c.Ls;
+        rx_captures(P, c.h, o, d, th, L, Ls, c.kR, c.R0, (flags & 2) != 0, c.rid);
+        if ((flags & 1) && c.h.n_diff < P.max_diff && c.h.n < NRT_MAX_INT)
+            edge_captures(P, c.h, o, d, th, L, c.rid);
+        if (sid >= 0 && c.seg < c.budget) {
+            // A4: reflect at the hit surfel: d' = d - (2 d.n) n, normalised
+            const float3 hp = make_float3(o.x + th * d.x, o.y + th * d.y, o.z + th * d.z);
+            const float4 nv = __ldg(&P.sn[sid]);
+            const float3 nn = make_float3(nv.x, nv.y, nv.z);
+            const int hn = c.h.n;
+            c.h.label[hn] = __ldg(&P.label[sid]);
+            c.h.prim[hn] = (uint32_t)sid;
+            c.h.v[hn][0] = hp.x;
+            c.h.v[hn][1] = hp.y;
+            c.h.v[hn][2] = hp.z;
+            c.h.n = hn + 1;
+            const float k2 = 2.0f * dot3(d, nn);
+            const float3 x = make_float3(d.x - k2 * nn.x, d.y - k2 * nn.y, d.z - k2 * nn.z);
+            const float l = sqrtf(dot3(x, x));
+            W.d[ray] = make_float4(x.x / l, x.y / l, x.z / l, 0.0f);
+            W.o[ray] = make_float4(hp.x, hp.y, hp.z, __int_as_float(sid));
+            W.l0[ray] = make_float4(nn.x, nn.y, nn.z, 0.0f);
+            W.l1[ray] = make_float4(nn.x, nn.y, nn.z, 0.0f);
+            c.L = L + th;
+            c.Ls = Ls + th;
+            c.seg = c.seg + 1;
+            next[agg_inc(&W.n_alive[b + 1])] = ray;
+        }
+    }
+}
+
+// primary ray generation (A2): lattice index i = rank + j * world
+__global__ void k_gen_primary(TP P, Wave W, uint64_t n_shard) {
+    const bool edges_on = P.n_edges > 0 && P.max_diff > 0;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_shard;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = (uint64_t)P.rank + j * (uint64_t)P.world;
+        const float3 d = fib_dir(i, P.n_rays);
+        W.o[j] = make_float4(P.tx, P.ty, P.tz, __int_as_float(-1));
+        W.d[j] = make_float4(d.x, d.y, d.z, 0.0f);
+        W.l0[j] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        W.l1[j] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        RayCold& c = W.cold[j];
+        c.L = 0.0f;
+        c.Ls = 0.0f;
+        c.kR = P.cRw;
+        c.R0 = 0.0f;
+        c.seg = 0;
+        c.budget = P.max_refl;
+        c.flags = edges_on ? 1 : 0;
+        c.rid = i;
+        c.h.n = 0;
+        c.h.n_diff = 0;
+        c.h.kinds = 0;
+        c.h.s_edge = 0.0f;
+        W.alive[0][j] = (unsigned)j;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) W.n_alive[0] = n_shard;
+}
+
+// fan ray generation (A7, R15-R16): fan index f -> (event r, m); Eq. 14 lift
+__global__ void k_gen_fans(TP P, Wave W, const nrt_event_rec* ev, int64_t n_ev,
+                           const unsigned int* off, unsigned int total) {
     for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < total;
          f += gridDim.x * blockDim.x) {
-        // event r: last r with off[r] <= f
         int64_t lo = 0, hi = n_ev - 1;
         while (lo < hi) {
-            int64_t mid = (lo + hi + 1) >> 1;
+            const int64_t mid = (lo + hi + 1) >> 1;
             if (off[mid] <= f) lo = mid;
             else hi = mid - 1;
         }
@@ -389,12 +649,18 @@ __global__ void __launch_bounds__(128) k_fans(TP P, const nrt_event_rec* ev, int
         const nrt_event_rec& e = ev[r];
         const DevEdge& E = P.edges[e.edge];
         const FanGeo g = fan_geo(P, e);
+        int n_refl = 0;
+        for (int k = 0; k < e.n_hist; ++k)
+            if (!((e.kinds >> k) & 1u)) n_refl++;
+        int budget = P.max_refl - n_refl;
+        if (budget < 0) continue;
         const double wedge = (double)E.n_exp * kPi;
-        const float kR = (float)((double)P.c_R * (wedge / (double)g.M) * g.st);
-        const float R0 = 0.5f * P.edge_bin;
+        RayCold& c = W.cold[f];
+        c.kR = (float)((double)P.c_R * (wedge / (double)g.M) * g.st);
+        c.R0 = 0.5f * P.edge_bin;
         const float3 o = make_float3(E.a[0] + e.s * E.e[0], E.a[1] + e.s * E.e[1],
                                      E.a[2] + e.s * E.e[2]);
-        Hist h;
+        Hist& h = c.h;
         h.n = e.n_hist;
         h.n_diff = e.n_diff;
         h.kinds = e.kinds;
@@ -414,11 +680,6 @@ __global__ void __launch_bounds__(128) k_fans(TP P, const nrt_event_rec* ev, int
         h.n++;
         h.n_diff++;
         h.s_edge = e.s;
-        int n_refl = 0;
-        for (int k = 0; k < e.n_hist; ++k)
-            if (!((e.kinds >> k) & 1u)) n_refl++;
-        int budget = P.max_refl - n_refl;
-        if (budget < 0) continue;
         if (h.n + budget > NRT_MAX_INT) budget = NRT_MAX_INT - h.n;
         const double phi = (((double)m + 0.5) * wedge) / (double)g.M;
         double sp, cp;
@@ -428,12 +689,18 @@ __global__ void __launch_bounds__(128) k_fans(TP P, const nrt_event_rec* ev, int
             const double x2 = cp * (double)E.t0[k] + sp * (double)E.n0[k];
             dir[k] = (float)(x2 * g.st + (double)E.e[k] * g.ct);
         }
-        const uint64_t rid = (1ull << 63) | ((uint64_t)r << 8) | (uint64_t)m;
-        trace<CNT>(P, h, o, make_float3(dir[0], dir[1], dir[2]), e.L, budget, false,
-                   make_float3(E.n0[0], E.n0[1], E.n0[2]), make_float3(E.n1[0], E.n1[1], E.n1[2]),
-                   true, kR, R0, rid, bounces, nullptr, cnt);
+        W.o[f] = make_float4(o.x, o.y, o.z, __int_as_float(-1));
+        W.d[f] = make_float4(dir[0], dir[1], dir[2], 0.0f);
+        W.l0[f] = make_float4(E.n0[0], E.n0[1], E.n0[2], 0.0f);
+        W.l1[f] = make_float4(E.n1[0], E.n1[1], E.n1[2], 0.0f);
+        c.L = e.L;
+        c.Ls = 0.0f;
+        c.seg = 0;
+        c.budget = budget;
+        c.flags = 2;
+        c.rid = (1ull << 63) | ((uint64_t)r << 8) | (uint64_t)m;
+        W.alive[0][agg_inc(&W.n_alive[0])] = f;
     }
-    flush_counts(P, bounces, cnt, CNT);
 }
 
 TP make_tp(nrt_scene s, const LaunchArgs& a) {
@@ -448,6 +715,7 @@ TP make_tp(nrt_scene s, const LaunchArgs& a) {
     P.v = s->v;
     P.inv_v = s->inv_v;
     P.pad = s->pad;
+    P.slack = fmaxf(s->slack, 4e-6f * fmaxf(fabsf(a.tx[0]), fmaxf(fabsf(a.tx[1]), fabsf(a.tx[2]))));
     P.nx = s->dims[0];
     P.ny = s->dims[1];
     P.nz = s->dims[2];
@@ -482,11 +750,79 @@ int sm_count(int dev) {
     return n > 0 ? n : 148;
 }
 
+template <class K>
+unsigned persistent_blocks(K kernel, int dev) {
+    static int per_sm_cache[2] = {0, 0};
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, 0);
+    (void)per_sm_cache;
+    if (per_sm < 1) per_sm = 1;
+    return (unsigned)(sm_count(dev) * per_sm);
+}
+
 }  // namespace
 
 struct Counters {
     unsigned long long raw_n, ev_n, bounces, tests, cells, nonempty;
+    unsigned long long n_alive[kMaxIter + 1];
+    unsigned long long ctr[kMaxIter];
 };
+
+static std::atomic<unsigned long long> g_hint_raw{0}, g_hint_ev{0}, g_hint_fan{0};
+
+// wavefront buffers for up to `cap` rays (stream-ordered; freed by free_wave)
+static nrt_status alloc_wave(Wave& W, uint64_t cap, cudaStream_t st) {
+    if (cap < 1) cap = 1;
+    NRT_CUDA(cudaMallocAsync(&W.o, cap * sizeof(float4), st));
+    NRT_CUDA(cudaMallocAsync(&W.d, cap * sizeof(float4), st));
+    NRT_CUDA(cudaMallocAsync(&W.l0, cap * sizeof(float4), st));
+    NRT_CUDA(cudaMallocAsync(&W.l1, cap * sizeof(float4), st));
+    NRT_CUDA(cudaMallocAsync(&W.hit, cap * sizeof(float2), st));
+    NRT_CUDA(cudaMallocAsync(&W.cold, cap * sizeof(RayCold), st));
+    NRT_CUDA(cudaMallocAsync(&W.alive[0], cap * sizeof(unsigned), st));
+    NRT_CUDA(cudaMallocAsync(&W.alive[1], cap * sizeof(unsigned), st));
+    return NRT_OK;
+}
+static void free_wave(Wave& W, cudaStream_t st) {
+    cudaFreeAsync(W.o, st);
+    cudaFreeAsync(W.d, st);
+    cudaFreeAsync(W.l0, st);
+    cudaFreeAsync(W.l1, st);
+    cudaFreeAsync(W.hit, st);
+    cudaFreeAsync(W.cold, st);
+    cudaFreeAsync(W.alive[0], st);
+    cudaFreeAsync(W.alive[1], st);
+}
+
+// bounce loop: TRACE + SHADE per bounce; ms_kernel accumulates the TRACE kernels' time
+static nrt_status run_bounces(const TP& P, Wave& W, int iters, int dev, bool counters,
+                              float* ms_trace, cudaStream_t st) {
+    const unsigned tb = counters ? persistent_blocks(k_trace<true>, dev)
+                                 : persistent_blocks(k_trace<false>, dev);
+    const unsigned sb = (unsigned)sm_count(dev) * 8;
+    cudaEvent_t ev[2 * kMaxIter + 2];
+    for (int i = 0; i < 2 * iters; ++i) cudaEventCreate(&ev[i]);
+    for (int b = 0; b < iters; ++b) {
+        cudaEventRecord(ev[2 * b], st);
+        if (counters) k_trace<true><<<tb, 128, 0, st>>>(P, W, b);
+        else k_trace<false><<<tb, 128, 0, st>>>(P, W, b);
+        ::nrt::count_launch();
+        cudaEventRecord(ev[2 * b + 1], st);
+        k_shade<<<sb, 128, 0, st>>>(P, W, b);
+        ::nrt::count_launch();
+    }
+    NRT_CUDA(cudaGetLastError());
+    NRT_CUDA(cudaStreamSynchronize(st));
+    float tot = 0;
+    for (int b = 0; b < iters; ++b) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev[2 * b], ev[2 * b + 1]);
+        tot += ms;
+    }
+    for (int i = 0; i < 2 * iters; ++i) cudaEventDestroy(ev[i]);
+    *ms_trace = tot;
+    return NRT_OK;
+}
 
 nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out,
                           int64_t* n_raw, nrt_event_rec** ev_out, int64_t* n_ev,
@@ -495,9 +831,19 @@ nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw
     const uint64_t n_shard =
         a.n_rays > a.desc.rank ? ((uint64_t)a.n_rays - a.desc.rank + a.desc.world - 1) / a.desc.world
                                : 0;
-    unsigned long long raw_cap = 1 << 16, ev_cap = 1 << 14;
+    // capacities start from the largest counts any launch of this process needed (scene
+    // handles are rebuilt often; a too-small buffer would re-run the whole launch)
+    if (g_hint_raw.load() > s->hint_raw) s->hint_raw = g_hint_raw.load();
+    if (g_hint_ev.load() > s->hint_ev) s->hint_ev = g_hint_ev.load();
+    unsigned long long raw_cap = s->hint_raw + s->hint_raw / 4 + 1024;
+    unsigned long long ev_cap = s->hint_ev + s->hint_ev / 4 + 1024;
+    if (P.n_edges > 0 && P.max_diff > 0 && ev_cap < n_shard / 8) ev_cap = n_shard / 8;
     Counters* dc = nullptr;
     NRT_CUDA(cudaMallocAsync(&dc, sizeof(Counters), st));
+    Wave W{};
+    NRT_TRY(alloc_wave(W, n_shard, st));
+    W.n_alive = dc->n_alive;
+    W.ctr = dc->ctr;
     nrt_coarse_rec* raw = nullptr;
     nrt_event_rec* ev = nullptr;
     Counters hc{};
@@ -512,35 +858,34 @@ nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw
         P.ev_cap = ev_cap;
         P.ev_n = &dc->ev_n;
         P.bounces = &dc->bounces;
-        const int sms = sm_count(s->device);
-        uint64_t blocks = (n_shard + 127) / 128;
-        const uint64_t maxb = (uint64_t)sms * 16;
-        if (blocks > maxb) blocks = maxb;
-        if (blocks < 1) blocks = 1;
         P.counters = &dc->tests;
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        cudaEventRecord(e0, st);
-        if (a.desc.counters) k_primary<true><<<(unsigned)blocks, 128, 0, st>>>(P, n_shard);
-        else k_primary<false><<<(unsigned)blocks, 128, 0, st>>>(P, n_shard);
-        ::nrt::count_launch();
-        cudaEventRecord(e1, st);
-        NRT_CUDA(cudaGetLastError());
+        if (n_shard > 0) {
+            unsigned gb = (unsigned)((n_shard + 255) / 256);
+            if (gb > (unsigned)sm_count(s->device) * 16) gb = (unsigned)sm_count(s->device) * 16;
+            k_gen_primary<<<gb, 256, 0, st>>>(P, W, n_shard);
+            ::nrt::count_launch();
+            NRT_TRY(run_bounces(P, W, a.max_refl + 1, s->device, a.desc.counters != 0,
+                                &stats->ms_kernel, st));
+        }
         NRT_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, st));
         NRT_CUDA(cudaStreamSynchronize(st));
-        cudaEventElapsedTime(&stats->ms_kernel, e0, e1);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
         stats->tests = hc.tests;
         stats->cells = hc.cells;
         stats->nonempty = hc.nonempty;
+        if (hc.raw_n > s->hint_raw) s->hint_raw = hc.raw_n;
+        if (hc.ev_n > s->hint_ev) s->hint_ev = hc.ev_n;
+        if (hc.raw_n > g_hint_raw.load()) g_hint_raw.store(hc.raw_n);
+        if (hc.ev_n > g_hint_ev.load()) g_hint_ev.store(hc.ev_n);
+        if (getenv("NRT_PHASES"))
+            fprintf(stderr, "[nrt] primary attempt %d: raw %llu/%llu events %llu/%llu\n", attempt,
+                    hc.raw_n, raw_cap, hc.ev_n, ev_cap);
         if (hc.raw_n <= raw_cap && hc.ev_n <= ev_cap) break;
         cudaFreeAsync(raw, st);
         cudaFreeAsync(ev, st);
         raw_cap = hc.raw_n > raw_cap ? hc.raw_n : raw_cap;
         ev_cap = hc.ev_n > ev_cap ? hc.ev_n : ev_cap;
     }
+    free_wave(W, st);
     cudaFreeAsync(dc, st);
     *raw_out = raw;
     *n_raw = (int64_t)hc.raw_n;
@@ -562,7 +907,8 @@ nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev
     unsigned int *cnt = nullptr, *off = nullptr;
     NRT_CUDA(cudaMallocAsync(&cnt, (n_ev + 1) * 4, st));
     NRT_CUDA(cudaMallocAsync(&off, (n_ev + 1) * 4, st));
-    k_fan_count<<<(unsigned)((n_ev + 127) / 128), 128, 0, st>>>(P, ev, n_ev, cnt); ::nrt::count_launch();
+    k_fan_count<<<(unsigned)((n_ev + 127) / 128), 128, 0, st>>>(P, ev, n_ev, cnt);
+    ::nrt::count_launch();
     NRT_CUDA(cudaGetLastError());
     NRT_CUDA(cudaMemsetAsync(cnt + n_ev, 0, 4, st));
     size_t tb = 0;
@@ -577,9 +923,14 @@ nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev
     *n_fan_rays = total;
     Counters* dc = nullptr;
     NRT_CUDA(cudaMallocAsync(&dc, sizeof(Counters), st));
-    unsigned long long raw_cap = 1 << 16;
+    if (g_hint_fan.load() > s->hint_fan) s->hint_fan = g_hint_fan.load();
+    unsigned long long raw_cap = s->hint_fan + s->hint_fan / 4 + 1024;
     nrt_coarse_rec* raw = nullptr;
     Counters hc{};
+    Wave W{};
+    if (total > 0) NRT_TRY(alloc_wave(W, total, st));
+    W.n_alive = dc->n_alive;
+    W.ctr = dc->ctr;
     for (int attempt = 0; attempt < 3 && total > 0; ++attempt) {
         NRT_CUDA(cudaMallocAsync(&raw, raw_cap * sizeof(nrt_coarse_rec), st));
         NRT_CUDA(cudaMemsetAsync(dc, 0, sizeof(Counters), st));
@@ -590,31 +941,26 @@ nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev
         P.ev_cap = 0;
         P.ev_n = &dc->ev_n;
         P.bounces = &dc->bounces;
-        const int sms = sm_count(s->device);
-        uint64_t blocks = (total + 127) / 128;
-        if (blocks > (uint64_t)sms * 16) blocks = (uint64_t)sms * 16;
         P.counters = &dc->tests;
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        cudaEventRecord(e0, st);
-        if (a.desc.counters) k_fans<true><<<(unsigned)blocks, 128, 0, st>>>(P, ev, n_ev, off, total);
-        else k_fans<false><<<(unsigned)blocks, 128, 0, st>>>(P, ev, n_ev, off, total);
+        unsigned gb = (total + 255) / 256;
+        if (gb > (unsigned)sm_count(s->device) * 16) gb = (unsigned)sm_count(s->device) * 16;
+        k_gen_fans<<<gb, 256, 0, st>>>(P, W, ev, n_ev, off, total);
         ::nrt::count_launch();
-        cudaEventRecord(e1, st);
-        NRT_CUDA(cudaGetLastError());
+        // fans need at most max_refl + 1 segments (budget <= max_refl)
+        NRT_TRY(run_bounces(P, W, a.max_refl + 1, s->device, a.desc.counters != 0,
+                            &stats->ms_kernel, st));
         NRT_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, st));
         NRT_CUDA(cudaStreamSynchronize(st));
-        cudaEventElapsedTime(&stats->ms_kernel, e0, e1);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
         stats->tests = hc.tests;
         stats->cells = hc.cells;
         stats->nonempty = hc.nonempty;
+        if (hc.raw_n > s->hint_fan) s->hint_fan = hc.raw_n;
+        if (hc.raw_n > g_hint_fan.load()) g_hint_fan.store(hc.raw_n);
         if (hc.raw_n <= raw_cap) break;
         cudaFreeAsync(raw, st);
         raw_cap = hc.raw_n;
     }
+    if (total > 0) free_wave(W, st);
     cudaFreeAsync(dc, st);
     cudaFreeAsync(cnt, st);
     cudaFreeAsync(off, st);
@@ -630,27 +976,18 @@ nrt_status debug_trace(nrt_scene s, const LaunchArgs& a, const uint64_t* ids, in
     TP P = make_tp(s, a);
     uint64_t* dids = nullptr;
     int64_t* dh = nullptr;
-    Counters* dc = nullptr;
     const size_t nseg = (size_t)a.max_refl + 1;
     NRT_CUDA(cudaMallocAsync(&dids, n * 8, st));
     NRT_CUDA(cudaMallocAsync(&dh, n * nseg * 8, st));
-    NRT_CUDA(cudaMallocAsync(&dc, sizeof(Counters), st));
-    NRT_CUDA(cudaMemsetAsync(dc, 0, sizeof(Counters), st));
     NRT_CUDA(cudaMemcpyAsync(dids, ids, n * 8, cudaMemcpyHostToDevice, st));
-    P.raw = nullptr;
-    P.raw_cap = 0;
-    P.raw_n = &dc->raw_n;
-    P.ev_n = &dc->ev_n;
-    P.bounces = &dc->bounces;
-    P.counters = &dc->tests;
     P.hit_out = dh;
-    k_debug<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(P, dids, n); ::nrt::count_launch();
+    k_debug<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(P, dids, n);
+    ::nrt::count_launch();
     NRT_CUDA(cudaGetLastError());
     NRT_CUDA(cudaMemcpyAsync(hit_ids, dh, n * nseg * 8, cudaMemcpyDeviceToHost, st));
     NRT_CUDA(cudaStreamSynchronize(st));
     cudaFreeAsync(dids, st);
     cudaFreeAsync(dh, st);
-    cudaFreeAsync(dc, st);
     return NRT_OK;
 }
 

@@ -170,7 +170,7 @@ __global__ void k_records(Grid g, const uint64_t* keys, const unsigned int* ids,
     if (k >= nref) return;
     unsigned id = ids[k];
     float4 p = sp[id], nv = sn[id];
-    rec[2 * k] = make_float4(p.x, p.y, p.z, p.w * p.w);
+    rec[2 * k] = make_float4(p.x, p.y, p.z, p.w);  // record carries r; the test squares it as the definition does
     rec[2 * k + 1] = make_float4(nv.x, nv.y, nv.z, __uint_as_float(id));
     uint64_t key = keys[k];
     bool first = (k == 0) || keys[k - 1] != key;
@@ -181,6 +181,43 @@ __global__ void k_records(Grid g, const uint64_t* keys, const unsigned int* ids,
         if (first) cell[lin].x = (unsigned)k;
         if (last) cell[lin].y = (unsigned)(k + 1);
     }
+}
+
+// Chebyshev distance field.  f = 0 on non-empty cells, kSkipCap elsewhere; one pass per axis:
+// g(x) = min_{|s| <= cap} max(|s|, f(x + s e_axis)) — exact for the L-infinity metric because
+// max distributes over min.
+constexpr int kSkipCap = 24;
+__global__ void k_occ(const uint2* cell, int64_t ncell, unsigned char* f) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    const uint2 r = cell[c];
+    f[c] = r.y > r.x ? 0 : kSkipCap;
+}
+__global__ void k_cheb_pass(const unsigned char* f, unsigned char* g, int nx, int ny, int nz,
+                            int axis) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t ncell = (int64_t)nx * ny * nz;
+    if (c >= ncell) return;
+    const int x = (int)(c % nx), y = (int)((c / nx) % ny), z = (int)(c / ((int64_t)nx * ny));
+    const int pos = axis == 0 ? x : (axis == 1 ? y : z);
+    const int len = axis == 0 ? nx : (axis == 1 ? ny : nz);
+    const int64_t stride = axis == 0 ? 1 : (axis == 1 ? nx : (int64_t)nx * ny);
+    int best = f[c];
+    for (int s = 1; s < best && s <= kSkipCap; ++s) {
+        int m = kSkipCap;
+        if (pos - s >= 0) m = min(m, (int)f[c - s * stride]);
+        if (pos + s < len) m = min(m, (int)f[c + s * stride]);
+        best = min(best, max(s, m));
+    }
+    g[c] = (unsigned char)best;
+}
+__global__ void k_pack_skip(uint2* cell, int64_t ncell, const unsigned char* f) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    const uint2 r = cell[c];
+    if (r.y > r.x) return;
+    const unsigned D = f[c] < 1 ? 1u : (unsigned)f[c];
+    cell[c] = make_uint2(D, D);  // empty: x == y == Chebyshev distance to non-empty (>= 1)
 }
 
 template <class T>
@@ -259,6 +296,12 @@ static nrt_status build_impl(const nrt_scene_desc* D, nrt_scene S, cudaStream_t 
         bmax[a] = ord2f(h.bounds[3 + a]);
     }
     memcpy(&S->r_max, &h.rmax, 4);
+    {
+        // FP32 error of |q| (either form) is a few ulp of the coordinates; 25x margin
+        float ext = 0.0f;
+        for (int a = 0; a < 3; ++a) ext = fmaxf(ext, fmaxf(fabsf(bmin[a]), fabsf(bmax[a])));
+        S->slack = fmaxf(1e-4f, 4e-6f * ext);
+    }
     if (!dl) {  // R6 pseudo-labels
         int lx = (int)floorf((bmax[0] - bmin[0]) / 0.5f) + 1;
         int ly = (int)floorf((bmax[1] - bmin[1]) / 0.5f) + 1;
@@ -356,6 +399,23 @@ static nrt_status build_impl(const nrt_scene_desc* D, nrt_scene S, cudaStream_t 
     cudaFreeAsync(v1, st);
     cudaFreeAsync(cnt, st);
     cudaFreeAsync(off, st);
+    // ---- empty-space skip field (the paper's "march distance", P:154 / P:281): Chebyshev
+    // distance (in cells, capped) from every empty cell to the nearest non-empty one, computed
+    // exactly by three separable min-max passes, then packed into empty entries as (D, D).
+    {
+        unsigned char *f0 = nullptr, *f1 = nullptr;
+        NRT_TRY(dmalloc(&f0, ncell, st));
+        NRT_TRY(dmalloc(&f1, ncell, st));
+        const unsigned cb = (unsigned)((ncell + 255) / 256);
+        k_occ<<<cb, 256, 0, st>>>(S->cell, ncell, f0); ::nrt::count_launch();
+        k_cheb_pass<<<cb, 256, 0, st>>>(f0, f1, g.nx, g.ny, g.nz, 2); ::nrt::count_launch();
+        k_cheb_pass<<<cb, 256, 0, st>>>(f1, f0, g.nx, g.ny, g.nz, 1); ::nrt::count_launch();
+        k_cheb_pass<<<cb, 256, 0, st>>>(f0, f1, g.nx, g.ny, g.nz, 0); ::nrt::count_launch();
+        k_pack_skip<<<cb, 256, 0, st>>>(S->cell, ncell, f1); ::nrt::count_launch();
+        NRT_CUDA(cudaGetLastError());
+        cudaFreeAsync(f0, st);
+        cudaFreeAsync(f1, st);
+    }
     // labels array (int) for the history
     {
         // sn.w holds the label bits; extract with a tiny kernel-free trick: copy strided
@@ -378,6 +438,7 @@ nrt_status scene_build(const nrt_scene_desc* D, nrt_scene* out) {
     if (D->n_edges < 0 || (D->n_edges > 0 && !D->edges))
         return set_error(NRT_E_INVALID, "bad edge array");
     NRT_CUDA(cudaSetDevice(D->device));
+    ensure_pool(D->device);
     cudaStream_t st = (cudaStream_t)D->stream;
     nrt_scene S = new nrt_scene_s();
     S->device = D->device;
@@ -411,6 +472,8 @@ nrt_status scene_build(const nrt_scene_desc* D, nrt_scene* out) {
         g.len = len;
         g.n_exp = E.n_exp;
         g.label = E.label;
+        for (int k = 0; k < 3; ++k) g.c[k] = 0.5f * (E.a[k] + E.b[k]);
+        g.hl = 0.5f * len * 1.001f + 1e-4f;
         S->h_edges.push_back(g);
     }
     S->n_edges = D->n_edges;
