@@ -102,6 +102,7 @@ struct DevEdge {
     float n_exp;
     int32_t label;
     float c[3], hl;  // bounding sphere (centre, half length) for conservative culling
+    float b_[3];     // the input end point b (refinement works in FP64 from a and b)
 };
 
 struct Hist {

@@ -473,6 +473,7 @@ nrt_status scene_build(const nrt_scene_desc* D, nrt_scene* out) {
         g.n_exp = E.n_exp;
         g.label = E.label;
         for (int k = 0; k < 3; ++k) g.c[k] = 0.5f * (E.a[k] + E.b[k]);
+        for (int k = 0; k < 3; ++k) g.b_[k] = E.b[k];
         g.hl = 0.5f * len * 1.001f + 1e-4f;
         S->h_edges.push_back(g);
     }
