@@ -1,4 +1,4 @@
-// refine.cu — A9-A10: batched path refinement, one warp per coarse path (FP64).
+// refine.cu — A9-A10: batched path refinement (FP64), one thread block (NW warps) per path.
 //
 // The refined path is the root of the residual of DESIGN.md §5 (readings R18-R28):
 //   reflection k: r_k = [g.u, g.v, f_sdf] with the MLS surface of Eqs. 1-4 over
@@ -9,15 +9,24 @@
 // -(J^T J + lam I)^-1 J^T r, Armijo backtracking (Eq. 12 form, R24), converged at |D|_inf <
 // tol.  Then validity (R25): on-edge, same side, support, FP64 visibility; delay = L/c (R26).
 //
-// B200 mapping: a warp owns a path.  Per reflection vertex the warp gathers once the
-// candidate surfels (same label, within Rq + M of a gather centre) from the fine grid into a
-// per-warp scratch list; every MLS evaluation then streams that list with lanes splitting the
-// candidates and a butterfly reduction of the 7 FP64 sums.  The small dense algebra lives in
-// per-warp shared memory.  Shadow rays walk the same grid with the warp splitting each cell.
+// B200 mapping.  Refinement is latency-bound (a few thousand small solves), so
+// one block of NW warps works on one path and spreads the independent pieces of each GN
+// iteration over its warps:
+//   * the 2m perturbed residuals of the Jacobian (column j on warp j mod NW);
+//   * the backtracking trials: warp w evaluates gamma = beta^(round*NW + w), and the block
+//     accepts the first trial (in sequence order) that passes Armijo — exactly the step the
+//     sequential loop would take;
+//   * the MLS sums inside a warp: lanes split the candidates, butterfly-reduce 7 FP64 sums.
+// Per reflection vertex the block gathers once (from the fine grid, home-cell dedupe, same
+// label, within rg of a gather centre) the candidate surfels into SHARED memory; an MLS
+// point farther than rg - rq from its centre falls back to a direct grid scan (same set).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -25,14 +34,16 @@ namespace nrt {
 
 namespace {
 
-constexpr int kWarps = 4;               // warps (paths in flight) per block
+#ifndef NRT_REFINE_WARPS
+#define NRT_REFINE_WARPS 8
+#endif
+constexpr int NW = NRT_REFINE_WARPS;      // warps per path
 constexpr int kMaxDim = 3 * NRT_MAX_INT;
-constexpr int kCap = 2048;              // candidate ids per vertex per warp slot
+constexpr int kCapS = 512;                // shared-memory candidates per reflection vertex
 constexpr double kC = 299792458.0;
-constexpr double kH = 1e-7;             // central-difference step (m)
+constexpr double kH = 1e-7;               // central-difference step (m)
 
 struct RP {
-    // grid (as in launch.cu)
     const uint2* cell;
     const float4* rec;
     const float4* sp;  // (p, r)
@@ -40,48 +51,19 @@ struct RP {
     float ox, oy, oz, v, inv_v, pad;
     int nx, ny, nz;
     const DevEdge* edges;
-    // problem
     const nrt_coarse_rec* in;
     int64_t n_in;
     int rank, world;
     double tx[3];
     const float* rx;
     double sigma, rq, rg, tau, cos_ex, tol, alpha, beta;
-    int max_iter;
-    // outputs
-    nrt_refined_rec* out;       // [n_in] (keep_invalid order) or compacted
+    int max_iter, nv_max;  // nv_max: reflection vertices with shared candidate storage
+    nrt_refined_rec* out;
     unsigned long long* n_out;
     int keep_invalid;
-    // scratch
-    unsigned* cand;             // [slots][NRT_MAX_INT][kCap]
-    int slots;
-    unsigned long long* work;   // path counter
+    unsigned long long* work;
+    long long* cycles;  // optional per-path latency (NRT_REFINE_TIMING diagnostics)
 };
-
-struct Vtx {  // per-vertex gather state (warp-uniform)
-    double c[3];
-    int n;
-    bool over;  // candidate list overflowed -> direct grid scan
-};
-
-struct WarpSmem {
-    double J[kMaxDim * kMaxDim];
-    double A[kMaxDim * kMaxDim];
-    double r[kMaxDim], rp[kMaxDim], rm[kMaxDim], b[kMaxDim], z[kMaxDim], zt[kMaxDim];
-    double pb[NRT_MAX_INT][3], nb[NRT_MAX_INT][3];  // MLS cache at z
-    double pbx[3], nbx[3];                           // MLS at a perturbed vertex
-    int ok;
-};
-
-__device__ __forceinline__ double ddot(const double a[3], const double b[3]) {
-    return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
-}
-
-__device__ __forceinline__ double wsum(double x) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    return x;
-}
 
 struct Path {
     int n, dim;
@@ -89,90 +71,152 @@ struct Path {
     int32_t label[NRT_MAX_INT];
     uint32_t prim[NRT_MAX_INT];
     int col[NRT_MAX_INT];
+    int slot[NRT_MAX_INT];  // shared candidate slot of a reflection vertex (-1: none)
     double nseed[NRT_MAX_INT][3];
     double ea[NRT_MAX_INT][3], ee[NRT_MAX_INT][3], elen[NRT_MAX_INT];
     double rxp[3];
 };
 
-// ---- candidate gather: home-cell records of the label within rg of c (superset of every
-// neighbourhood the GN iterations evaluate while |x - c| <= rg - rq)
-__device__ void gather(const RP& P, int32_t label, const double c[3], unsigned* list, Vtx& V,
-                       int lane) {
-    V.c[0] = c[0];
-    V.c[1] = c[1];
-    V.c[2] = c[2];
-    V.over = false;
+struct Vtx {
+    double c[3];
+    int n;       // candidates in shared memory
+    int direct;  // 1: no usable list (overflow) -> direct scans
+};
+
+struct Trial {  // one warp's residual evaluation result
+    double r[kMaxDim];
+    double pb[NRT_MAX_INT][3], nb[NRT_MAX_INT][3];
+    double f;
+    int ok;
+};
+
+struct Smem {
+    double J[kMaxDim * kMaxDim];
+    double A[kMaxDim * kMaxDim];
+    double z[kMaxDim], r[kMaxDim], b[kMaxDim];
+    double pb[NRT_MAX_INT][3], nb[NRT_MAX_INT][3];
+    Trial tr[NW];
+    Vtx V[NRT_MAX_INT];
+    int flag[NW];
+    double dval;
+    unsigned long long q;
+};
+
+__device__ __forceinline__ double ddot(const double a[3], const double b[3]) {
+    return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
+}
+__device__ __forceinline__ double wsum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// candidate storage of slot s: p (xyz) and n (xyz) as floats, kCapS entries
+__device__ __forceinline__ float* cand_ptr(float* cand, int s) { return cand + (size_t)s * kCapS * 6; }
+
+typedef cub::BlockScan<int, 32 * NW> BlockScanT;
+
+__device__ unsigned long long g_dbg[8];  // diagnostics (NRT_REFINE_TIMING): MLS list/direct, LS rounds, gathers
+
+// does record k of cell (ci,cj,ck) belong to the candidate set around c?  (home cell, label,
+// distance) -> surfel data
+__device__ __forceinline__ bool cand_match(const RP& P, unsigned k, int ci, int cj, int ck,
+                                           int32_t label, const double c[3], double rg2, float4& A,
+                                           float4& nv) {
+    A = __ldg(&P.rec[2 * k]);
+    const double dx = (double)A.x - c[0], dy = (double)A.y - c[1], dz = (double)A.z - c[2];
+    if (dx * dx + dy * dy + dz * dz > rg2) return false;
+    const int hx = (int)floorf((A.x - P.ox) * P.inv_v), hy = (int)floorf((A.y - P.oy) * P.inv_v),
+              hz = (int)floorf((A.z - P.oz) * P.inv_v);
+    if (hx != ci || hy != cj || hz != ck) return false;
+    const float4 B = __ldg(&P.rec[2 * k + 1]);
+    nv = __ldg(&P.sn[__float_as_uint(B.w)]);
+    return __float_as_int(nv.w) == label;
+}
+
+// ---- block-cooperative gather of vertex k's candidates around c (home-cell dedupe).
+// Deterministic order: cells in linear order, each round of blockDim cells compacted by a
+// block prefix sum (so the MLS sums, hence the results, are bitwise reproducible).
+__device__ void gather(const RP& P, int32_t label, const double c[3], float* list, Vtx& V,
+                       int* counter, typename BlockScanT::TempStorage& scan) {
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        V.c[0] = c[0];
+        V.c[1] = c[1];
+        V.c[2] = c[2];
+        *counter = 0;
+        atomicAdd(&g_dbg[3], 1ull);
+    }
+    __syncthreads();
     const float lo[3] = {(float)(c[0] - P.rg), (float)(c[1] - P.rg), (float)(c[2] - P.rg)};
     const float hi[3] = {(float)(c[0] + P.rg), (float)(c[1] + P.rg), (float)(c[2] + P.rg)};
-    int i0 = max(0, (int)floorf((lo[0] - P.ox) * P.inv_v)), i1 = min(P.nx - 1, (int)floorf((hi[0] - P.ox) * P.inv_v));
-    int j0 = max(0, (int)floorf((lo[1] - P.oy) * P.inv_v)), j1 = min(P.ny - 1, (int)floorf((hi[1] - P.oy) * P.inv_v));
-    int k0 = max(0, (int)floorf((lo[2] - P.oz) * P.inv_v)), k1 = min(P.nz - 1, (int)floorf((hi[2] - P.oz) * P.inv_v));
+    const int i0 = max(0, (int)floorf((lo[0] - P.ox) * P.inv_v)), i1 = min(P.nx - 1, (int)floorf((hi[0] - P.ox) * P.inv_v));
+    const int j0 = max(0, (int)floorf((lo[1] - P.oy) * P.inv_v)), j1 = min(P.ny - 1, (int)floorf((hi[1] - P.oy) * P.inv_v));
+    const int k0 = max(0, (int)floorf((lo[2] - P.oz) * P.inv_v)), k1 = min(P.nz - 1, (int)floorf((hi[2] - P.oz) * P.inv_v));
     const int nxr = i1 - i0 + 1, nyr = j1 - j0 + 1, nzr = k1 - k0 + 1;
     const int ncells = (nxr > 0 && nyr > 0 && nzr > 0) ? nxr * nyr * nzr : 0;
     const double rg2 = P.rg * P.rg;
-    int count = 0;
-    for (int base = 0; base < ncells; base += 32) {
-        const int q = base + lane;
-        unsigned mine[48];
-        int nm = 0;
-        bool spill = false;
+    for (int base = 0; base < ncells; base += blockDim.x) {
+        const int q = base + tid;
+        int ci = 0, cj = 0, ck = 0;
+        uint2 rg = make_uint2(0, 0);
+        int cnt = 0;
         if (q < ncells) {
-            const int ci = i0 + q % nxr, cj = j0 + (q / nxr) % nyr, ck = k0 + q / (nxr * nyr);
-            const uint2 rg = __ldg(&P.cell[ci + P.nx * (cj + P.ny * ck)]);
-            if (rg.y > rg.x) {
+            ci = i0 + q % nxr;
+            cj = j0 + (q / nxr) % nyr;
+            ck = k0 + q / (nxr * nyr);
+            rg = __ldg(&P.cell[ci + P.nx * (cj + P.ny * ck)]);
+            if (rg.y > rg.x)
                 for (unsigned k = rg.x; k < rg.y; ++k) {
-                    const float4 A = __ldg(&P.rec[2 * k]);
-                    const float4 B = __ldg(&P.rec[2 * k + 1]);
-                    const unsigned id = __float_as_uint(B.w);
-                    const float4 nv = __ldg(&P.sn[id]);
-                    if (__float_as_int(nv.w) != label) continue;
-                    // home cell of p: count each surfel once
-                    const int hx = (int)floorf((A.x - P.ox) * P.inv_v), hy = (int)floorf((A.y - P.oy) * P.inv_v),
-                              hz = (int)floorf((A.z - P.oz) * P.inv_v);
-                    if (hx != ci || hy != cj || hz != ck) continue;
-                    const double dx = (double)A.x - c[0], dy = (double)A.y - c[1], dz = (double)A.z - c[2];
-                    if (dx * dx + dy * dy + dz * dz > rg2) continue;
-                    if (nm < 48) mine[nm++] = id;
-                    else spill = true;
+                    float4 A, nv;
+                    cnt += cand_match(P, k, ci, cj, ck, label, c, rg2, A, nv);
+                }
+        }
+        int off = 0, tot = 0;
+        BlockScanT(scan).ExclusiveSum(cnt, off, tot);
+        const int start = *counter;
+        if (cnt)
+            for (unsigned k = rg.x, w = 0; k < rg.y; ++k) {
+                float4 A, nv;
+                if (!cand_match(P, k, ci, cj, ck, label, c, rg2, A, nv)) continue;
+                const int at = start + off + (int)w++;
+                if (at < kCapS) {
+                    float* e = list + 6 * at;
+                    e[0] = A.x;
+                    e[1] = A.y;
+                    e[2] = A.z;
+                    e[3] = nv.x;
+                    e[4] = nv.y;
+                    e[5] = nv.z;
                 }
             }
-        }
-        // warp-ordered append (deterministic for a given grid)
-        int pre = nm;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(0xffffffffu, pre, o);
-            if (lane >= o) pre += t;
-        }
-        const int tot = __shfl_sync(0xffffffffu, pre, 31);
-        const int start = count + pre - nm;
-        for (int m = 0; m < nm; ++m)
-            if (start + m < kCap) list[start + m] = mine[m];
-        count += tot;
-        if (__any_sync(0xffffffffu, spill)) V.over = true;
+        __syncthreads();
+        if (tid == 0) *counter = start + tot;
+        __syncthreads();
     }
-    if (count > kCap) V.over = true;
-    V.n = count < kCap ? count : kCap;
-    __syncwarp();
+    if (tid == 0) {
+        V.direct = *counter > kCapS;
+        V.n = V.direct ? 0 : *counter;
+    }
+    __syncthreads();
 }
 
-// MLS (Eqs. 1-4) at x: sums over the cached candidates (or a direct scan on overflow)
-__device__ bool mls(const RP& P, const Path& D, int k, const double x[3], const unsigned* list,
+// ---- MLS (Eqs. 1-4) at x, one warp.  From the shared list when x lies in the safe ball of
+// the gather centre, else by a direct scan of the grid (home-cell dedupe, same label).
+__device__ bool mls(const RP& P, const Path& D, int k, const double x[3], const float* list,
                     const Vtx& V, double pb[3], double nb[3], int lane) {
     const double inv2s2 = 1.0 / (2.0 * P.sigma * P.sigma);
     const double r2 = (4.0 * P.sigma) * (4.0 * P.sigma);
-    double W = 0, Px = 0, Py = 0, Pz = 0, Nx = 0, Ny = 0, Nz = 0;
     const double* ns = D.nseed[k];
-    for (int j = lane; j < V.n; j += 32) {
-        const unsigned id = list[j];
-        const float4 pa = __ldg(&P.sp[id]);
-        const float4 na = __ldg(&P.sn[id]);
-        const double p0 = pa.x, p1 = pa.y, p2 = pa.z;
+    double W = 0, Px = 0, Py = 0, Pz = 0, Nx = 0, Ny = 0, Nz = 0;
+    const double dxc = x[0] - V.c[0], dyc = x[1] - V.c[1], dzc = x[2] - V.c[2];
+    const bool use_list = !V.direct && sqrt(dxc * dxc + dyc * dyc + dzc * dzc) <= P.rg - P.rq;
+    if (P.cycles && lane == 0) atomicAdd(&g_dbg[use_list ? 0 : 1], 1ull);
+    auto acc = [&](double p0, double p1, double p2, double n0, double n1, double n2) {
         const double d0 = p0 - x[0], d1 = p1 - x[1], d2 = p2 - x[2];
         const double dd = (d0 * d0 + d1 * d1) + d2 * d2;
-        if (dd > r2) continue;
+        if (dd > r2) return;
         const double w = exp(-dd * inv2s2);
-        const double n0 = na.x, n1 = na.y, n2 = na.z;
         const double sg = ((n0 * ns[0] + n1 * ns[1]) + n2 * ns[2]) < 0.0 ? -1.0 : 1.0;
         W += w;
         Px += w * p0;
@@ -181,6 +225,55 @@ __device__ bool mls(const RP& P, const Path& D, int k, const double x[3], const 
         Nx += w * sg * n0;
         Ny += w * sg * n1;
         Nz += w * sg * n2;
+    };
+    if (use_list) {
+        for (int j = lane; j < V.n; j += 32) {
+            const float* e = list + 6 * j;
+            acc(e[0], e[1], e[2], e[3], e[4], e[5]);
+        }
+    } else {
+        const double R = 4.0 * P.sigma;
+        const float lo[3] = {(float)(x[0] - R), (float)(x[1] - R), (float)(x[2] - R)};
+        const float hi[3] = {(float)(x[0] + R), (float)(x[1] + R), (float)(x[2] + R)};
+        const int i0 = max(0, (int)floorf((lo[0] - P.ox) * P.inv_v)), i1 = min(P.nx - 1, (int)floorf((hi[0] - P.ox) * P.inv_v));
+        const int j0 = max(0, (int)floorf((lo[1] - P.oy) * P.inv_v)), j1 = min(P.ny - 1, (int)floorf((hi[1] - P.oy) * P.inv_v));
+        const int k0 = max(0, (int)floorf((lo[2] - P.oz) * P.inv_v)), k1 = min(P.nz - 1, (int)floorf((hi[2] - P.oz) * P.inv_v));
+        // cell headers 32 at a time; the warp walks the non-empty ones (ballot) with lanes
+        // splitting each cell's records; distance and home cell are decided from the first
+        // float4 before the dependent loads of the normal and label
+        const int nxr = i1 - i0 + 1, nyr = j1 - j0 + 1, nzr = k1 - k0 + 1;
+        const int ncells = (nxr > 0 && nyr > 0 && nzr > 0) ? nxr * nyr * nzr : 0;
+        for (int base = 0; base < ncells; base += 32) {
+            const int q0 = base + lane;
+            int ci = 0, cj = 0, ck = 0;
+            uint2 rg = make_uint2(0, 0);
+            if (q0 < ncells) {
+                ci = i0 + q0 % nxr;
+                cj = j0 + (q0 / nxr) % nyr;
+                ck = k0 + q0 / (nxr * nyr);
+                rg = __ldg(&P.cell[ci + P.nx * (cj + P.ny * ck)]);
+            }
+            unsigned live = __ballot_sync(0xffffffffu, rg.y > rg.x);
+            while (live) {
+                const int src = __ffs(live) - 1;
+                live &= live - 1;
+                const unsigned s0 = __shfl_sync(0xffffffffu, rg.x, src), s1 = __shfl_sync(0xffffffffu, rg.y, src);
+                const int cx = __shfl_sync(0xffffffffu, ci, src), cy = __shfl_sync(0xffffffffu, cj, src),
+                          cz = __shfl_sync(0xffffffffu, ck, src);
+                for (unsigned q = s0 + lane; q < s1; q += 32) {
+                    const float4 A = __ldg(&P.rec[2 * q]);
+                    const double d0 = (double)A.x - x[0], d1 = (double)A.y - x[1], d2 = (double)A.z - x[2];
+                    if ((d0 * d0 + d1 * d1) + d2 * d2 > r2) continue;
+                    const int hx = (int)floorf((A.x - P.ox) * P.inv_v), hy = (int)floorf((A.y - P.oy) * P.inv_v),
+                              hz = (int)floorf((A.z - P.oz) * P.inv_v);
+                    if (hx != cx || hy != cy || hz != cz) continue;
+                    const float4 B = __ldg(&P.rec[2 * q + 1]);
+                    const float4 nv = __ldg(&P.sn[__float_as_uint(B.w)]);
+                    if (__float_as_int(nv.w) != D.label[k]) continue;
+                    acc(A.x, A.y, A.z, nv.x, nv.y, nv.z);
+                }
+            }
+        }
     }
     W = wsum(W);
     Px = wsum(Px);
@@ -244,16 +337,6 @@ __device__ __forceinline__ void vpoint(const RP& P, const Path& D, const double*
     }
 }
 
-// MLS of vertex k at x, re-gathering when x left the safe ball of the gather centre
-__device__ bool vertex_mls(const RP& P, const Path& D, int k, const double x[3], unsigned* list,
-                           Vtx& V, double pb[3], double nb[3], int lane) {
-    const double dx = x[0] - V.c[0], dy = x[1] - V.c[1], dz = x[2] - V.c[2];
-    if (sqrt(dx * dx + dy * dy + dz * dz) > P.rg - P.rq || V.over) gather(P, D.label[k], x, list, V, lane);
-    if (V.over) return false;  // neighbourhood larger than the scratch: reported as NO_SUPPORT
-    return mls(P, D, k, x, list, V, pb, nb, lane);
-}
-
-// residual components of vertex k (writes r[col..]), given its MLS (reflection)
 __device__ bool vertex_residual(const RP& P, const Path& D, const double* z, int k, const double* pb,
                                 const double* nb, double* r) {
     double x[3], a[3], c[3];
@@ -279,27 +362,35 @@ __device__ bool vertex_residual(const RP& P, const Path& D, const double* z, int
     return true;
 }
 
-// full residual at z (MLS of every reflection vertex recomputed; cache updated)
-__device__ bool residual_all(const RP& P, const Path& D, const double* z, double* r, unsigned* lists,
-                             Vtx* V, double (*pb)[3], double (*nb)[3], int lane) {
-    for (int k = 0; k < D.n; ++k) {
+// one warp: full residual at z into T (MLS of every reflection vertex recomputed)
+__device__ void residual_all(const RP& P, const Path& D, const double* z, const float* cand,
+                             const Vtx* V, Trial& T, int lane) {
+    bool ok = true;
+    double pb[3], nb[3];
+    for (int k = 0; k < D.n && ok; ++k) {
         if (D.kind[k] != 0) continue;
         double x[3];
         vpoint(P, D, z, k, x);
-        if (!vertex_mls(P, D, k, x, lists + (size_t)k * kCap, V[k], pb[k], nb[k], lane)) return false;
+        ok = mls(P, D, k, x, cand_ptr(const_cast<float*>(cand), D.slot[k]), V[D.slot[k]], pb, nb, lane);
+        if (ok && lane == 0)
+            for (int a = 0; a < 3; ++a) {
+                T.pb[k][a] = pb[a];
+                T.nb[k][a] = nb[a];
+            }
     }
-    for (int k = 0; k < D.n; ++k)
-        if (!vertex_residual(P, D, z, k, pb[k], nb[k], r)) return false;
-    return true;
+    __syncwarp();
+    if (ok && lane == 0) {
+        for (int k = 0; k < D.n && ok; ++k) ok = vertex_residual(P, D, z, k, T.pb[k], T.nb[k], T.r);
+        double f = 0;
+        for (int i = 0; i < D.dim; ++i) f += T.r[i] * T.r[i];
+        T.f = f;
+    }
+    if (lane == 0) T.ok = ok;
+    __syncwarp();
 }
 
-__device__ double sq(const double* r, int m) {
-    double s = 0;
-    for (int i = 0; i < m; ++i) s += r[i] * r[i];
-    return s;
-}
-
-// FP64 occlusion of segment x0 -> x1 (R25 d): warp walks the grid cells the segment crosses
+// FP64 occlusion of segment x0 -> x1 (R25 d): one warp walks the grid cells the segment
+// crosses, lanes split each cell's records, any-hit by ballot
 __device__ bool occluded(const RP& P, const double x0[3], const double x1[3], const double* lam0,
                          int n0, const double* lam1, int n1, int lane) {
     const double dv[3] = {x1[0] - x0[0], x1[1] - x0[1], x1[2] - x0[2]};
@@ -356,350 +447,438 @@ __device__ bool occluded(const RP& P, const double x0[3], const double x1[3], co
     }
 }
 
-__device__ bool supported(const RP& P, int32_t label, const double x[3], const unsigned* list,
-                          const Vtx& V, int lane) {
+// support (R25 c) over every same-label surfel near x: direct scan, one warp
+__device__ bool supported(const RP& P, int32_t label, const double x[3], int lane) {
+    const double R = (double)P.rq;
+    const float lo[3] = {(float)(x[0] - R), (float)(x[1] - R), (float)(x[2] - R)};
+    const float hi[3] = {(float)(x[0] + R), (float)(x[1] + R), (float)(x[2] + R)};
+    const int i0 = max(0, (int)floorf((lo[0] - P.ox) * P.inv_v)), i1 = min(P.nx - 1, (int)floorf((hi[0] - P.ox) * P.inv_v));
+    const int j0 = max(0, (int)floorf((lo[1] - P.oy) * P.inv_v)), j1 = min(P.ny - 1, (int)floorf((hi[1] - P.oy) * P.inv_v));
+    const int k0 = max(0, (int)floorf((lo[2] - P.oz) * P.inv_v)), k1 = min(P.nz - 1, (int)floorf((hi[2] - P.oz) * P.inv_v));
     bool s = false;
-    for (int j = lane; j < V.n; j += 32) {
-        const unsigned id = list[j];
-        const float4 pa = __ldg(&P.sp[id]);
-        const float4 na = __ldg(&P.sn[id]);
-        const double w[3] = {x[0] - pa.x, x[1] - pa.y, x[2] - pa.z};
-        const double n[3] = {na.x, na.y, na.z};
-        const double r = pa.w;
-        if (fabs(ddot(w, n)) <= P.tau && ddot(w, w) <= r * r + P.tau * P.tau) s = true;
+    const int nxr = i1 - i0 + 1, nyr = j1 - j0 + 1, nzr = k1 - k0 + 1;
+    const int ncells = (nxr > 0 && nyr > 0 && nzr > 0) ? nxr * nyr * nzr : 0;
+    for (int q0 = lane; q0 < ncells && !s; q0 += 32) {
+        const int ci = i0 + q0 % nxr, cj = j0 + (q0 / nxr) % nyr, ck = k0 + q0 / (nxr * nyr);
+        const uint2 rg = __ldg(&P.cell[ci + P.nx * (cj + P.ny * ck)]);
+        for (unsigned q = rg.x; q < rg.y && rg.y > rg.x; ++q) {
+            const float4 A = __ldg(&P.rec[2 * q]);
+            const float4 B = __ldg(&P.rec[2 * q + 1]);
+            const float4 nv = __ldg(&P.sn[__float_as_uint(B.w)]);
+            if (__float_as_int(nv.w) != label) continue;
+            const double w[3] = {x[0] - A.x, x[1] - A.y, x[2] - A.z};
+            const double n[3] = {B.x, B.y, B.z};
+            const double r = A.w;
+            if (fabs(ddot(w, n)) <= P.tau && ddot(w, w) <= r * r + P.tau * P.tau) {
+                s = true;
+                break;
+            }
+        }
     }
     return __any_sync(0xffffffffu, s);
 }
 
-__global__ void __launch_bounds__(32 * kWarps) k_refine(RP P) {
-    __shared__ WarpSmem smem[kWarps];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpSmem& S = smem[wid];
-    const int slot = blockIdx.x * kWarps + wid;
-    unsigned* lists = P.cand + (size_t)slot * NRT_MAX_INT * kCap;
+__global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    Smem& S = *reinterpret_cast<Smem*>(dyn);
+    float* cand = reinterpret_cast<float*>(dyn + ((sizeof(Smem) + 15) & ~size_t(15)));
+    __shared__ int counter;
+    __shared__ typename BlockScanT::TempStorage scan;
+    const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     const int64_t n_mine = P.n_in > P.rank ? (P.n_in - P.rank + P.world - 1) / P.world : 0;
     for (;;) {
-        unsigned long long q = 0;
-        if (lane == 0) q = atomicAdd(P.work, 1ull);
-        q = __shfl_sync(0xffffffffu, q, 0);
+        const long long t_start = clock64();
+        if (tid == 0) S.q = atomicAdd(P.work, 1ull);
+        __syncthreads();
+        const unsigned long long q = S.q;
+        __syncthreads();
         if ((int64_t)q >= n_mine) break;
-        const int64_t pi = P.rank + (int64_t)q * P.world;
+        // hand out the paths from the end of the key order (most interactions first) so the
+        // expensive ones do not start last
+        const int64_t jq = n_mine - 1 - (int64_t)q;
+        const int64_t pi = P.rank + jq * P.world;
         const nrt_coarse_rec& c = P.in[pi];
-        // ---- set up the unknowns at the coarse seed
+        // ---- the path and its unknowns at the coarse seed (every thread holds D)
         Path D;
         D.n = c.n_int;
-        int m = 0;
+        int m = 0, nslot = 0;
         for (int a = 0; a < 3; ++a) D.rxp[a] = (double)P.rx[3 * (size_t)c.rx + a];
         for (int k = 0; k < D.n; ++k) {
             D.kind[k] = (c.kinds >> k) & 1u;
             D.label[k] = c.label[k];
             D.prim[k] = c.prim[k];
             D.col[k] = m;
+            D.slot[k] = -1;
             if (D.kind[k] == 0) {
                 const float4 nv = __ldg(&P.sn[c.prim[k]]);
                 D.nseed[k][0] = nv.x;
                 D.nseed[k][1] = nv.y;
                 D.nseed[k][2] = nv.z;
-                if (lane == 0)
-                    for (int a = 0; a < 3; ++a) S.z[m + a] = c.v[k][a];
+                D.slot[k] = nslot++;
                 m += 3;
             } else {
                 const DevEdge& E = P.edges[c.prim[k]];
-                for (int a = 0; a < 3; ++a) D.ea[k][a] = E.a[a];
+                const double ev[3] = {(double)E.b_[0] - E.a[0], (double)E.b_[1] - E.a[1], (double)E.b_[2] - E.a[2]};
+                const double l = sqrt(ddot(ev, ev));
+                for (int a = 0; a < 3; ++a) {
+                    D.ea[k][a] = E.a[a];
+                    D.ee[k][a] = ev[a] / l;
+                }
+                D.elen[k] = l;
                 m += 1;
             }
         }
         D.dim = m;
-        // diffraction: unit direction and length in FP64 from the f32 endpoints a, b
-        for (int k = 0; k < D.n; ++k) {
-            if (D.kind[k] == 0) continue;
-            const DevEdge& E = P.edges[c.prim[k]];
-            const double ev[3] = {(double)E.b_[0] - E.a[0], (double)E.b_[1] - E.a[1], (double)E.b_[2] - E.a[2]};
-            const double l = sqrt(ddot(ev, ev));
-            for (int a = 0; a < 3; ++a) D.ee[k][a] = ev[a] / l;
-            D.elen[k] = l;
-            const double w[3] = {c.v[k][0] - D.ea[k][0], c.v[k][1] - D.ea[k][1], c.v[k][2] - D.ea[k][2]};
-            if (lane == 0) S.z[D.col[k]] = ddot(w, D.ee[k]);
-        }
-        __syncwarp();
-        Vtx V[NRT_MAX_INT];
+        if (tid == 0)
+            for (int k = 0; k < D.n; ++k) {
+                if (D.kind[k] == 0) {
+                    for (int a = 0; a < 3; ++a) S.z[D.col[k] + a] = c.v[k][a];
+                } else {
+                    const double w[3] = {c.v[k][0] - D.ea[k][0], c.v[k][1] - D.ea[k][1], c.v[k][2] - D.ea[k][2]};
+                    S.z[D.col[k]] = ddot(w, D.ee[k]);
+                }
+            }
+        __syncthreads();
         for (int k = 0; k < D.n; ++k) {
             if (D.kind[k] != 0) continue;
             const double x[3] = {S.z[D.col[k]], S.z[D.col[k] + 1], S.z[D.col[k] + 2]};
-            gather(P, D.label[k], x, lists + (size_t)k * kCap, V[k], lane);
+            if (D.slot[k] < P.nv_max) {
+                gather(P, D.label[k], x, cand_ptr(cand, D.slot[k]), S.V[D.slot[k]], &counter, scan);
+            } else if (tid == 0) {
+                // no shared slot (more reflections than provisioned): direct scans
+                S.V[D.slot[k]].direct = 1;
+                S.V[D.slot[k]].n = 0;
+            }
         }
+        __syncthreads();
         int status = NRT_REF_NO_CONVERGE, it = 0;
-        double pbk[3], nbk[3];
-        if (m == 0) status = NRT_REF_OK;
-        else if (!residual_all(P, D, S.z, S.r, lists, V, S.pb, S.nb, lane)) status = NRT_REF_NO_SUPPORT;
-        else {
-            for (it = 1; it <= P.max_iter; ++it) {
-                // ---- Jacobian by central differences; only the perturbed vertex's MLS moves
-                bool ok = true;
-                for (int j = 0; j < m && ok; ++j) {
-                    int k = 0;
-                    while (k + 1 < D.n && D.col[k + 1] <= j) ++k;
-                    for (int sgn = 0; sgn < 2 && ok; ++sgn) {
-                        double* rr = sgn == 0 ? S.rp : S.rm;
-                        __syncwarp();
-                        const double zj = S.z[j];
-                        double zz[kMaxDim];
-                        for (int i = 0; i < m; ++i) zz[i] = S.z[i];
-                        zz[j] = sgn == 0 ? zj + kH : zj - kH;
-                        if (D.kind[k] == 0) {
-                            double x[3];
-                            vpoint(P, D, zz, k, x);
-                            ok = vertex_mls(P, D, k, x, lists + (size_t)k * kCap, V[k], pbk, nbk, lane);
+        if (m == 0) {
+            status = NRT_REF_OK;
+        } else {
+            if (wid == 0) residual_all(P, D, S.z, cand, S.V, S.tr[0], lane);
+            __syncthreads();
+            if (!S.tr[0].ok) status = NRT_REF_NO_SUPPORT;
+            else {
+                if (tid == 0) {
+                    for (int i = 0; i < m; ++i) S.r[i] = S.tr[0].r[i];
+                    for (int k = 0; k < D.n; ++k)
+                        for (int a = 0; a < 3; ++a) {
+                            S.pb[k][a] = S.tr[0].pb[k][a];
+                            S.nb[k][a] = S.tr[0].nb[k][a];
                         }
-                        for (int q2 = 0; q2 < D.n && ok; ++q2) {
-                            const bool mine = q2 == k && D.kind[k] == 0;
-                            ok = vertex_residual(P, D, zz, q2, mine ? pbk : S.pb[q2], mine ? nbk : S.nb[q2], rr);
+                }
+                __syncthreads();
+                for (it = 1; it <= P.max_iter; ++it) {
+                    // keep every vertex inside the safe ball of its candidate list: re-centre
+                    // the gather when the iterate drifted more than half the margin
+                    for (int k = 0; k < D.n; ++k) {
+                        if (D.kind[k] != 0 || D.slot[k] >= P.nv_max) continue;
+                        const Vtx& V = S.V[D.slot[k]];
+                        const double* x = S.z + D.col[k];
+                        const double dx = x[0] - V.c[0], dy = x[1] - V.c[1], dz = x[2] - V.c[2];
+                        if (V.direct || sqrt(dx * dx + dy * dy + dz * dz) > 0.5 * (P.rg - P.rq)) {
+                            const double xc[3] = {x[0], x[1], x[2]};
+                            __syncthreads();
+                            gather(P, D.label[k], xc, cand_ptr(cand, D.slot[k]), S.V[D.slot[k]], &counter, scan);
                         }
-                        (void)rr;
                     }
-                    if (ok && lane == 0)
-                        for (int i = 0; i < m; ++i) S.J[i * m + j] = (S.rp[i] - S.rm[i]) / (2.0 * kH);
-                    __syncwarp();
-                }
-                if (!ok) {
-                    status = NRT_REF_NO_SUPPORT;
-                    break;
-                }
-                // ---- normal equations + Cholesky (lane 0; m <= 24)
-                int solved = 1;
-                double dmax = 0;
-                if (lane == 0) {
-                    double tr = 0;
-                    for (int i = 0; i < m; ++i) {
-                        for (int j = 0; j < m; ++j) {
+                    // ---- Jacobian: column j on warp j mod NW (only vertex k's MLS moves)
+                    if (tid < NW) S.flag[tid] = 1;
+                    __syncthreads();
+                    for (int j = wid; j < m; j += NW) {
+                        int k = 0;
+                        while (k + 1 < D.n && D.col[k + 1] <= j) ++k;
+                        Trial& T = S.tr[wid];
+                        bool okj = true;
+                        for (int sgn = 0; sgn < 2 && okj; ++sgn) {
+                            double zz[kMaxDim];
+                            for (int i = 0; i < m; ++i) zz[i] = S.z[i];
+                            zz[j] = sgn == 0 ? S.z[j] + kH : S.z[j] - kH;
+                            double pbk[3] = {0, 0, 0}, nbk[3] = {0, 0, 0};
+                            if (D.kind[k] == 0) {
+                                double x[3];
+                                vpoint(P, D, zz, k, x);
+                                okj = mls(P, D, k, x, cand_ptr(cand, D.slot[k]), S.V[D.slot[k]], pbk, nbk, lane);
+                            }
+                            if (okj && lane == 0) {
+                                double* rr = sgn == 0 ? T.r : T.pb[0];  // T.pb as scratch (24 doubles)
+                                for (int q2 = 0; q2 < D.n && okj; ++q2) {
+                                    const bool mine = q2 == k && D.kind[k] == 0;
+                                    okj = vertex_residual(P, D, zz, q2, mine ? pbk : S.pb[q2], mine ? nbk : S.nb[q2], rr);
+                                }
+                            }
+                            okj = __shfl_sync(0xffffffffu, okj, 0);
+                        }
+                        if (lane == 0) {
+                            if (okj)
+                                for (int i = 0; i < m; ++i) S.J[i * m + j] = (T.r[i] - (&T.pb[0][0])[i]) / (2.0 * kH);
+                            else
+                                S.flag[wid] = 0;
+                        }
+                        __syncwarp();
+                    }
+                    __syncthreads();
+                    bool okJ = true;
+                    for (int w = 0; w < NW; ++w) okJ = okJ && S.flag[w];
+                    if (!okJ) {
+                        status = NRT_REF_NO_SUPPORT;
+                        break;
+                    }
+                    // ---- normal equations (whole block) + Cholesky solve (warp 0), m <= 24
+                    for (int e = tid; e < m * m + m; e += blockDim.x) {
+                        if (e < m * m) {
+                            const int i = e / m, j = e % m;
                             double s = 0;
                             for (int q2 = 0; q2 < m; ++q2) s += S.J[q2 * m + i] * S.J[q2 * m + j];
                             S.A[i * m + j] = s;
-                        }
-                        tr += S.A[i * m + i];
-                        double s = 0;
-                        for (int q2 = 0; q2 < m; ++q2) s += S.J[q2 * m + i] * S.r[q2];
-                        S.b[i] = -s;
-                    }
-                    const double lam = 1e-12 * tr / m;
-                    for (int i = 0; i < m; ++i) S.A[i * m + i] += lam;
-                    for (int j = 0; j < m && solved; ++j) {
-                        double d = S.A[j * m + j];
-                        for (int k = 0; k < j; ++k) d -= S.A[j * m + k] * S.A[j * m + k];
-                        if (!(d > 0.0)) {
-                            solved = 0;
-                            break;
-                        }
-                        d = sqrt(d);
-                        S.A[j * m + j] = d;
-                        for (int i = j + 1; i < m; ++i) {
-                            double s = S.A[i * m + j];
-                            for (int k = 0; k < j; ++k) s -= S.A[i * m + k] * S.A[j * m + k];
-                            S.A[i * m + j] = s / d;
+                        } else {
+                            const int i = e - m * m;
+                            double s = 0;
+                            for (int q2 = 0; q2 < m; ++q2) s += S.J[q2 * m + i] * S.r[q2];
+                            S.b[i] = -s;
                         }
                     }
-                    if (solved) {
-                        for (int i = 0; i < m; ++i) {
-                            double s = S.b[i];
-                            for (int k = 0; k < i; ++k) s -= S.A[i * m + k] * S.b[k];
-                            S.b[i] = s / S.A[i * m + i];
-                        }
-                        for (int i = m - 1; i >= 0; --i) {
-                            double s = S.b[i];
-                            for (int k = i + 1; k < m; ++k) s -= S.A[k * m + i] * S.b[k];
-                            S.b[i] = s / S.A[i * m + i];
-                        }
-                        for (int i = 0; i < m; ++i) dmax = fmax(dmax, fabs(S.b[i]));
-                    }
-                }
-                solved = __shfl_sync(0xffffffffu, solved, 0);
-                dmax = __shfl_sync(0xffffffffu, dmax, 0);
-                __syncwarp();
-                if (!solved) {
-                    status = NRT_REF_DEGENERATE;
-                    break;
-                }
-                if (dmax < P.tol) {  // converged: take the (tiny) full step
-                    if (lane == 0)
-                        for (int i = 0; i < m; ++i) S.zt[i] = S.z[i] + S.b[i];
-                    __syncwarp();
-                    double pbs[NRT_MAX_INT][3], nbs[NRT_MAX_INT][3];
-                    for (int k = 0; k < D.n; ++k)
-                        for (int a = 0; a < 3; ++a) {
-                            pbs[k][a] = S.pb[k][a];
-                            nbs[k][a] = S.nb[k][a];
-                        }
-                    __syncwarp();
-                    if (residual_all(P, D, S.zt, S.rp, lists, V, pbs, nbs, lane)) {
+                    __syncthreads();
+                    if (wid == 0) {
+                        double tr = 0;
+                        for (int i = 0; i < m; ++i) tr += S.A[i * m + i];
+                        const double lam = 1e-12 * tr / m;
+                        if (lane < m) S.A[lane * m + lane] += lam;
                         __syncwarp();
-                        if (lane == 0)
-                            for (int i = 0; i < m; ++i) {
-                                S.z[i] = S.zt[i];
-                                S.r[i] = S.rp[i];
+                        int solved = 1;
+                        for (int j = 0; j < m; ++j) {
+                            double d = S.A[j * m + j];
+                            for (int k = 0; k < j; ++k) d -= S.A[j * m + k] * S.A[j * m + k];
+                            if (!(d > 0.0)) {
+                                solved = 0;
+                                break;
                             }
+                            d = sqrt(d);
+                            // rows below the diagonal in parallel (each reads row j, written before)
+                            double s = 0;
+                            const int i = j + 1 + lane;
+                            if (i < m) {
+                                s = S.A[i * m + j];
+                                for (int k = 0; k < j; ++k) s -= S.A[i * m + k] * S.A[j * m + k];
+                            }
+                            __syncwarp();
+                            if (i < m) S.A[i * m + j] = s / d;
+                            if (lane == 0) S.A[j * m + j] = d;
+                            __syncwarp();
+                        }
+                        double dmax = 0;
+                        if (solved && lane == 0) {
+                            for (int i = 0; i < m; ++i) {
+                                double s = S.b[i];
+                                for (int k = 0; k < i; ++k) s -= S.A[i * m + k] * S.b[k];
+                                S.b[i] = s / S.A[i * m + i];
+                            }
+                            for (int i = m - 1; i >= 0; --i) {
+                                double s = S.b[i];
+                                for (int k = i + 1; k < m; ++k) s -= S.A[k * m + i] * S.b[k];
+                                S.b[i] = s / S.A[i * m + i];
+                            }
+                            for (int i = 0; i < m; ++i) dmax = fmax(dmax, fabs(S.b[i]));
+                        }
+                        if (lane == 0) S.dval = solved ? dmax : -1.0;
                     }
-                    status = NRT_REF_OK;
-                    __syncwarp();
-                    break;
-                }
-                const double f0 = sq(S.r, m);
-                double gam = 1.0;
-                bool acc = false;
-                while (gam > 1e-12) {
-                    if (lane == 0)
-                        for (int i = 0; i < m; ++i) S.zt[i] = S.z[i] + gam * S.b[i];
-                    __syncwarp();
-                    double pbs[NRT_MAX_INT][3], nbs[NRT_MAX_INT][3];
-                    const bool okr = residual_all(P, D, S.zt, S.rp, lists, V, pbs, nbs, lane);
-                    __syncwarp();
-                    if (okr && sq(S.rp, m) <= (1.0 - 2.0 * P.alpha * gam) * f0) {
-                        if (lane == 0)
-                            for (int i = 0; i < m; ++i) {
-                                S.z[i] = S.zt[i];
-                                S.r[i] = S.rp[i];
-                            }
-                        for (int k = 0; k < D.n; ++k)
-                            for (int a = 0; a < 3; ++a) {
-                                S.pb[k][a] = pbs[k][a];
-                                S.nb[k][a] = nbs[k][a];
-                            }
-                        acc = true;
-                        __syncwarp();
+                    __syncthreads();
+                    const double dmax = S.dval;
+                    if (dmax < 0.0) {
+                        status = NRT_REF_DEGENERATE;
                         break;
                     }
-                    gam *= P.beta;
+                    if (dmax < P.tol) {  // converged: take the (tiny) full step
+                        if (wid == 0) {
+                            double zt[kMaxDim];
+                            for (int i = 0; i < m; ++i) zt[i] = S.z[i] + S.b[i];
+                            residual_all(P, D, zt, cand, S.V, S.tr[0], lane);
+                            if (S.tr[0].ok && lane == 0)
+                                for (int i = 0; i < m; ++i) S.z[i] = zt[i];
+                        }
+                        status = NRT_REF_OK;
+                        __syncthreads();
+                        break;
+                    }
+                    // ---- backtracking: NW trials per round, first accepted in sequence order
+                    const double f0 = [&] {
+                        double s = 0;
+                        for (int i = 0; i < m; ++i) s += S.r[i] * S.r[i];
+                        return s;
+                    }();
+                    int accepted = -1;
+                    for (int round = 0; accepted < 0; ++round) {
+                        if (P.cycles && tid == 0) atomicAdd(&g_dbg[2], 1ull);
+                        double gam = 1.0;
+                        for (int e = 0; e < round * NW + wid; ++e) gam *= P.beta;
+                        const bool live = gam > 1e-12;
+                        if (live) {
+                            double zt[kMaxDim];
+                            for (int i = 0; i < m; ++i) zt[i] = S.z[i] + gam * S.b[i];
+                            residual_all(P, D, zt, cand, S.V, S.tr[wid], lane);
+                            if (lane == 0)
+                                S.flag[wid] = S.tr[wid].ok && S.tr[wid].f <= (1.0 - 2.0 * P.alpha * gam) * f0;
+                        } else if (lane == 0) {
+                            S.flag[wid] = 2;  // exhausted
+                        }
+                        __syncthreads();
+                        int first = -1;
+                        bool exhausted = false;
+                        for (int w = 0; w < NW; ++w) {
+                            if (S.flag[w] == 2) {
+                                exhausted = true;
+                                break;
+                            }
+                            if (S.flag[w] == 1) {
+                                first = w;
+                                break;
+                            }
+                        }
+                        if (first >= 0) {
+                            if (tid == 0) {
+                                double gm = 1.0;
+                                for (int e = 0; e < round * NW + first; ++e) gm *= P.beta;
+                                for (int i = 0; i < m; ++i) {
+                                    S.z[i] = S.z[i] + gm * S.b[i];
+                                    S.r[i] = S.tr[first].r[i];
+                                }
+                                for (int k = 0; k < D.n; ++k)
+                                    for (int a = 0; a < 3; ++a) {
+                                        S.pb[k][a] = S.tr[first].pb[k][a];
+                                        S.nb[k][a] = S.tr[first].nb[k][a];
+                                    }
+                            }
+                            accepted = first;
+                        } else if (exhausted) {
+                            accepted = NW;  // sentinel: failed
+                        }
+                        __syncthreads();
+                    }
+                    if (accepted == NW) {
+                        status = NRT_REF_NO_CONVERGE;
+                        break;
+                    }
                 }
-                if (!acc) {
-                    status = NRT_REF_NO_CONVERGE;
-                    break;
-                }
+                if (it > P.max_iter) it = P.max_iter;
             }
-            if (it > P.max_iter) it = P.max_iter;
         }
-        __syncwarp();
-        // ---- final residual, gradient norm, validity
-        double I[NRT_MAX_INT + 2][3];
-        for (int k = -1; k <= D.n; ++k) vpoint(P, D, S.z, k, I[k + 1]);
-        double gsq = 0, rmax = 0;
-        if (status == NRT_REF_OK && m > 0) {
-            double pbs[NRT_MAX_INT][3], nbs[NRT_MAX_INT][3];
-            __syncwarp();
-            if (!residual_all(P, D, S.z, S.rp, lists, V, pbs, nbs, lane)) status = NRT_REF_NO_SUPPORT;
-            else {
+        __syncthreads();
+        // ---- final residual, gradient norm, validity (warp 0)
+        if (wid == 0) {
+            double I[NRT_MAX_INT + 2][3];
+            for (int k = -1; k <= D.n; ++k) vpoint(P, D, S.z, k, I[k + 1]);
+            double gsq = 0, rmax = 0;
+            Trial& T = S.tr[0];
+            if (status == NRT_REF_OK && m > 0) {
+                residual_all(P, D, S.z, cand, S.V, T, lane);
+                if (!T.ok) status = NRT_REF_NO_SUPPORT;
+                else {
+                    for (int k = 0; k < D.n; ++k) {
+                        const double* rk = T.r + D.col[k];
+                        gsq += D.kind[k] == 0 ? rk[0] * rk[0] + rk[1] * rk[1] : rk[0] * rk[0];
+                    }
+                    for (int i = 0; i < m; ++i) rmax = fmax(rmax, fabs(T.r[i]));
+                }
+            } else {
+                for (int i = 0; i < m; ++i) rmax = fmax(rmax, fabs(S.r[i]));
+            }
+            const double (*nbf)[3] = (status == NRT_REF_OK && m > 0) ? T.nb : S.nb;
+            if (status == NRT_REF_OK)
                 for (int k = 0; k < D.n; ++k)
-                    for (int a = 0; a < 3; ++a) {
-                        S.nb[k][a] = nbs[k][a];
+                    if (D.kind[k] == 1) {
+                        const double t = S.z[D.col[k]];
+                        if (!(t >= 0.0 && t <= D.elen[k])) status = NRT_REF_OFF_EDGE;
                     }
+            if (status == NRT_REF_OK)
+                for (int k = 0; k < D.n; ++k)
+                    if (D.kind[k] == 0) {
+                        const double a[3] = {I[k][0] - I[k + 1][0], I[k][1] - I[k + 1][1], I[k][2] - I[k + 1][2]};
+                        const double b[3] = {I[k + 2][0] - I[k + 1][0], I[k + 2][1] - I[k + 1][1], I[k + 2][2] - I[k + 1][2]};
+                        const double sa = ddot(a, nbf[k]), sb = ddot(b, nbf[k]);
+                        if (!((sa > 0 && sb > 0) || (sa < 0 && sb < 0))) status = NRT_REF_WRONG_SIDE;
+                    }
+            if (status == NRT_REF_OK)
+                for (int k = 0; k < D.n && status == NRT_REF_OK; ++k)
+                    if (D.kind[k] == 0 && !supported(P, D.label[k], I[k + 1], lane)) status = NRT_REF_NO_SUPPORT;
+            if (status == NRT_REF_OK) {
+                for (int j = 0; j <= D.n && status == NRT_REF_OK; ++j) {
+                    double l0[6], l1[6];
+                    int n0 = 0, n1 = 0;
+                    if (j >= 1) {
+                        const int k = j - 1;
+                        if (D.kind[k] == 0) {
+                            for (int a = 0; a < 3; ++a) l0[a] = nbf[k][a];
+                            n0 = 1;
+                        } else {
+                            const DevEdge& E = P.edges[D.prim[k]];
+                            for (int a = 0; a < 3; ++a) {
+                                l0[a] = E.n0[a];
+                                l0[3 + a] = E.n1[a];
+                            }
+                            n0 = 2;
+                        }
+                    }
+                    if (j + 1 <= D.n) {
+                        const int k = j;
+                        if (D.kind[k] == 0) {
+                            for (int a = 0; a < 3; ++a) l1[a] = nbf[k][a];
+                            n1 = 1;
+                        } else {
+                            const DevEdge& E = P.edges[D.prim[k]];
+                            for (int a = 0; a < 3; ++a) {
+                                l1[a] = E.n0[a];
+                                l1[3 + a] = E.n1[a];
+                            }
+                            n1 = 2;
+                        }
+                    }
+                    if (occluded(P, I[j], I[j + 1], l0, n0, l1, n1, lane)) status = NRT_REF_OCCLUDED;
+                }
+            }
+            if (lane == 0 && (P.keep_invalid || status == NRT_REF_OK)) {
+                nrt_refined_rec o;
+                memset(&o, 0, sizeof(o));
+                o.rx = c.rx;
+                o.n_int = c.n_int;
+                o.n_diff = c.n_diff;
+                o.kinds = c.kinds;
+                for (int k = 0; k < NRT_MAX_INT; ++k) {
+                    o.label[k] = c.label[k];
+                    o.prim[k] = c.prim[k];
+                }
+                o.ray_id = c.ray_id;
+                double L = 0;
+                for (int j = 0; j <= D.n; ++j) {
+                    const double s3[3] = {I[j + 1][0] - I[j][0], I[j + 1][1] - I[j][1], I[j + 1][2] - I[j][2]};
+                    L += sqrt(ddot(s3, s3));
+                }
+                o.L = L;
+                o.delay = L / kC;
+                for (int k = 0; k < D.n; ++k)
+                    for (int a = 0; a < 3; ++a) o.v[k][a] = I[k + 1][a];
+                const double d0[3] = {I[1][0] - I[0][0], I[1][1] - I[0][1], I[1][2] - I[0][2]};
+                const double dl[3] = {I[D.n][0] - I[D.n + 1][0], I[D.n][1] - I[D.n + 1][1], I[D.n][2] - I[D.n + 1][2]};
+                const double l0 = sqrt(ddot(d0, d0)), ll = sqrt(ddot(dl, dl));
+                o.aod_az = (float)(atan2(d0[1], d0[0]) * 180.0 / kPi);
+                o.aod_el = (float)(asin(fmax(-1.0, fmin(1.0, d0[2] / l0))) * 180.0 / kPi);
+                o.aoa_az = (float)(atan2(dl[1], dl[0]) * 180.0 / kPi);
+                o.aoa_el = (float)(asin(fmax(-1.0, fmin(1.0, dl[2] / ll))) * 180.0 / kPi);
                 for (int k = 0; k < D.n; ++k) {
-                    const double* rk = S.rp + D.col[k];
-                    gsq += D.kind[k] == 0 ? rk[0] * rk[0] + rk[1] * rk[1] : rk[0] * rk[0];
+                    const double din[3] = {I[k + 1][0] - I[k][0], I[k + 1][1] - I[k][1], I[k + 1][2] - I[k][2]};
+                    const double l = sqrt(ddot(din, din));
+                    const double c2 = D.kind[k] == 0 ? fabs(ddot(din, nbf[k])) / l : ddot(din, D.ee[k]) / l;
+                    o.inc[k] = (float)(acos(fmax(-1.0, fmin(1.0, c2))) * 180.0 / kPi);
                 }
-                for (int i = 0; i < m; ++i) S.r[i] = S.rp[i];
+                o.status = status;
+                o.iters = it;
+                o.resid = m ? rmax : 0.0;
+                o.gradsq = gsq;
+                if (P.cycles) P.cycles[jq] = clock64() - t_start;
+                const unsigned long long at = P.keep_invalid ? (unsigned long long)jq : atomicAdd(P.n_out, 1ull);
+                P.out[at] = o;
             }
         }
-        for (int i = 0; i < m; ++i) rmax = fmax(rmax, fabs(S.r[i]));
-        if (status == NRT_REF_OK)
-            for (int k = 0; k < D.n; ++k)
-                if (D.kind[k] == 1) {
-                    const double t = S.z[D.col[k]];
-                    if (!(t >= 0.0 && t <= D.elen[k])) status = NRT_REF_OFF_EDGE;
-                }
-        if (status == NRT_REF_OK)
-            for (int k = 0; k < D.n; ++k)
-                if (D.kind[k] == 0) {
-                    const double a[3] = {I[k][0] - I[k + 1][0], I[k][1] - I[k + 1][1], I[k][2] - I[k + 1][2]};
-                    const double b[3] = {I[k + 2][0] - I[k + 1][0], I[k + 2][1] - I[k + 1][1], I[k + 2][2] - I[k + 1][2]};
-                    const double sa = ddot(a, S.nb[k]), sb = ddot(b, S.nb[k]);
-                    if (!((sa > 0 && sb > 0) || (sa < 0 && sb < 0))) status = NRT_REF_WRONG_SIDE;
-                }
-        if (status == NRT_REF_OK)
-            for (int k = 0; k < D.n; ++k)
-                if (D.kind[k] == 0 && status == NRT_REF_OK) {
-                    // the support query may need a wider list than the GN ball: re-gather here
-                    const double dx = I[k + 1][0] - V[k].c[0], dy = I[k + 1][1] - V[k].c[1], dz = I[k + 1][2] - V[k].c[2];
-                    if (sqrt(dx * dx + dy * dy + dz * dz) > P.rg - P.rq || V[k].over)
-                        gather(P, D.label[k], I[k + 1], lists + (size_t)k * kCap, V[k], lane);
-                    if (V[k].over || !supported(P, D.label[k], I[k + 1], lists + (size_t)k * kCap, V[k], lane))
-                        status = NRT_REF_NO_SUPPORT;
-                }
-        if (status == NRT_REF_OK) {
-            for (int j = 0; j <= D.n && status == NRT_REF_OK; ++j) {
-                double l0[6], l1[6];
-                int n0 = 0, n1 = 0;
-                if (j >= 1) {
-                    const int k = j - 1;
-                    if (D.kind[k] == 0) {
-                        for (int a = 0; a < 3; ++a) l0[a] = S.nb[k][a];
-                        n0 = 1;
-                    } else {
-                        const DevEdge& E = P.edges[D.prim[k]];
-                        for (int a = 0; a < 3; ++a) {
-                            l0[a] = E.n0[a];
-                            l0[3 + a] = E.n1[a];
-                        }
-                        n0 = 2;
-                    }
-                }
-                if (j + 1 <= D.n) {
-                    const int k = j;
-                    if (D.kind[k] == 0) {
-                        for (int a = 0; a < 3; ++a) l1[a] = S.nb[k][a];
-                        n1 = 1;
-                    } else {
-                        const DevEdge& E = P.edges[D.prim[k]];
-                        for (int a = 0; a < 3; ++a) {
-                            l1[a] = E.n0[a];
-                            l1[3 + a] = E.n1[a];
-                        }
-                        n1 = 2;
-                    }
-                }
-                if (occluded(P, I[j], I[j + 1], l0, n0, l1, n1, lane)) status = NRT_REF_OCCLUDED;
-            }
-        }
-        // ---- output
-        if (lane == 0 && (P.keep_invalid || status == NRT_REF_OK)) {
-            nrt_refined_rec o;
-            memset(&o, 0, sizeof(o));
-            o.rx = c.rx;
-            o.n_int = c.n_int;
-            o.n_diff = c.n_diff;
-            o.kinds = c.kinds;
-            for (int k = 0; k < NRT_MAX_INT; ++k) {
-                o.label[k] = c.label[k];
-                o.prim[k] = c.prim[k];
-            }
-            o.ray_id = c.ray_id;
-            double L = 0;
-            for (int j = 0; j <= D.n; ++j) {
-                const double s3[3] = {I[j + 1][0] - I[j][0], I[j + 1][1] - I[j][1], I[j + 1][2] - I[j][2]};
-                L += sqrt(ddot(s3, s3));
-            }
-            o.L = L;
-            o.delay = L / kC;
-            for (int k = 0; k < D.n; ++k)
-                for (int a = 0; a < 3; ++a) o.v[k][a] = I[k + 1][a];
-            const double d0[3] = {I[1][0] - I[0][0], I[1][1] - I[0][1], I[1][2] - I[0][2]};
-            const double dl[3] = {I[D.n][0] - I[D.n + 1][0], I[D.n][1] - I[D.n + 1][1], I[D.n][2] - I[D.n + 1][2]};
-            const double l0 = sqrt(ddot(d0, d0)), ll = sqrt(ddot(dl, dl));
-            o.aod_az = (float)(atan2(d0[1], d0[0]) * 180.0 / kPi);
-            o.aod_el = (float)(asin(fmax(-1.0, fmin(1.0, d0[2] / l0))) * 180.0 / kPi);
-            o.aoa_az = (float)(atan2(dl[1], dl[0]) * 180.0 / kPi);
-            o.aoa_el = (float)(asin(fmax(-1.0, fmin(1.0, dl[2] / ll))) * 180.0 / kPi);
-            for (int k = 0; k < D.n; ++k) {
-                const double din[3] = {I[k + 1][0] - I[k][0], I[k + 1][1] - I[k][1], I[k + 1][2] - I[k][2]};
-                const double l = sqrt(ddot(din, din));
-                const double c2 = D.kind[k] == 0 ? fabs(ddot(din, S.nb[k])) / l : ddot(din, D.ee[k]) / l;
-                o.inc[k] = (float)(acos(fmax(-1.0, fmin(1.0, c2))) * 180.0 / kPi);
-            }
-            o.status = status;
-            o.iters = it;
-            o.resid = m ? rmax : 0.0;
-            o.gradsq = gsq;
-            const unsigned long long at = P.keep_invalid ? (unsigned long long)q : atomicAdd(P.n_out, 1ull);
-            P.out[at] = o;
-        }
-        __syncwarp();
+        __syncthreads();
     }
 }
 
@@ -737,12 +916,22 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
         P.cos_ex = cs;
     }
     P.rq = fmax(4.0 * P.sigma, (double)s->r_max + d->tau);
-    P.rg = P.rq + fmax(0.05, 2.0 * P.sigma);
+    P.rg = P.rq + (getenv("NRT_REFINE_MARGIN") ? atof(getenv("NRT_REFINE_MARGIN")) : fmax(0.05, 2.0 * P.sigma));
     P.tol = d->tol_m;
     P.alpha = d->alpha;
     P.beta = d->beta;
     P.max_iter = d->max_iter;
     P.keep_invalid = d->keep_invalid;
+    // shared candidate slots: one per reflection vertex of the longest path (<= max_refl)
+    int nv = 0;
+    {
+        // the coarse set's max reflections = its launch max_refl (imports: assume NRT_MAX_INT)
+        nv = coarse->max_refl > 0 ? coarse->max_refl : NRT_MAX_INT;
+        if (nv > NRT_MAX_INT) nv = NRT_MAX_INT;
+    }
+    P.nv_max = nv;
+    const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) + (size_t)nv * kCapS * 6 * sizeof(float);
+    NRT_CUDA(cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t n_mine = n > d->rank ? (n - d->rank + d->world - 1) / d->world : 0;
     float* d_rx = nullptr;
     const size_t nrx = coarse->rx.size();
@@ -757,23 +946,25 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     P.out = o;
     P.n_out = ctr;
     P.work = ctr + 1;
+    const bool timing = getenv("NRT_REFINE_TIMING") != nullptr && d->keep_invalid;
+    if (timing) {
+        NRT_CUDA(cudaMallocAsync(&P.cycles, (size_t)(n_mine > 0 ? n_mine : 1) * 8, st));
+        NRT_CUDA(cudaMemsetAsync(P.cycles, 0, (size_t)(n_mine > 0 ? n_mine : 1) * 8, st));
+    }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine, 32 * kWarps, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine, 32 * NW, smem);
     if (per_sm < 1) per_sm = 1;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
     int64_t blocks = (int64_t)sms * per_sm;
-    const int64_t need = (n_mine + kWarps - 1) / kWarps;
-    if (blocks > need) blocks = need;
+    if (blocks > n_mine) blocks = n_mine;
     if (blocks < 1) blocks = 1;
-    P.slots = (int)blocks * kWarps;
-    NRT_CUDA(cudaMallocAsync(&P.cand, (size_t)P.slots * NRT_MAX_INT * kCap * sizeof(unsigned), st));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
     if (n_mine > 0) {
-        k_refine<<<(unsigned)blocks, 32 * kWarps, 0, st>>>(P);
+        k_refine<<<(unsigned)blocks, 32 * NW, smem, st>>>(P);
         ::nrt::count_launch();
     }
     cudaEventRecord(e1, st);
@@ -786,9 +977,30 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     out->info.ms_refine = ms;
-    cudaFreeAsync(P.cand, st);
     cudaFreeAsync(d_rx, st);
     cudaFreeAsync(ctr, st);
+    if (timing) {
+        std::vector<long long> cyc(n_mine > 0 ? n_mine : 1);
+        std::vector<nrt_refined_rec> rr(n_mine > 0 ? n_mine : 1);
+        cudaMemcpy(cyc.data(), P.cycles, n_mine * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(rr.data(), o, n_mine * sizeof(nrt_refined_rec), cudaMemcpyDeviceToHost);
+        std::vector<int64_t> ix(n_mine);
+        for (int64_t i = 0; i < n_mine; ++i) ix[i] = i;
+        std::sort(ix.begin(), ix.end(), [&](int64_t a, int64_t b) { return cyc[a] > cyc[b]; });
+        long long tot = 0;
+        for (int64_t i = 0; i < n_mine; ++i) tot += cyc[i];
+        fprintf(stderr, "[nrt] refine: %lld paths, sum %.3g cycles, blocks %lld\n", (long long)n_mine,
+                (double)tot, (long long)blocks);
+        unsigned long long dbg[8];
+        cudaMemcpyFromSymbol(dbg, g_dbg, sizeof(dbg));
+        fprintf(stderr, "[nrt]   mls list %llu direct %llu, ls rounds %llu, gathers %llu\n", dbg[0], dbg[1],
+                dbg[2], dbg[3]);
+        for (int64_t i = 0; i < n_mine && i < 12; ++i)
+            fprintf(stderr, "[nrt]   path %lld: %.3g cycles, n_int %d, iters %d, status %d\n",
+                    (long long)ix[i], (double)cyc[ix[i]], rr[ix[i]].n_int, rr[ix[i]].iters,
+                    rr[ix[i]].status);
+        cudaFree(P.cycles);
+    }
     if (d->keep_invalid) {
         out->d_rec = o;
         out->n = n_mine;

@@ -39,6 +39,17 @@ def main():
         torch.cuda.synchronize()
         t2 = time.perf_counter()
         info = p.info()
+        rf = N.nrt_refine_ex(sc, p, xi=case.xi, r_s=case.r_s, tau=case.tau, keep_invalid=1,
+                             stream=st)
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        rr = rf.export()
+        rinfo = rf.info()
+        import collections
+        out.append({"refine_ms": 1e3 * (t3 - t2), "ms_refine_kernel": rinfo["ms_refine"],
+                    "status": dict(collections.Counter(int(x) for x in rr["status"])),
+                    "iters_hist": np.histogram(rr["iters"], bins=[0, 2, 4, 8, 16, 32, 64, 101])[0].tolist(),
+                    "iters_max": int(rr["iters"].max()) if len(rr) else 0})
         out.append({"build_ms": 1e3 * (t1 - t0), "launch_ms": 1e3 * (t2 - t1),
                     **{k: info[k] for k in ("ms_trace", "ms_fans", "ms_dedupe", "ms_total",
                                             "bounces", "n_raw", "n", "n_events", "n_fan_rays",
