@@ -48,6 +48,8 @@ class Clocks:
         self.path = os.path.join("/tmp", f"nrt_clocks_{os.getpid()}.csv")
 
     def __enter__(self):
+        if os.environ.get("NRT_BENCH_NO_CLOCKS"):
+            return self
         try:
             self.f = open(self.path, "w")
             self.p = subprocess.Popen(
@@ -102,86 +104,69 @@ def dist_env():
     return world, rank, local
 
 
-def allgather_bytes(t, world):
-    """All-gather variable-length uint8 cuda tensors (count exchange, then padded gather)."""
-    import torch
-    import torch.distributed as dist
-    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
-    ns = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(ns, n)
-    ns = [int(x.item()) for x in ns]
-    m = max(ns) if ns else 0
-    if m == 0:
-        return torch.zeros(0, dtype=torch.uint8, device=t.device)
-    pad = torch.zeros(m, dtype=torch.uint8, device=t.device)
-    pad[: t.numel()] = t
-    out = torch.zeros(world * m, dtype=torch.uint8, device=t.device)
-    dist.all_gather_into_tensor(out, pad)
-    return torch.cat([out[r * m: r * m + ns[r]] for r in range(world)])
-
-
 class Runner:
-    """One hot-path step on this rank, device-resident inputs."""
+    """One hot-path step on this rank, device-resident inputs.  Weak scaling: the Fibonacci
+    lattice has n_rays x world directions, rank r traces i == r (mod world)."""
 
     def __init__(self, N, case, world, rank, stream, refine_on):
         import torch
         self.N, self.case, self.world, self.rank, self.stream = N, case, world, rank, stream
         s = case.scene
         dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
         self.pts, self.nrm, self.rad, self.lab = t(s.points), t(s.normals), t(s.radii), t(s.labels)
         self.tx = t(case.tx)
         self.rx = t(case.rx.reshape(-1, 3))
+        self.n_rays = case.n_rays * world
         self.refine_on = refine_on
         self.desc = dict(kappa=case.kappa, tau=case.tau, c_R=case.c_R, dphi_deg=case.dphi_deg,
                          theta_ex_deg=case.theta_ex_deg, edge_bin=case.edge_bin)
+        self.rdesc = dict(xi=case.xi, r_s=case.r_s, tau=case.tau, theta_ex_deg=case.theta_ex_deg)
 
     def step(self, counters=0):
+        import torch
+        from paper_2403_06648_b200 import dist as D
         N, c = self.N, self.case
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(self.stream)
         sc = N.nrt_scene_build_ex(self.pts, self.nrm, c.voxel, radii=self.rad, labels=self.lab,
                                   edges=c.scene.edges, stream=self.stream)
+        ev[1].record(self.stream)
         if self.world == 1:
-            coarse = N.nrt_launch_ex(sc, self.tx, self.rx, c.n_rays, c.max_refl, c.max_diff,
+            coarse = N.nrt_launch_ex(sc, self.tx, self.rx, self.n_rays, c.max_refl, c.max_diff,
                                      counters=counters, stream=self.stream, **self.desc)
-            merged = coarse
-            parts = [coarse]
+            info = coarse.info()
         else:
-            import torch
-            has_diff = c.max_diff > 0 and len(c.scene.edges) > 0
-            coarse = N.nrt_launch_ex(sc, self.tx, self.rx, c.n_rays, c.max_refl, c.max_diff,
-                                     rank=self.rank, world=self.world, stage=1 if has_diff else 0,
-                                     counters=counters, stream=self.stream, **self.desc)
-            if has_diff:
-                ev = torch.from_numpy(coarse.export_events().view(np.uint8)).cuda()
-                evall = allgather_bytes(ev, self.world)
-                N.nrt_launch_fans(sc, coarse, evall, rank=self.rank, world=self.world,
-                                  stream=self.stream, **self.desc)
-            rs = coarse.record_size()
-            buf = torch.zeros(coarse.count() * rs, dtype=torch.uint8, device="cuda")
-            coarse.export(buf)
-            allr = allgather_bytes(buf, self.world)
-            merged = N.nrt_paths_import(allr, N.PATHS_COARSE, c.tx, c.rx)
-            merged = N.nrt_paths_merge([merged], c.kappa)
-            parts = [coarse]
-        refined = None
+            coarse, info = D.launch_distributed(
+                N, sc, c.tx, c.rx, self.n_rays, c.max_refl, c.max_diff, self.rank, self.world,
+                has_edges=len(c.scene.edges) > 0, device=self.dev, stream=self.stream,
+                counters=counters, **self.desc)
+        ev[2].record(self.stream)
+        refined, rinfo = None, None
         if self.refine_on:
-            refined = N.nrt_refine_ex(sc, merged, xi=c.xi, r_s=c.r_s, tau=c.tau + 0.0,
-                                      rank=self.rank, world=self.world, stream=self.stream)
-        infos = [p.info() for p in parts]
+            refined, rinfo = D.refine_distributed(N, sc, coarse, c.tx, c.rx, self.rank, self.world,
+                                                  device=self.dev, stream=self.stream, **self.rdesc)
+        ev[3].record(self.stream)
+        ev[3].synchronize()
         out = {
-            "bounces": sum(i["bounces"] for i in infos),
-            "coarse": merged.count(),
+            "phase_ms": [round(ev[i].elapsed_time(ev[i + 1]), 3) for i in range(3)],
+            "bounces": info["bounces"],
+            "coarse": coarse.count(),
             "refined": refined.count() if refined is not None else 0,
-            "ms_trace": sum(i["ms_trace"] for i in infos),
-            "ms_fans": sum(i["ms_fans"] for i in infos),
-            "tests": sum(i["surfel_tests"] for i in infos),
-            "cells": sum(i["cells_visited"] for i in infos),
-            "nonempty": sum(i["cells_nonempty"] for i in infos),
-            "n_events": infos[0]["n_events"],
-            "n_fan_rays": infos[0]["n_fan_rays"],
+            "ms_trace": info["ms_trace"],
+            "ms_fans": info["ms_fans"],
+            "tests": info["surfel_tests"],
+            "cells": info["cells_visited"],
+            "nonempty": info["cells_nonempty"],
+            "n_events": info["n_events"],
+            "n_fan_rays": info["n_fan_rays"],
             "scene": sc.info(),
-            "refined_info": refined.info() if refined is not None else None,
+            "refined_info": rinfo,
         }
+        for h in (refined, coarse, sc):
+            if h is not None:
+                h.free()
         return out
 
 
@@ -346,7 +331,7 @@ def main():
     pb = 32 * prim_only["tests"] + 8 * prim_only["cells"]
     achieved = pb / (ms_trace / 1000.0) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "kernel": "k_primary",
+            "frac": achieved / hbm, "traffic": None, "kernel": "k_trace (primary bounces)",
             "peak_source": src,
             "bytes_per_launch": pb, "bytes_per_bounce": pb / max(1, prim_only["bounces"]),
             "ms_per_launch": ms_trace}
@@ -375,11 +360,13 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{case.name}: SR room {case.scene.n} surfels sigma={args.sigma} m, "
-                               f"1 TX/{len(case.rx)} RX, {case.n_rays} rays/GPU-shard-set, "
-                               f"max_refl {case.max_refl}, max_diff {case.max_diff}",
-                   "voxel_m": case.voxel, "n_rays": case.n_rays, "l2": "512 MiB write between steps",
-                   "parallelism": f"dp{world} (rays i == rank mod {world})"},
+        "config": {"workload": f"{case.name}: {case.scene.name}, 1 TX/{len(case.rx)} RX, "
+                               f"{case.n_rays} rays per GPU, max_refl {case.max_refl}, "
+                               f"max_diff {case.max_diff}; step = scene build + launch + refine",
+                   "voxel_m": case.voxel, "n_rays_total": case.n_rays * world,
+                   "l2": "512 MiB write between steps (outside the timed events)",
+                   "parallelism": f"dp{world}: rays i == rank mod {world}, paths j == rank mod "
+                                  f"{world}, NCCL all-gather of events/coarse/refined records"},
         # refined paths/s: coarse paths refined (the refinement's input rate, as the paper's
         # Table IV refine times count) per second of the whole step, and of the refine kernel
         "refined_paths_per_s": (outs[-1]["coarse"] * args.steps / (total_ms / 1000.0))
@@ -391,6 +378,8 @@ def main():
                          "step": total_ms / args.steps},
         "n_events": outs[-1]["n_events"], "n_fan_rays": outs[-1]["n_fan_rays"],
         "bounces_per_step": bounces,
+        "step_ms": [round(x, 3) for x in step_ms],
+        "phase_ms_build_launch_refine": [o["phase_ms"] for o in outs],
         "roofline": roof,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -408,7 +397,7 @@ def prim_counts(N, R, case):
     """Instrumented primary-only launch (stage 1: no fans) for the k_primary byte count."""
     sc = N.nrt_scene_build_ex(R.pts, R.nrm, case.voxel, radii=R.rad, labels=R.lab,
                               edges=case.scene.edges, stream=R.stream)
-    p = N.nrt_launch_ex(sc, R.tx, R.rx, case.n_rays, case.max_refl, case.max_diff, counters=1,
+    p = N.nrt_launch_ex(sc, R.tx, R.rx, R.n_rays, case.max_refl, case.max_diff, counters=1,
                         stage=1, rank=R.rank, world=R.world, stream=R.stream, **R.desc)
     i = p.info()
     return {"tests": i["surfel_tests"], "cells": i["cells_visited"], "bounces": i["bounces"]}

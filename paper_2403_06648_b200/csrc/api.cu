@@ -39,6 +39,19 @@ void ensure_pool(int dev) {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        // pre-reserve: one large allocation returned to the pool keeps its physical backing
+        // mapped, so later launches sub-allocate without growing the pool (NRT_POOL_GB, def. 4)
+        const char* e = getenv("NRT_POOL_GB");
+        const double gb = e ? atof(e) : 4.0;
+        if (gb > 0) {
+            void* p = nullptr;
+            if (cudaMallocAsync(&p, (size_t)(gb * (1ull << 30)), nullptr) == cudaSuccess) {
+                cudaFreeAsync(p, nullptr);
+                cudaStreamSynchronize(nullptr);
+            } else {
+                cudaGetLastError();
+            }
+        }
     }
     done.fetch_or(bit);
 }
@@ -153,16 +166,17 @@ nrt_status nrt_scene_build_ex(const nrt_scene_desc* desc, nrt_scene* out) {
     return scene_build(desc, out);
 }
 
+// Every entry point synchronises its stream before returning and handle memory is private,
+// so no device work can still reference it: free into the stream-ordered pool directly.
 void nrt_scene_free(nrt_scene s) {
     if (!s) return;
     cudaSetDevice(s->device);
-    cudaDeviceSynchronize();
-    cudaFree(s->cell);
-    cudaFree(s->rec);
-    cudaFree(s->sp);
-    cudaFree(s->sn);
-    cudaFree(s->label);
-    cudaFree(s->edges);
+    cudaFreeAsync(s->cell, nullptr);
+    cudaFreeAsync(s->rec, nullptr);
+    cudaFreeAsync(s->sp, nullptr);
+    cudaFreeAsync(s->sn, nullptr);
+    cudaFreeAsync(s->label, nullptr);
+    cudaFreeAsync(s->edges, nullptr);
     delete s;
 }
 
@@ -544,7 +558,8 @@ nrt_status nrt_paths_import(const void* src, int64_t n, int32_t kind, nrt_mem me
     P->info.kind = kind;
     P->info.n = n;
     const size_t b = (size_t)n * rec_size(kind);
-    if (cudaMalloc(&P->d_rec, b > 0 ? b : 1) != cudaSuccess) {
+    ensure_pool(dev);
+    if (cudaMallocAsync(&P->d_rec, b > 0 ? b : 1, nullptr) != cudaSuccess) {
         delete P;
         return set_error(NRT_E_NOMEM, "import buffer");
     }
@@ -571,7 +586,8 @@ nrt_status nrt_paths_merge(const nrt_paths* parts, int32_t n_parts, int32_t kapp
     cudaStream_t st = nullptr;
     const size_t rs = rec_size(kind);
     char* all = nullptr;
-    NRT_CUDA(cudaMalloc(&all, (total > 0 ? total : 1) * rs));
+    ensure_pool(parts[0]->device);
+    NRT_CUDA(cudaMallocAsync(&all, (total > 0 ? total : 1) * rs, st));
     int64_t off = 0;
     for (int i = 0; i < n_parts; ++i) {
         if (parts[i]->n)
@@ -593,7 +609,7 @@ nrt_status nrt_paths_merge(const nrt_paths* parts, int32_t n_parts, int32_t kapp
     }
     nrt_status rc;
     void* o = nullptr;
-    if (cudaMalloc(&o, (total > 0 ? total : 1) * rs) != cudaSuccess) {
+    if (cudaMallocAsync(&o, (total > 0 ? total : 1) * rs, st) != cudaSuccess) {
         rc = set_error(NRT_E_NOMEM, "merge buffer");
     } else {
         int64_t m = 0;
@@ -605,12 +621,12 @@ nrt_status nrt_paths_merge(const nrt_paths* parts, int32_t n_parts, int32_t kapp
         P->n = m;
         P->info.n = m;
     }
-    cudaFree(all);
+    cudaFreeAsync(all, st);
     if (rc != NRT_OK) {
         nrt_paths_free(P);
         return rc;
     }
-    cudaDeviceSynchronize();
+    NRT_CUDA(cudaStreamSynchronize(st));
     *out = P;
     return NRT_OK;
 }
@@ -618,9 +634,13 @@ nrt_status nrt_paths_merge(const nrt_paths* parts, int32_t n_parts, int32_t kapp
 void nrt_paths_free(nrt_paths p) {
     if (!p) return;
     cudaSetDevice(p->device);
-    cudaDeviceSynchronize();
-    cudaFree(p->d_rec);
-    cudaFree(p->d_ev);
+    if (p->pool_owned) {
+        cudaFreeAsync(p->d_rec, nullptr);
+        cudaFreeAsync(p->d_ev, nullptr);
+    } else {
+        cudaFree(p->d_rec);
+        cudaFree(p->d_ev);
+    }
     delete p;
 }
 

@@ -151,6 +151,7 @@ struct nrt_paths_s {
     // launch parameters (for stage-2 fans)
     int64_t n_rays = 0;
     int32_t max_refl = 0, max_diff = 0;
+    bool pool_owned = true;  // d_rec/d_ev from cudaMallocAsync (false: cudaMalloc)
 };
 
 namespace nrt {

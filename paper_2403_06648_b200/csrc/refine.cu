@@ -212,6 +212,7 @@ __device__ bool mls(const RP& P, const Path& D, int k, const double x[3], const 
     const double dxc = x[0] - V.c[0], dyc = x[1] - V.c[1], dzc = x[2] - V.c[2];
     const bool use_list = !V.direct && sqrt(dxc * dxc + dyc * dyc + dzc * dzc) <= P.rg - P.rq;
     if (P.cycles && lane == 0) atomicAdd(&g_dbg[use_list ? 0 : 1], 1ull);
+    const long long t_mls0 = P.cycles ? clock64() : 0;
     auto acc = [&](double p0, double p1, double p2, double n0, double n1, double n2) {
         const double d0 = p0 - x[0], d1 = p1 - x[1], d2 = p2 - x[2];
         const double dd = (d0 * d0 + d1 * d1) + d2 * d2;
@@ -276,6 +277,7 @@ __device__ bool mls(const RP& P, const Path& D, int k, const double x[3], const 
         }
     }
     W = wsum(W);
+    if (P.cycles && lane == 0) atomicAdd(&g_dbg[use_list ? 4 : 5], (unsigned long long)(clock64() - t_mls0));
     Px = wsum(Px);
     Py = wsum(Py);
     Pz = wsum(Pz);
@@ -995,6 +997,8 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
         cudaMemcpyFromSymbol(dbg, g_dbg, sizeof(dbg));
         fprintf(stderr, "[nrt]   mls list %llu direct %llu, ls rounds %llu, gathers %llu\n", dbg[0], dbg[1],
                 dbg[2], dbg[3]);
+        fprintf(stderr, "[nrt]   avg cycles: mls list %.0f direct %.0f\n", (double)dbg[4] / (dbg[0] + 1),
+                (double)dbg[5] / (dbg[1] + 1));
         for (int64_t i = 0; i < n_mine && i < 12; ++i)
             fprintf(stderr, "[nrt]   path %lld: %.3g cycles, n_int %d, iters %d, status %d\n",
                     (long long)ix[i], (double)cyc[ix[i]], rr[ix[i]].n_int, rr[ix[i]].iters,

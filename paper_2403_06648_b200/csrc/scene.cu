@@ -480,10 +480,11 @@ nrt_status scene_build(const nrt_scene_desc* D, nrt_scene* out) {
     S->n_edges = D->n_edges;
     nrt_status rc = build_impl(D, S, st);
     if (rc == NRT_OK && S->n_edges > 0) {
-        cudaError_t e = cudaMalloc(&S->edges, sizeof(DevEdge) * S->n_edges);
+        cudaError_t e = cudaMallocAsync((void**)&S->edges, sizeof(DevEdge) * S->n_edges, st);
         if (e == cudaSuccess)
-            e = cudaMemcpy(S->edges, S->h_edges.data(), sizeof(DevEdge) * S->n_edges,
-                           cudaMemcpyHostToDevice);
+            e = cudaMemcpyAsync(S->edges, S->h_edges.data(), sizeof(DevEdge) * S->n_edges,
+                                cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) rc = set_error(NRT_E_CUDA, "edge upload: %s", cudaGetErrorString(e));
     }
     if (rc != NRT_OK) {
