@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnrt.so")
+LIB_PATH = os.environ.get("NRT_LIB") or os.path.join(_HERE, "libnrt.so")  # NRT_LIB: tuning variants
 
 NRT_MAX_INT = 8
 STATUS = {0: "NRT_OK", 1: "NRT_E_INVALID", 2: "NRT_E_NOMEM", 3: "NRT_E_CUDA", 4: "NRT_E_OVERFLOW",

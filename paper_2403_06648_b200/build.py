@@ -21,17 +21,21 @@ NVCC_FLAGS = [
 ]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile every .cu of csrc/ into one shared library (out, default libnrt.so).
+    `defines` (e.g. ["NRT_TRACE_MINB=8"]) are tuning variants for experiments."""
+    lib = out or LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, "internal.cuh"), os.path.join(ROOT, "include", "nrt.h")]
-    if not force and os.path.exists(LIB):
-        mt = os.path.getmtime(LIB)
+    if not force and os.path.exists(lib):
+        mt = os.path.getmtime(lib)
         if all(os.path.getmtime(s) <= mt for s in deps):
-            return LIB
+            return lib
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *srcs]
+    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+           "-o", lib + ".tmp", *srcs]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(HERE, "build.log")
+    log = os.path.join(HERE, "build.log" if out is None else os.path.basename(lib) + ".log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:
@@ -39,10 +43,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    outs = [a for a in args if a.endswith(".so")]
+    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, defines=defs,
+          out=os.path.abspath(outs[0]) if outs else None)

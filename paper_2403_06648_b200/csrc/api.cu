@@ -176,6 +176,8 @@ void nrt_scene_free(nrt_scene s) {
     cudaFreeAsync(s->sp, nullptr);
     cudaFreeAsync(s->sn, nullptr);
     cudaFreeAsync(s->label, nullptr);
+    cudaFreeAsync(s->hcell, nullptr);
+    cudaFreeAsync(s->hrec, nullptr);
     cudaFreeAsync(s->edges, nullptr);
     delete s;
 }

@@ -130,6 +130,12 @@ struct nrt_scene_s {
     float4* rec = nullptr;     // [2*nref] AoS: (p, r^2), (n, id bits)
     float4* sp = nullptr;      // [n] (p, r)
     float4* sn = nullptr;      // [n] (n, label bits)
+    // home grid for neighbourhood queries (refinement): every surfel once, in the cell of
+    // size hv = 2 v that contains p; hrec = (p, r), (n, label bits) sorted by cell
+    float hv = 0, inv_hv = 0;
+    int hdims[3] = {0, 0, 0};
+    uint2* hcell = nullptr;
+    float4* hrec = nullptr;
     int32_t* label = nullptr;  // [n]
     nrt::DevEdge* edges = nullptr;
     int n_edges = 0;

@@ -107,6 +107,22 @@ struct Cnt {
     unsigned long long tests = 0, cells = 0, nonempty = 0;
 };
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ unsigned long long lane_inc(unsigned long long* ctr) {
+    return atomicAdd(ctr, 1ull);
+}
+#ifndef NRT_TRACE_MINB
+#define NRT_TRACE_MINB 8  // min resident blocks/SM for k_trace: 64 registers, 50% occupancy
+                          // (measured best of 4/6/8 on C2, scripts/variant_sweep.sh)
+#endif
+#ifndef NRT_TRACE_FETCH
+#define NRT_TRACE_FETCH lane_inc
+#endif
+
 // ---- A3 reference walk (debug path): nearest surfel along (o, d) by plain 3D-DDA --------
 __device__ int nearest(const TP& P, float3 o, float3 d, float3 l0, float3 l1, int prev,
                        float& t_out) {
@@ -374,7 +390,7 @@ __device__ __forceinline__ bool seg_begin(const TP& P, Seg& s, Cnt& cnt) {
     s.best = -1;
     s.k = s.kend = 0;
     const float3 o = s.o, d = s.d;
-    s.inv = make_float3(__frcp_rn(d.x), __frcp_rn(d.y), __frcp_rn(d.z));
+    s.inv = make_float3(rcp_approx(d.x), rcp_approx(d.y), rcp_approx(d.z));  // walk only: approximate is fine (§6.2)
     const float gx1 = P.ox + P.nx * P.v, gy1 = P.oy + P.ny * P.v, gz1 = P.oz + P.nz * P.v;
     float t0 = 0.0f, t1 = INFINITY;
     {
@@ -506,7 +522,7 @@ __device__ __forceinline__ void flush_counts(const TP& P, unsigned long long bou
 
 // TRACE: nearest hit of every live segment of bounce b (persistent, dynamic refill)
 template <bool CNT>
-__global__ void __launch_bounds__(128) k_trace(TP P, Wave W, int b) {
+__global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace(TP P, Wave W, int b) {
     const unsigned long long n = W.n_alive[b];
     const unsigned* alive = W.alive[b & 1];
     unsigned long long bounces = 0;
@@ -516,7 +532,7 @@ __global__ void __launch_bounds__(128) k_trace(TP P, Wave W, int b) {
     bool have = false;
     for (;;) {
         if (!have) {
-            const unsigned long long j = agg_inc(&W.ctr[b]);
+            const unsigned long long j = NRT_TRACE_FETCH(&W.ctr[b]);
             if (j >= n) break;
             ray = alive[j];
             const float4 o = W.o[ray], d = W.d[ray], a = W.l0[ray], c = W.l1[ray];
@@ -601,6 +617,20 @@ __global__ void __launch_bounds__(128) k_shade(TP P, Wave W, int b) {
             c.seg = c.seg + 1;
             next[agg_inc(&W.n_alive[b + 1])] = ray;
         }
+    }
+}
+
+// processing order for coherence: key = (latitude band of B lattice slots, azimuth).  Only the
+// order in which lanes pick up rays changes; ray ids and results do not.
+__global__ void k_order_keys(const float4* d, uint64_t n, uint64_t band, unsigned long long* keys,
+                             unsigned* vals) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const float4 v = d[j];
+        float a = atan2f(v.y, v.x);  // (-pi, pi]
+        const unsigned q = (unsigned)fminf(65535.0f, fmaxf(0.0f, (a + 3.14159265f) * (65536.0f / 6.2831853f)));
+        keys[j] = ((unsigned long long)(j / band) << 16) | q;
+        vals[j] = (unsigned)j;
     }
 }
 
@@ -864,6 +894,31 @@ nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw
             if (gb > (unsigned)sm_count(s->device) * 16) gb = (unsigned)sm_count(s->device) * 16;
             k_gen_primary<<<gb, 256, 0, st>>>(P, W, n_shard);
             ::nrt::count_launch();
+            const char* eb = getenv("NRT_SORT_BAND");
+            const uint64_t band = eb ? (uint64_t)atoll(eb) : 0;
+            if (band > 0 && n_shard > 1) {  // coherent processing order (alive list permutation)
+                unsigned long long *k0 = nullptr, *k1 = nullptr;
+                unsigned* v1 = nullptr;
+                NRT_CUDA(cudaMallocAsync(&k0, n_shard * 8, st));
+                NRT_CUDA(cudaMallocAsync(&k1, n_shard * 8, st));
+                NRT_CUDA(cudaMallocAsync(&v1, n_shard * 4, st));
+                k_order_keys<<<gb, 256, 0, st>>>(W.d, n_shard, band, k0, W.alive[1]);
+                ::nrt::count_launch();
+                int bits = 17;
+                while (bits < 64 && ((n_shard / band) >> (bits - 16)) > 0) ++bits;
+                cub::DoubleBuffer<unsigned long long> kb(k0, k1);
+                cub::DoubleBuffer<unsigned> vb(W.alive[1], v1);
+                size_t tbs = 0;
+                void* tmp = nullptr;
+                cub::DeviceRadixSort::SortPairs(nullptr, tbs, kb, vb, (int)n_shard, 0, bits, st);
+                NRT_CUDA(cudaMallocAsync(&tmp, tbs, st));
+                cub::DeviceRadixSort::SortPairs(tmp, tbs, kb, vb, (int)n_shard, 0, bits, st);
+                NRT_CUDA(cudaMemcpyAsync(W.alive[0], vb.Current(), n_shard * 4, cudaMemcpyDeviceToDevice, st));
+                cudaFreeAsync(tmp, st);
+                cudaFreeAsync(k0, st);
+                cudaFreeAsync(k1, st);
+                cudaFreeAsync(v1, st);
+            }
             NRT_TRY(run_bounces(P, W, a.max_refl + 1, s->device, a.desc.counters != 0,
                                 &stats->ms_kernel, st));
         }

@@ -50,6 +50,10 @@ struct RP {
     const float4* sn;  // (n, label bits)
     float ox, oy, oz, v, inv_v, pad;
     int nx, ny, nz;
+    const uint2* hcell;   // home grid (each surfel once)
+    const float4* hrec;
+    float inv_hv;
+    int hx, hy, hz;
     const DevEdge* edges;
     const nrt_coarse_rec* in;
     int64_t n_in;
@@ -116,26 +120,65 @@ __device__ __forceinline__ float* cand_ptr(float* cand, int s) { return cand + (
 
 typedef cub::BlockScan<int, 32 * NW> BlockScanT;
 
-__device__ unsigned long long g_dbg[8];  // diagnostics (NRT_REFINE_TIMING): MLS list/direct, LS rounds, gathers
+__device__ unsigned long long g_dbg[12];  // diagnostics (NRT_REFINE_TIMING): MLS list/direct, LS rounds, gathers
 
-// does record k of cell (ci,cj,ck) belong to the candidate set around c?  (home cell, label,
-// distance) -> surfel data
-__device__ __forceinline__ bool cand_match(const RP& P, unsigned k, int ci, int cj, int ck,
-                                           int32_t label, const double c[3], double rg2, float4& A,
-                                           float4& nv) {
-    A = __ldg(&P.rec[2 * k]);
-    const double dx = (double)A.x - c[0], dy = (double)A.y - c[1], dz = (double)A.z - c[2];
-    if (dx * dx + dy * dy + dz * dz > rg2) return false;
-    const int hx = (int)floorf((A.x - P.ox) * P.inv_v), hy = (int)floorf((A.y - P.oy) * P.inv_v),
-              hz = (int)floorf((A.z - P.oz) * P.inv_v);
-    if (hx != ci || hy != cj || hz != ck) return false;
-    const float4 B = __ldg(&P.rec[2 * k + 1]);
-    nv = __ldg(&P.sn[__float_as_uint(B.w)]);
-    return __float_as_int(nv.w) == label;
+// home-grid cell range of the axis-aligned box [c - R, c + R] (clamped)
+struct Box {
+    int i0, i1, j0, j1, k0, k1;
+};
+__device__ __forceinline__ Box home_box(const RP& P, const double c[3], double R) {
+    Box b;
+    b.i0 = max(0, (int)floorf(((float)(c[0] - R) - P.ox) * P.inv_hv));
+    b.i1 = min(P.hx - 1, (int)floorf(((float)(c[0] + R) - P.ox) * P.inv_hv));
+    b.j0 = max(0, (int)floorf(((float)(c[1] - R) - P.oy) * P.inv_hv));
+    b.j1 = min(P.hy - 1, (int)floorf(((float)(c[1] + R) - P.oy) * P.inv_hv));
+    b.k0 = max(0, (int)floorf(((float)(c[2] - R) - P.oz) * P.inv_hv));
+    b.k1 = min(P.hz - 1, (int)floorf(((float)(c[2] + R) - P.oz) * P.inv_hv));
+    return b;
 }
 
-// ---- block-cooperative gather of vertex k's candidates around c (home-cell dedupe).
-// Deterministic order: cells in linear order, each round of blockDim cells compacted by a
+// ---- one warp visits every surfel of the home cells of box B: f(home record index) is called
+// by the lane that owns the record (32 cell headers per round trip, warp prefix sum of the
+// counts, lanes stride over the flattened records).
+template <class F>
+__device__ __forceinline__ void scan_box(const RP& P, const Box& B, int lane, F&& f) {
+    const int nxr = B.i1 - B.i0 + 1, nyr = B.j1 - B.j0 + 1, nzr = B.k1 - B.k0 + 1;
+    const int ncells = (nxr > 0 && nyr > 0 && nzr > 0) ? nxr * nyr * nzr : 0;
+    for (int base = 0; base < ncells; base += 32) {
+        const int q0 = base + lane;
+        unsigned s0 = 0, cnt = 0;
+        if (q0 < ncells) {
+            const int ci = B.i0 + q0 % nxr, cj = B.j0 + (q0 / nxr) % nyr, ck = B.k0 + q0 / (nxr * nyr);
+            const uint2 rg = __ldg(&P.hcell[ci + P.hx * (cj + P.hy * ck)]);
+            if (rg.y > rg.x) {
+                s0 = rg.x;
+                cnt = rg.y - rg.x;
+            }
+        }
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        for (unsigned g0 = 0; g0 < total; g0 += 32) {  // warp-uniform trip count
+            const unsigned g = g0 + lane;
+            int lo = 0;  // owner lane: first lane whose inclusive prefix exceeds g
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const unsigned pm = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+                if (pm <= g) lo += step;
+            }
+            const unsigned excl = __shfl_sync(0xffffffffu, incl - cnt, lo);
+            const unsigned st = __shfl_sync(0xffffffffu, s0, lo);
+            if (g < total) f(st + (g - excl));
+        }
+    }
+}
+
+// ---- block-cooperative gather of the label's surfels within rg of c from the home grid.
+// Deterministic order: home cells in linear order, each round of blockDim cells compacted by a
 // block prefix sum (so the MLS sums, hence the results, are bitwise reproducible).
 __device__ void gather(const RP& P, int32_t label, const double c[3], float* list, Vtx& V,
                        int* counter, typename BlockScanT::TempStorage& scan) {
@@ -145,32 +188,31 @@ __device__ void gather(const RP& P, int32_t label, const double c[3], float* lis
         V.c[1] = c[1];
         V.c[2] = c[2];
         *counter = 0;
-        atomicAdd(&g_dbg[3], 1ull);
+        if (P.cycles) atomicAdd(&g_dbg[3], 1ull);
     }
     __syncthreads();
-    const float lo[3] = {(float)(c[0] - P.rg), (float)(c[1] - P.rg), (float)(c[2] - P.rg)};
-    const float hi[3] = {(float)(c[0] + P.rg), (float)(c[1] + P.rg), (float)(c[2] + P.rg)};
-    const int i0 = max(0, (int)floorf((lo[0] - P.ox) * P.inv_v)), i1 = min(P.nx - 1, (int)floorf((hi[0] - P.ox) * P.inv_v));
-    const int j0 = max(0, (int)floorf((lo[1] - P.oy) * P.inv_v)), j1 = min(P.ny - 1, (int)floorf((hi[1] - P.oy) * P.inv_v));
-    const int k0 = max(0, (int)floorf((lo[2] - P.oz) * P.inv_v)), k1 = min(P.nz - 1, (int)floorf((hi[2] - P.oz) * P.inv_v));
-    const int nxr = i1 - i0 + 1, nyr = j1 - j0 + 1, nzr = k1 - k0 + 1;
+    const Box B = home_box(P, c, P.rg);
+    const int nxr = B.i1 - B.i0 + 1, nyr = B.j1 - B.j0 + 1, nzr = B.k1 - B.k0 + 1;
     const int ncells = (nxr > 0 && nyr > 0 && nzr > 0) ? nxr * nyr * nzr : 0;
     const double rg2 = P.rg * P.rg;
+    auto match = [&](unsigned k, float4& A, float4& nv) {
+        A = __ldg(&P.hrec[2 * k]);
+        const double dx = (double)A.x - c[0], dy = (double)A.y - c[1], dz = (double)A.z - c[2];
+        if (dx * dx + dy * dy + dz * dz > rg2) return false;
+        nv = __ldg(&P.hrec[2 * k + 1]);
+        return __float_as_int(nv.w) == label;
+    };
     for (int base = 0; base < ncells; base += blockDim.x) {
         const int q = base + tid;
-        int ci = 0, cj = 0, ck = 0;
         uint2 rg = make_uint2(0, 0);
         int cnt = 0;
         if (q < ncells) {
-            ci = i0 + q % nxr;
-            cj = j0 + (q / nxr) % nyr;
-            ck = k0 + q / (nxr * nyr);
-            rg = __ldg(&P.cell[ci + P.nx * (cj + P.ny * ck)]);
-            if (rg.y > rg.x)
-                for (unsigned k = rg.x; k < rg.y; ++k) {
-                    float4 A, nv;
-                    cnt += cand_match(P, k, ci, cj, ck, label, c, rg2, A, nv);
-                }
+            const int ci = B.i0 + q % nxr, cj = B.j0 + (q / nxr) % nyr, ck = B.k0 + q / (nxr * nyr);
+            rg = __ldg(&P.hcell[ci + P.hx * (cj + P.hy * ck)]);
+            for (unsigned k = rg.x; k < rg.y; ++k) {
+                float4 A, nv;
+                cnt += match(k, A, nv);
+            }
         }
         int off = 0, tot = 0;
         BlockScanT(scan).ExclusiveSum(cnt, off, tot);
@@ -178,7 +220,7 @@ __device__ void gather(const RP& P, int32_t label, const double c[3], float* lis
         if (cnt)
             for (unsigned k = rg.x, w = 0; k < rg.y; ++k) {
                 float4 A, nv;
-                if (!cand_match(P, k, ci, cj, ck, label, c, rg2, A, nv)) continue;
+                if (!match(k, A, nv)) continue;
                 const int at = start + off + (int)w++;
                 if (at < kCapS) {
                     float* e = list + 6 * at;
@@ -202,7 +244,7 @@ __device__ void gather(const RP& P, int32_t label, const double c[3], float* lis
 }
 
 // ---- MLS (Eqs. 1-4) at x, one warp.  From the shared list when x lies in the safe ball of
-// the gather centre, else by a direct scan of the grid (home-cell dedupe, same label).
+// the gather centre, else by a direct scan of the home grid (same set, another order).
 __device__ bool mls(const RP& P, const Path& D, int k, const double x[3], const float* list,
                     const Vtx& V, double pb[3], double nb[3], int lane) {
     const double inv2s2 = 1.0 / (2.0 * P.sigma * P.sigma);
@@ -233,48 +275,15 @@ __device__ bool mls(const RP& P, const Path& D, int k, const double x[3], const 
             acc(e[0], e[1], e[2], e[3], e[4], e[5]);
         }
     } else {
-        const double R = 4.0 * P.sigma;
-        const float lo[3] = {(float)(x[0] - R), (float)(x[1] - R), (float)(x[2] - R)};
-        const float hi[3] = {(float)(x[0] + R), (float)(x[1] + R), (float)(x[2] + R)};
-        const int i0 = max(0, (int)floorf((lo[0] - P.ox) * P.inv_v)), i1 = min(P.nx - 1, (int)floorf((hi[0] - P.ox) * P.inv_v));
-        const int j0 = max(0, (int)floorf((lo[1] - P.oy) * P.inv_v)), j1 = min(P.ny - 1, (int)floorf((hi[1] - P.oy) * P.inv_v));
-        const int k0 = max(0, (int)floorf((lo[2] - P.oz) * P.inv_v)), k1 = min(P.nz - 1, (int)floorf((hi[2] - P.oz) * P.inv_v));
-        // cell headers 32 at a time; the warp walks the non-empty ones (ballot) with lanes
-        // splitting each cell's records; distance and home cell are decided from the first
-        // float4 before the dependent loads of the normal and label
-        const int nxr = i1 - i0 + 1, nyr = j1 - j0 + 1, nzr = k1 - k0 + 1;
-        const int ncells = (nxr > 0 && nyr > 0 && nzr > 0) ? nxr * nyr * nzr : 0;
-        for (int base = 0; base < ncells; base += 32) {
-            const int q0 = base + lane;
-            int ci = 0, cj = 0, ck = 0;
-            uint2 rg = make_uint2(0, 0);
-            if (q0 < ncells) {
-                ci = i0 + q0 % nxr;
-                cj = j0 + (q0 / nxr) % nyr;
-                ck = k0 + q0 / (nxr * nyr);
-                rg = __ldg(&P.cell[ci + P.nx * (cj + P.ny * ck)]);
-            }
-            unsigned live = __ballot_sync(0xffffffffu, rg.y > rg.x);
-            while (live) {
-                const int src = __ffs(live) - 1;
-                live &= live - 1;
-                const unsigned s0 = __shfl_sync(0xffffffffu, rg.x, src), s1 = __shfl_sync(0xffffffffu, rg.y, src);
-                const int cx = __shfl_sync(0xffffffffu, ci, src), cy = __shfl_sync(0xffffffffu, cj, src),
-                          cz = __shfl_sync(0xffffffffu, ck, src);
-                for (unsigned q = s0 + lane; q < s1; q += 32) {
-                    const float4 A = __ldg(&P.rec[2 * q]);
-                    const double d0 = (double)A.x - x[0], d1 = (double)A.y - x[1], d2 = (double)A.z - x[2];
-                    if ((d0 * d0 + d1 * d1) + d2 * d2 > r2) continue;
-                    const int hx = (int)floorf((A.x - P.ox) * P.inv_v), hy = (int)floorf((A.y - P.oy) * P.inv_v),
-                              hz = (int)floorf((A.z - P.oz) * P.inv_v);
-                    if (hx != cx || hy != cy || hz != cz) continue;
-                    const float4 B = __ldg(&P.rec[2 * q + 1]);
-                    const float4 nv = __ldg(&P.sn[__float_as_uint(B.w)]);
-                    if (__float_as_int(nv.w) != D.label[k]) continue;
-                    acc(A.x, A.y, A.z, nv.x, nv.y, nv.z);
-                }
-            }
-        }
+        const int32_t label = D.label[k];
+        scan_box(P, home_box(P, x, 4.0 * P.sigma), lane, [&](unsigned q) {
+            const float4 A = __ldg(&P.hrec[2 * q]);
+            const double d0 = (double)A.x - x[0], d1 = (double)A.y - x[1], d2 = (double)A.z - x[2];
+            if ((d0 * d0 + d1 * d1) + d2 * d2 > r2) return;
+            const float4 nv = __ldg(&P.hrec[2 * q + 1]);
+            if (__float_as_int(nv.w) != label) return;
+            acc(A.x, A.y, A.z, nv.x, nv.y, nv.z);
+        });
     }
     W = wsum(W);
     if (P.cycles && lane == 0) atomicAdd(&g_dbg[use_list ? 4 : 5], (unsigned long long)(clock64() - t_mls0));
@@ -381,8 +390,12 @@ __device__ void residual_all(const RP& P, const Path& D, const double* z, const 
             }
     }
     __syncwarp();
+    // vertex residuals in parallel (lane k -> vertex k), then |r|^2 in index order on lane 0
+    bool okv = true;
+    if (ok && lane < D.n) okv = vertex_residual(P, D, z, lane, T.pb[lane], T.nb[lane], T.r);
+    ok = ok && __all_sync(0xffffffffu, okv);
+    __syncwarp();
     if (ok && lane == 0) {
-        for (int k = 0; k < D.n && ok; ++k) ok = vertex_residual(P, D, z, k, T.pb[k], T.nb[k], T.r);
         double f = 0;
         for (int i = 0; i < D.dim; ++i) f += T.r[i] * T.r[i];
         T.f = f;
@@ -449,34 +462,21 @@ __device__ bool occluded(const RP& P, const double x0[3], const double x1[3], co
     }
 }
 
-// support (R25 c) over every same-label surfel near x: direct scan, one warp
+// support (R25 c) over every same-label surfel near x (home grid, one warp)
 __device__ bool supported(const RP& P, int32_t label, const double x[3], int lane) {
-    const double R = (double)P.rq;
-    const float lo[3] = {(float)(x[0] - R), (float)(x[1] - R), (float)(x[2] - R)};
-    const float hi[3] = {(float)(x[0] + R), (float)(x[1] + R), (float)(x[2] + R)};
-    const int i0 = max(0, (int)floorf((lo[0] - P.ox) * P.inv_v)), i1 = min(P.nx - 1, (int)floorf((hi[0] - P.ox) * P.inv_v));
-    const int j0 = max(0, (int)floorf((lo[1] - P.oy) * P.inv_v)), j1 = min(P.ny - 1, (int)floorf((hi[1] - P.oy) * P.inv_v));
-    const int k0 = max(0, (int)floorf((lo[2] - P.oz) * P.inv_v)), k1 = min(P.nz - 1, (int)floorf((hi[2] - P.oz) * P.inv_v));
     bool s = false;
-    const int nxr = i1 - i0 + 1, nyr = j1 - j0 + 1, nzr = k1 - k0 + 1;
-    const int ncells = (nxr > 0 && nyr > 0 && nzr > 0) ? nxr * nyr * nzr : 0;
-    for (int q0 = lane; q0 < ncells && !s; q0 += 32) {
-        const int ci = i0 + q0 % nxr, cj = j0 + (q0 / nxr) % nyr, ck = k0 + q0 / (nxr * nyr);
-        const uint2 rg = __ldg(&P.cell[ci + P.nx * (cj + P.ny * ck)]);
-        for (unsigned q = rg.x; q < rg.y && rg.y > rg.x; ++q) {
-            const float4 A = __ldg(&P.rec[2 * q]);
-            const float4 B = __ldg(&P.rec[2 * q + 1]);
-            const float4 nv = __ldg(&P.sn[__float_as_uint(B.w)]);
-            if (__float_as_int(nv.w) != label) continue;
-            const double w[3] = {x[0] - A.x, x[1] - A.y, x[2] - A.z};
-            const double n[3] = {B.x, B.y, B.z};
-            const double r = A.w;
-            if (fabs(ddot(w, n)) <= P.tau && ddot(w, w) <= r * r + P.tau * P.tau) {
-                s = true;
-                break;
-            }
-        }
-    }
+    const double lim2 = P.rq * P.rq;
+    scan_box(P, home_box(P, x, P.rq), lane, [&](unsigned q) {
+        if (s) return;
+        const float4 A = __ldg(&P.hrec[2 * q]);
+        const double w[3] = {x[0] - A.x, x[1] - A.y, x[2] - A.z};
+        if (ddot(w, w) > lim2) return;
+        const float4 nv = __ldg(&P.hrec[2 * q + 1]);
+        if (__float_as_int(nv.w) != label) return;
+        const double n[3] = {nv.x, nv.y, nv.z};
+        const double r = A.w;
+        if (fabs(ddot(w, n)) <= P.tau && ddot(w, w) <= r * r + P.tau * P.tau) s = true;
+    });
     return __any_sync(0xffffffffu, s);
 }
 
@@ -571,6 +571,14 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
                 }
                 __syncthreads();
                 for (it = 1; it <= P.max_iter; ++it) {
+                    long long tph = clock64();
+                    auto phase = [&](int slot) {
+                        if (P.cycles && tid == 0) {
+                            const long long t = clock64();
+                            atomicAdd(&g_dbg[slot], (unsigned long long)(t - tph));
+                            tph = t;
+                        }
+                    };
                     // keep every vertex inside the safe ball of its candidate list: re-centre
                     // the gather when the iterate drifted more than half the margin
                     for (int k = 0; k < D.n; ++k) {
@@ -584,6 +592,7 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
                             gather(P, D.label[k], xc, cand_ptr(cand, D.slot[k]), S.V[D.slot[k]], &counter, scan);
                         }
                     }
+                    phase(8);
                     // ---- Jacobian: column j on warp j mod NW (only vertex k's MLS moves)
                     if (tid < NW) S.flag[tid] = 1;
                     __syncthreads();
@@ -602,14 +611,21 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
                                 vpoint(P, D, zz, k, x);
                                 okj = mls(P, D, k, x, cand_ptr(cand, D.slot[k]), S.V[D.slot[k]], pbk, nbk, lane);
                             }
-                            if (okj && lane == 0) {
-                                double* rr = sgn == 0 ? T.r : T.pb[0];  // T.pb as scratch (24 doubles)
-                                for (int q2 = 0; q2 < D.n && okj; ++q2) {
+                            // only vertices k-1, k, k+1 see unknown j; the rest keep r(z)
+                            double* rr = sgn == 0 ? T.r : T.pb[0];  // T.pb as scratch (24 doubles)
+                            bool okv = true;
+                            if (okj && lane < D.n) {
+                                const int q2 = lane;
+                                if (q2 >= k - 1 && q2 <= k + 1) {
                                     const bool mine = q2 == k && D.kind[k] == 0;
-                                    okj = vertex_residual(P, D, zz, q2, mine ? pbk : S.pb[q2], mine ? nbk : S.nb[q2], rr);
+                                    okv = vertex_residual(P, D, zz, q2, mine ? pbk : S.pb[q2], mine ? nbk : S.nb[q2], rr);
+                                } else {
+                                    const int c0 = D.col[q2], c1 = q2 + 1 < D.n ? D.col[q2 + 1] : m;
+                                    for (int i = c0; i < c1; ++i) rr[i] = S.r[i];
                                 }
                             }
-                            okj = __shfl_sync(0xffffffffu, okj, 0);
+                            okj = okj && __all_sync(0xffffffffu, okv);
+                            __syncwarp();
                         }
                         if (lane == 0) {
                             if (okj)
@@ -626,6 +642,7 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
                         status = NRT_REF_NO_SUPPORT;
                         break;
                     }
+                    phase(9);
                     // ---- normal equations (whole block) + Cholesky solve (warp 0), m <= 24
                     for (int e = tid; e < m * m + m; e += blockDim.x) {
                         if (e < m * m) {
@@ -702,6 +719,7 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
                         __syncthreads();
                         break;
                     }
+                    phase(10);
                     // ---- backtracking: NW trials per round, first accepted in sequence order
                     const double f0 = [&] {
                         double s = 0;
@@ -756,6 +774,7 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
                         }
                         __syncthreads();
                     }
+                    phase(11);
                     if (accepted == NW) {
                         status = NRT_REF_NO_CONVERGE;
                         break;
@@ -904,6 +923,12 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     P.nx = s->dims[0];
     P.ny = s->dims[1];
     P.nz = s->dims[2];
+    P.hcell = s->hcell;
+    P.hrec = s->hrec;
+    P.inv_hv = s->inv_hv;
+    P.hx = s->hdims[0];
+    P.hy = s->hdims[1];
+    P.hz = s->hdims[2];
     P.edges = s->edges;
     P.in = (const nrt_coarse_rec*)coarse->d_rec;
     P.n_in = n;
@@ -993,8 +1018,10 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
         for (int64_t i = 0; i < n_mine; ++i) tot += cyc[i];
         fprintf(stderr, "[nrt] refine: %lld paths, sum %.3g cycles, blocks %lld\n", (long long)n_mine,
                 (double)tot, (long long)blocks);
-        unsigned long long dbg[8];
+        unsigned long long dbg[12];
         cudaMemcpyFromSymbol(dbg, g_dbg, sizeof(dbg));
+        fprintf(stderr, "[nrt]   block cycles: regather %.3g jacobian %.3g solve %.3g linesearch %.3g\n",
+                (double)dbg[8], (double)dbg[9], (double)dbg[10], (double)dbg[11]);
         fprintf(stderr, "[nrt]   mls list %llu direct %llu, ls rounds %llu, gathers %llu\n", dbg[0], dbg[1],
                 dbg[2], dbg[3]);
         fprintf(stderr, "[nrt]   avg cycles: mls list %.0f direct %.0f\n", (double)dbg[4] / (dbg[0] + 1),

@@ -220,6 +220,30 @@ __global__ void k_pack_skip(uint2* cell, int64_t ncell, const unsigned char* f) 
     cell[c] = make_uint2(D, D);  // empty: x == y == Chebyshev distance to non-empty (>= 1)
 }
 
+// home grid: key = linear index of the hv-cell containing p (each surfel exactly once)
+__global__ void k_home_keys(const float4* sp, int64_t n, float ox, float oy, float oz, float inv_hv,
+                            int hx, int hy, int hz, unsigned* keys, unsigned* vals) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 p = sp[i];
+    const int x = min(hx - 1, max(0, (int)floorf((p.x - ox) * inv_hv)));
+    const int y = min(hy - 1, max(0, (int)floorf((p.y - oy) * inv_hv)));
+    const int z = min(hz - 1, max(0, (int)floorf((p.z - oz) * inv_hv)));
+    keys[i] = (unsigned)(x + hx * (y + hy * z));
+    vals[i] = (unsigned)i;
+}
+__global__ void k_home_records(const unsigned* keys, const unsigned* ids, int64_t n, const float4* sp,
+                               const float4* sn, float4* hrec, uint2* hcell) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const unsigned id = ids[k];
+    hrec[2 * k] = sp[id];
+    hrec[2 * k + 1] = sn[id];
+    const unsigned key = keys[k];
+    if (k == 0 || keys[k - 1] != key) hcell[key].x = (unsigned)k;
+    if (k == n - 1 || keys[k + 1] != key) hcell[key].y = (unsigned)(k + 1);
+}
+
 template <class T>
 nrt_status dmalloc(T** p, size_t count, cudaStream_t st) {
     if (count == 0) count = 1;
@@ -415,6 +439,40 @@ static nrt_status build_impl(const nrt_scene_desc* D, nrt_scene S, cudaStream_t 
         NRT_CUDA(cudaGetLastError());
         cudaFreeAsync(f0, st);
         cudaFreeAsync(f1, st);
+    }
+    // ---- home grid (refinement neighbourhoods): cell 2v, one record per surfel
+    {
+        S->hv = 2.0f * v;
+        S->inv_hv = 1.0f / S->hv;
+        for (int a = 0; a < 3; ++a) S->hdims[a] = (dims[a] + 1) / 2;
+        const int64_t nh = (int64_t)S->hdims[0] * S->hdims[1] * S->hdims[2];
+        unsigned *hk0 = nullptr, *hk1 = nullptr, *hv0 = nullptr, *hv1 = nullptr;
+        NRT_TRY(dmalloc(&hk0, n, st));
+        NRT_TRY(dmalloc(&hk1, n, st));
+        NRT_TRY(dmalloc(&hv0, n, st));
+        NRT_TRY(dmalloc(&hv1, n, st));
+        k_home_keys<<<nb, 256, 0, st>>>(S->sp, n, g.ox, g.oy, g.oz, S->inv_hv, S->hdims[0], S->hdims[1],
+                                        S->hdims[2], hk0, hv0);
+        ::nrt::count_launch();
+        int hbits = 1;
+        while (((int64_t)1 << hbits) < nh) ++hbits;
+        cub::DoubleBuffer<unsigned> hkb(hk0, hk1), hvb(hv0, hv1);
+        tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, hkb, hvb, (int)n, 0, hbits, st);
+        NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+        cub::DeviceRadixSort::SortPairs(tmp, tb, hkb, hvb, (int)n, 0, hbits, st);
+        cudaFreeAsync(tmp, st);
+        NRT_TRY(dmalloc(&S->hrec, 2 * n, st));
+        NRT_TRY(dmalloc(&S->hcell, nh, st));
+        NRT_CUDA(cudaMemsetAsync(S->hcell, 0, nh * sizeof(uint2), st));
+        k_home_records<<<nb, 256, 0, st>>>(hkb.Current(), hvb.Current(), n, S->sp, S->sn, S->hrec,
+                                           S->hcell);
+        ::nrt::count_launch();
+        NRT_CUDA(cudaGetLastError());
+        cudaFreeAsync(hk0, st);
+        cudaFreeAsync(hk1, st);
+        cudaFreeAsync(hv0, st);
+        cudaFreeAsync(hv1, st);
     }
     // labels array (int) for the history
     {
