@@ -253,6 +253,11 @@ const char* nrt_last_error(void);
 const char* nrt_version(void);
 /* Number of CUDA kernels this library has launched in the process so far (evidence counter). */
 uint64_t nrt_kernel_launches(void);
+/* Bytes of device memory the library keeps cached between launches (wavefront workspaces:
+ * per-ray state of the rays in flight, up to ~300 B x 2^24 rays), and a call that returns
+ * all idle cached blocks to the CUDA memory pool.  Must not race with a running launch. */
+uint64_t nrt_workspace_bytes(void);
+void nrt_workspace_trim(void);
 
 #ifdef __cplusplus
 }

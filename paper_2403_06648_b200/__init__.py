@@ -126,6 +126,8 @@ _SIGS = {
     "nrt_last_error": ([], C.c_char_p),
     "nrt_version": ([], C.c_char_p),
     "nrt_kernel_launches": ([], C.c_uint64),
+    "nrt_workspace_bytes": ([], C.c_uint64),
+    "nrt_workspace_trim": ([], None),
 }
 EXPORTED = tuple(_SIGS)
 
@@ -448,6 +450,14 @@ def nrt_version() -> str:
 
 def nrt_kernel_launches() -> int:
     return int(lib().nrt_kernel_launches())
+
+
+def nrt_workspace_bytes() -> int:
+    return int(lib().nrt_workspace_bytes())
+
+
+def nrt_workspace_trim() -> None:
+    lib().nrt_workspace_trim()
 
 
 # ------------------------------------------------------------------------------------------

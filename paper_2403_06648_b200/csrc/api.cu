@@ -5,6 +5,8 @@
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include <cmath>
 #include <cstdarg>
@@ -55,6 +57,64 @@ void ensure_pool(int dev) {
     }
     done.fetch_or(bit);
 }
+
+namespace {
+struct WsBlock {
+    int dev;
+    void* p;
+    size_t bytes;
+    bool busy;
+};
+std::mutex g_ws_mu;
+std::vector<WsBlock> g_ws;
+}  // namespace
+
+void* ws_get(int dev, size_t bytes, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    WsBlock* best = nullptr;
+    for (auto& b : g_ws)
+        if (!b.busy && b.dev == dev && b.bytes >= bytes && (!best || b.bytes < best->bytes))
+            best = &b;
+    if (best) {
+        best->busy = true;
+        return best->p;
+    }
+    const size_t gran = 64ull << 20;
+    const size_t sz = (bytes + gran - 1) / gran * gran;
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, sz, st) != cudaSuccess) {
+        cudaGetLastError();
+        // idle cached blocks of this device may be what stands in the way: drop them, retry
+        for (auto it = g_ws.begin(); it != g_ws.end();) {
+            if (!it->busy && it->dev == dev) {
+                cudaFreeAsync(it->p, st);
+                it = g_ws.erase(it);
+            } else {
+                ++it;
+            }
+        }
+        cudaStreamSynchronize(st);
+        if (cudaMallocAsync(&p, sz, st) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+    }
+    g_ws.push_back({dev, p, sz, true});
+    return p;
+}
+
+void ws_put(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto& b : g_ws)
+        if (b.p == p) b.busy = false;
+}
+
+struct RxGuard {  // frees a launch's receiver grid on every exit path
+    RxGrid* g;
+    cudaStream_t st;
+    ~RxGuard() { rxgrid_free(g, st); }
+};
 
 // NRT_PHASES=1: synchronise and print host wall time per phase (diagnostics only)
 struct PhaseLog {
@@ -148,6 +208,30 @@ extern "C" {
 const char* nrt_last_error(void) { return g_err; }
 const char* nrt_version(void) { return "nrt 0.1 (sm_100a)"; }
 uint64_t nrt_kernel_launches(void) { return g_launches.load(); }
+
+uint64_t nrt_workspace_bytes(void) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    uint64_t t = 0;
+    for (auto& b : g_ws) t += b.bytes;
+    return t;
+}
+
+void nrt_workspace_trim(void) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto it = g_ws.begin(); it != g_ws.end();) {
+        if (!it->busy) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(it->dev);
+            cudaFreeAsync(it->p, nullptr);
+            cudaStreamSynchronize(nullptr);
+            cudaSetDevice(cur);
+            it = g_ws.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
 
 nrt_status nrt_scene_build(const float* points, const float* normals, int64_t n, float voxel_size,
                            nrt_scene* out) {
@@ -271,6 +355,14 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
     a.max_refl = max_refl;
     a.max_diff = max_diff;
     a.desc = d;
+    float r_prim = 0, r_fan = 0;
+    capture_radius_bounds(s, a, &r_prim, &r_fan);
+    NRT_TRY(rxgrid_build(s, hrx.data(), n_rx, r_prim, &a.rxg, st));
+    RxGuard rx_guard{&a.rxg, st};
+    LaunchArgs af = a;  // fans: capture radii up to r_fan (R16)
+    af.rxg = RxGrid{};
+    if (max_diff > 0 && s->n_edges > 0) NRT_TRY(rxgrid_build(s, hrx.data(), n_rx, r_fan, &af.rxg, st));
+    RxGuard rx_guard_f{&af.rxg, st};
 
     nrt_paths P = new nrt_paths_s();
     P->kind = NRT_PATHS_COARSE;
@@ -330,7 +422,7 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
         uint64_t b2 = 0;
         {
             KernelStats ks;
-            rc = launch_fans(s, a, evu, n_evu, &fraw, &nf, &nfr, &b2, &ks, st);
+            rc = launch_fans(s, af, evu, n_evu, &fraw, &nf, &nfr, &b2, &ks, st);
             P->info.ms_fans = ks.ms_kernel;
             P->info.surfel_tests += ks.tests;
             P->info.cells_visited += ks.cells;
@@ -391,6 +483,10 @@ nrt_status nrt_launch_fans(nrt_scene s, nrt_paths coarse, const void* events, in
     a.desc = d;
     NRT_TRY(check_launch(s, coarse->tx, coarse->rx.data(), a.n_rx, a.n_rays, a.max_refl, a.max_diff,
                          [&] { nrt_launch_desc x = d; x.stage = 1; return x; }()));
+    float r_prim = 0, r_fan = 0;
+    capture_radius_bounds(s, a, &r_prim, &r_fan);
+    NRT_TRY(rxgrid_build(s, coarse->rx.data(), a.n_rx, r_fan, &a.rxg, st));
+    RxGuard rx_guard{&a.rxg, st};
     float* d_rx = nullptr;
     NRT_CUDA(cudaMallocAsync(&d_rx, 12 * (size_t)(a.n_rx > 0 ? a.n_rx : 1), st));
     if (a.n_rx)

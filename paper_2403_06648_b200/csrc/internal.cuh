@@ -21,6 +21,12 @@ nrt_status set_error(nrt_status st, const char* fmt, ...);
 void clear_error();
 void count_launch();  // every kernel launch of the library increments a process-wide counter
 void ensure_pool(int dev);  // default mempool keeps freed memory cached
+// Workspace cache for large per-launch buffers (wavefront state).  Growing the stream-ordered
+// pool by gigabytes maps fresh physical pages (~50 ms/GB measured), so the biggest buffers are
+// kept across launches: ws_get returns an idle cached block of >= bytes on dev (or a new one);
+// ws_put marks it idle again and may only be called once no queued work still uses it.
+void* ws_get(int dev, size_t bytes, cudaStream_t st);
+void ws_put(void* p);
 
 #define NRT_CUDA(call)                                                                    \
     do {                                                                                  \
@@ -171,6 +177,13 @@ nrt_status dedupe_events(const nrt_event_rec* in, int64_t n, nrt_event_rec* out,
 nrt_status dedupe_refined(const nrt_refined_rec* in, int64_t n, nrt_refined_rec* out,
                           int64_t* n_out, cudaStream_t st);
 // launch.cu
+struct RxGrid {  // receiver home grid (device arrays; null when the RX set is small)
+    uint2* cell = nullptr;
+    float4* rx = nullptr;
+    float o[3] = {0, 0, 0}, v = 0, tmax = 0;
+    float lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};  // tight bounding box of the receivers
+    int n[3] = {0, 0, 0};
+};
 struct LaunchArgs {
     float tx[3];
     const float* d_rx;  // device
@@ -178,7 +191,13 @@ struct LaunchArgs {
     int64_t n_rays;
     int32_t max_refl, max_diff;
     nrt_launch_desc desc;
+    RxGrid rxg;
 };
+// build / free the receiver grid for rx (host, n_rx x 3) around the scene grid
+nrt_status rxgrid_build(nrt_scene s, const float* rx, int32_t n_rx, float rreg, RxGrid* g,
+                        cudaStream_t st);
+void capture_radius_bounds(nrt_scene s, const LaunchArgs& a, float* r_primary, float* r_fan);
+void rxgrid_free(RxGrid* g, cudaStream_t st);
 struct KernelStats {
     float ms_kernel = 0;  // device time of the traversal kernel alone
     unsigned long long tests = 0, cells = 0, nonempty = 0;  // counters build only

@@ -18,11 +18,14 @@
 
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -53,6 +56,7 @@ struct RayCold {
 };
 
 struct Wave {
+    void* slab;      // one workspace block holding all arrays below
     float4* o;       // [cap] origin xyz, prev surfel id (int bits)
     float4* d;       // [cap] direction
     float4* l0;      // [cap] departure-sheet normal 0
@@ -81,6 +85,12 @@ struct TP {  // trace parameters (by value into the kernels)
     int max_refl, max_diff;
     float tau, cos_ex, cRw, b_e, edge_bin, c_R, dphi_deg;
     float slack;  // absolute slack of the division-free disk prefilter (m)
+    // receiver home grid (many RX): cells of rxg_v, RX sorted by cell as (x, y, z, j bits)
+    const uint2* rxg_cell;
+    const float4* rxg_rx;
+    float rxg_o[3], rxg_v, rxg_inv, rxg_tmax;
+    float rxg_lo[3], rxg_hi[3];  // tight bounding box of the receivers
+    int rxg_n[3];
     const DevEdge* edges;
     int n_edges;
     // outputs
@@ -223,18 +233,79 @@ __device__ void write_record(const TP& P, const Hist& h, int rx, float L, uint64
 }
 
 // ---- A5: RX reception spheres (R12 / R16) ---------------------------------------------
+// the capture test of RX j exactly as the definition orders it
+__device__ __forceinline__ void rx_test(const TP& P, const Hist& h, float3 o, float3 d, float t_hit,
+                                        float L, float Ls, float kR, float R0, bool after_diff,
+                                        uint64_t ray_id, int j, float x0, float x1, float x2) {
+    const float wx = x0 - o.x, wy = x1 - o.y, wz = x2 - o.z;
+    const float tj = (wx * d.x + wy * d.y) + wz * d.z;
+    if (!(tj > 0.0f && tj < t_hit)) return;
+    const float px = wx - tj * d.x, py = wy - tj * d.y, pz = wz - tj * d.z;
+    const float pp = (px * px + py * py) + pz * pz;
+    const float R = after_diff ? kR * (Ls + tj) + R0 : kR * (L + tj);
+    if (!(pp <= R * R)) return;
+    write_record(P, h, j, L + tj, ray_id);
+}
+
 __device__ void rx_captures(const TP& P, const Hist& h, float3 o, float3 d, float t_hit, float L,
                             float Ls, float kR, float R0, bool after_diff, uint64_t ray_id) {
-    for (int j = 0; j < P.n_rx; ++j) {
-        const float x0 = P.rx[3 * j], x1 = P.rx[3 * j + 1], x2 = P.rx[3 * j + 2];
-        const float wx = x0 - o.x, wy = x1 - o.y, wz = x2 - o.z;
-        const float tj = (wx * d.x + wy * d.y) + wz * d.z;
-        if (!(tj > 0.0f && tj < t_hit)) continue;
-        const float px = wx - tj * d.x, py = wy - tj * d.y, pz = wz - tj * d.z;
-        const float pp = (px * px + py * py) + pz * pz;
-        const float R = after_diff ? kR * (Ls + tj) + R0 : kR * (L + tj);
-        if (!(pp <= R * R)) continue;
-        write_record(P, h, j, L + tj, ray_id);
+    if (!P.rxg_cell) {  // few receivers: test them all
+        for (int j = 0; j < P.n_rx; ++j)
+            rx_test(P, h, o, d, t_hit, L, Ls, kR, R0, after_diff, ray_id, j, P.rx[3 * j],
+                    P.rx[3 * j + 1], P.rx[3 * j + 2]);
+        return;
+    }
+    // many receivers: every receiver is registered in all cells of the receiver grid within
+    // the launch's largest capture radius Rreg (+ pad) of it.  The segment walks that grid by
+    // 3D-DDA; the walk's cell t-intervals partition the segment, and receiver j is tested only
+    // in the cell whose interval holds its closest-approach parameter t_j — whose point lies
+    // within R <= Rreg of the receiver, so the receiver is registered there: every capturable
+    // receiver is tested exactly once.
+    float T = fminf(t_hit, P.rxg_tmax);
+    float t0 = 0.0f;
+    const float ov[3] = {o.x, o.y, o.z}, dv[3] = {d.x, d.y, d.z};
+    for (int a = 0; a < 3; ++a) {  // clip to the grid box (it holds every receiver's ball)
+        const float lo = P.rxg_o[a], hi = P.rxg_o[a] + P.rxg_n[a] * P.rxg_v;
+        if (dv[a] != 0.0f) {
+            const float inv = 1.0f / dv[a];
+            const float ta = (lo - ov[a]) * inv, tb = (hi - ov[a]) * inv;
+            t0 = fmaxf(t0, fminf(ta, tb));
+            T = fminf(T, fmaxf(ta, tb));
+        } else if (ov[a] < lo || ov[a] > hi) {
+            T = -1.0f;
+        }
+    }
+    if (!(t0 < T)) return;
+    int c[3];
+    float tm[3], inv[3];
+    for (int a = 0; a < 3; ++a) {
+        const float p = ov[a] + t0 * dv[a];
+        c[a] = min(P.rxg_n[a] - 1, max(0, (int)floorf((p - P.rxg_o[a]) * P.rxg_inv)));
+        inv[a] = 1.0f / dv[a];
+        tm[a] = dv[a] != 0.0f ? ((P.rxg_o[a] + (float)(c[a] + (dv[a] > 0.0f)) * P.rxg_v) - ov[a]) * inv[a]
+                              : INFINITY;
+    }
+    float t_in = t0;
+    for (;;) {
+        int ax = 0;
+        if (tm[1] < tm[ax]) ax = 1;
+        if (tm[2] < tm[ax]) ax = 2;
+        const float t_out = tm[ax];
+        const bool last = !(t_out < T);
+        const uint2 rg = __ldg(&P.rxg_cell[c[0] + P.rxg_n[0] * (c[1] + P.rxg_n[1] * c[2])]);
+        for (unsigned q = rg.x; q < rg.y; ++q) {
+            const float4 r = __ldg(&P.rxg_rx[q]);
+            const float wx = r.x - o.x, wy = r.y - o.y, wz = r.z - o.z;
+            const float tj = (wx * d.x + wy * d.y) + wz * d.z;
+            if (!((tj >= t_in || t_in == t0) && (tj < t_out || last))) continue;  // owner cell
+            rx_test(P, h, o, d, t_hit, L, Ls, kR, R0, after_diff, ray_id, __float_as_int(r.w), r.x,
+                    r.y, r.z);
+        }
+        if (last) break;
+        c[ax] += dv[ax] > 0.0f ? 1 : -1;
+        if (c[ax] < 0 || c[ax] >= P.rxg_n[ax]) break;
+        t_in = t_out;
+        tm[ax] = ((P.rxg_o[ax] + (float)(c[ax] + (dv[ax] > 0.0f)) * P.rxg_v) - ov[ax]) * inv[ax];
     }
 }
 
@@ -635,11 +706,12 @@ __global__ void k_order_keys(const float4* d, uint64_t n, uint64_t band, unsigne
 }
 
 // primary ray generation (A2): lattice index i = rank + j * world
-__global__ void k_gen_primary(TP P, Wave W, uint64_t n_shard) {
+// batch slots j in [0, n_batch) hold shard rays j0 + j
+__global__ void k_gen_primary(TP P, Wave W, uint64_t n_shard, uint64_t j0) {
     const bool edges_on = P.n_edges > 0 && P.max_diff > 0;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_shard;
          j += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = (uint64_t)P.rank + j * (uint64_t)P.world;
+        const uint64_t i = (uint64_t)P.rank + (j0 + j) * (uint64_t)P.world;
         const float3 d = fib_dir(i, P.n_rays);
         W.o[j] = make_float4(P.tx, P.ty, P.tz, __int_as_float(-1));
         W.d[j] = make_float4(d.x, d.y, d.z, 0.0f);
@@ -768,6 +840,17 @@ TP make_tp(nrt_scene s, const LaunchArgs& a) {
     P.dphi_deg = a.desc.dphi_deg;
     P.edges = s->edges;
     P.n_edges = s->n_edges;
+    P.rxg_cell = a.rxg.cell;
+    P.rxg_rx = a.rxg.rx;
+    for (int k = 0; k < 3; ++k) {
+        P.rxg_o[k] = a.rxg.o[k];
+        P.rxg_n[k] = a.rxg.n[k];
+        P.rxg_lo[k] = a.rxg.lo[k];
+        P.rxg_hi[k] = a.rxg.hi[k];
+    }
+    P.rxg_v = a.rxg.v;
+    P.rxg_inv = a.rxg.v > 0 ? 1.0f / a.rxg.v : 0.0f;
+    P.rxg_tmax = a.rxg.tmax;
     return P;
 }
 
@@ -792,6 +875,90 @@ unsigned persistent_blocks(K kernel, int dev) {
 
 }  // namespace
 
+nrt_status rxgrid_build(nrt_scene s, const float* rx, int32_t n_rx, float rreg, RxGrid* g,
+                        cudaStream_t st) {
+    *g = RxGrid{};
+    const char* e = getenv("NRT_RX_GRID_MIN");
+    const int min_rx = e ? atoi(e) : 16;
+    const char* ev = getenv("NRT_RX_GRID_V");
+    const float v = ev ? (float)atof(ev) : 0.5f;
+    // few receivers, or capture balls larger than the cells: the all-receivers loop is cheaper
+    if (n_rx < min_rx || n_rx <= 0 || !(rreg <= 2.0f * v)) return NRT_OK;
+    (void)s;
+    const float reg = rreg * 1.001f + 1e-3f;  // registration radius with a float pad
+    g->v = v;
+    for (int a = 0; a < 3; ++a) {
+        g->lo[a] = rx[a];
+        g->hi[a] = rx[a];
+    }
+    for (int j = 0; j < n_rx; ++j)
+        for (int a = 0; a < 3; ++a) {
+            g->lo[a] = fminf(g->lo[a], rx[3 * j + a]);
+            g->hi[a] = fmaxf(g->hi[a], rx[3 * j + a]);
+        }
+    for (int a = 0; a < 3; ++a) {
+        g->o[a] = g->lo[a] - reg - v;
+        g->n[a] = (int)ceilf((g->hi[a] + reg + v - g->o[a]) / v) + 1;
+    }
+    g->tmax = 1e30f;
+    const int64_t nc = (int64_t)g->n[0] * g->n[1] * g->n[2];
+    std::vector<std::vector<int>> bins(nc);
+    for (int j = 0; j < n_rx; ++j) {
+        int lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::max(0, (int)floorf((rx[3 * j + a] - reg - g->o[a]) / v));
+            hi[a] = std::min(g->n[a] - 1, (int)floorf((rx[3 * j + a] + reg - g->o[a]) / v));
+        }
+        for (int z = lo[2]; z <= hi[2]; ++z)
+            for (int y = lo[1]; y <= hi[1]; ++y)
+                for (int x = lo[0]; x <= hi[0]; ++x)
+                    bins[x + (int64_t)g->n[0] * (y + (int64_t)g->n[1] * z)].push_back(j);
+    }
+    std::vector<uint2> cells(nc);
+    std::vector<float4> srt;
+    srt.reserve(n_rx);
+    for (int64_t c = 0; c < nc; ++c) {
+        cells[c].x = (unsigned)srt.size();
+        for (int j : bins[c]) {
+            float4 r;
+            r.x = rx[3 * j];
+            r.y = rx[3 * j + 1];
+            r.z = rx[3 * j + 2];
+            int jj = j;
+            memcpy(&r.w, &jj, 4);
+            srt.push_back(r);
+        }
+        cells[c].y = (unsigned)srt.size();
+    }
+    NRT_CUDA(cudaMallocAsync(&g->cell, nc * sizeof(uint2), st));
+    NRT_CUDA(cudaMallocAsync(&g->rx, (srt.size() ? srt.size() : 1) * sizeof(float4), st));
+    NRT_CUDA(cudaMemcpyAsync(g->cell, cells.data(), nc * sizeof(uint2), cudaMemcpyHostToDevice, st));
+    if (srt.size())
+        NRT_CUDA(cudaMemcpyAsync(g->rx, srt.data(), srt.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
+    NRT_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+    return NRT_OK;
+}
+
+// largest capture radius of a launch (R12 / R16): L and the distance since an edge are bounded by
+// (segments + 1) grid diagonals; after a diffraction kR = c_R (n pi / M)|sin theta| <= c_R dphi
+void capture_radius_bounds(nrt_scene s, const LaunchArgs& a, float* r_primary, float* r_fan) {
+    double d2 = 0;
+    for (int k = 0; k < 3; ++k) d2 += (double)s->dims[k] * s->v * s->dims[k] * s->v;
+    const double lmax = (a.max_refl + 2.0) * sqrt(d2) + 1.0;
+    *r_primary = (float)(cRw_of(a.desc.c_R, a.n_rays) * lmax);
+    *r_fan = (float)(a.desc.c_R * a.desc.dphi_deg * (kPi / 180.0) * lmax + 0.5 * a.desc.edge_bin);
+}
+
+void rxgrid_free(RxGrid* g, cudaStream_t st) {
+    if (g->cell) cudaFreeAsync(g->cell, st);
+    if (g->rx) cudaFreeAsync(g->rx, st);
+    *g = RxGrid{};
+}
+
+static double host_ms_since(std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+}
+
 struct Counters {
     unsigned long long raw_n, ev_n, bounces, tests, cells, nonempty;
     unsigned long long n_alive[kMaxIter + 1];
@@ -799,30 +966,40 @@ struct Counters {
 };
 
 static std::atomic<unsigned long long> g_hint_raw{0}, g_hint_ev{0}, g_hint_fan{0};
+static const uint64_t kBatch = 1ull << 24;  // rays in flight per wavefront batch
 
 // wavefront buffers for up to `cap` rays (stream-ordered; freed by free_wave)
-static nrt_status alloc_wave(Wave& W, uint64_t cap, cudaStream_t st) {
+static nrt_status alloc_wave(Wave& W, uint64_t cap, int dev, cudaStream_t st) {
     if (cap < 1) cap = 1;
-    NRT_CUDA(cudaMallocAsync(&W.o, cap * sizeof(float4), st));
-    NRT_CUDA(cudaMallocAsync(&W.d, cap * sizeof(float4), st));
-    NRT_CUDA(cudaMallocAsync(&W.l0, cap * sizeof(float4), st));
-    NRT_CUDA(cudaMallocAsync(&W.l1, cap * sizeof(float4), st));
-    NRT_CUDA(cudaMallocAsync(&W.hit, cap * sizeof(float2), st));
-    NRT_CUDA(cudaMallocAsync(&W.cold, cap * sizeof(RayCold), st));
-    NRT_CUDA(cudaMallocAsync(&W.alive[0], cap * sizeof(unsigned), st));
-    NRT_CUDA(cudaMallocAsync(&W.alive[1], cap * sizeof(unsigned), st));
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t b_o = al(cap * sizeof(float4)), b_h = al(cap * sizeof(float2)),
+                 b_c = al(cap * sizeof(RayCold)), b_a = al(cap * sizeof(unsigned));
+    const size_t total = 4 * b_o + b_h + b_c + 2 * b_a;
+    char* p = (char*)ws_get(dev, total, st);
+    if (!p) return set_error(NRT_E_NOMEM, "wavefront workspace of %zu bytes", total);
+    W.slab = p;
+    W.o = (float4*)p;
+    W.d = (float4*)(p + b_o);
+    W.l0 = (float4*)(p + 2 * b_o);
+    W.l1 = (float4*)(p + 3 * b_o);
+    W.hit = (float2*)(p + 4 * b_o);
+    W.cold = (RayCold*)(p + 4 * b_o + b_h);
+    W.alive[0] = (unsigned*)(p + 4 * b_o + b_h + b_c);
+    W.alive[1] = (unsigned*)(p + 4 * b_o + b_h + b_c + b_a);
     return NRT_OK;
 }
+// returns the slab to the workspace cache once no queued kernel still reads it
 static void free_wave(Wave& W, cudaStream_t st) {
-    cudaFreeAsync(W.o, st);
-    cudaFreeAsync(W.d, st);
-    cudaFreeAsync(W.l0, st);
-    cudaFreeAsync(W.l1, st);
-    cudaFreeAsync(W.hit, st);
-    cudaFreeAsync(W.cold, st);
-    cudaFreeAsync(W.alive[0], st);
-    cudaFreeAsync(W.alive[1], st);
+    if (!W.slab) return;
+    cudaStreamSynchronize(st);
+    ws_put(W.slab);
+    W.slab = nullptr;
 }
+struct WaveGuard {  // every exit path of a launch phase
+    Wave* W;
+    cudaStream_t st;
+    ~WaveGuard() { free_wave(*W, st); }
+};
 
 // bounce loop: TRACE + SHADE per bounce; ms_kernel accumulates the TRACE kernels' time
 static nrt_status run_bounces(const TP& P, Wave& W, int iters, int dev, bool counters,
@@ -830,26 +1007,30 @@ static nrt_status run_bounces(const TP& P, Wave& W, int iters, int dev, bool cou
     const unsigned tb = counters ? persistent_blocks(k_trace<true>, dev)
                                  : persistent_blocks(k_trace<false>, dev);
     const unsigned sb = (unsigned)sm_count(dev) * 8;
-    cudaEvent_t ev[2 * kMaxIter + 2];
-    for (int i = 0; i < 2 * iters; ++i) cudaEventCreate(&ev[i]);
+    cudaEvent_t ev[3 * kMaxIter + 3];
+    for (int i = 0; i < 3 * iters; ++i) cudaEventCreate(&ev[i]);
     for (int b = 0; b < iters; ++b) {
-        cudaEventRecord(ev[2 * b], st);
+        cudaEventRecord(ev[3 * b], st);
         if (counters) k_trace<true><<<tb, 128, 0, st>>>(P, W, b);
         else k_trace<false><<<tb, 128, 0, st>>>(P, W, b);
         ::nrt::count_launch();
-        cudaEventRecord(ev[2 * b + 1], st);
+        cudaEventRecord(ev[3 * b + 1], st);
         k_shade<<<sb, 128, 0, st>>>(P, W, b);
         ::nrt::count_launch();
+        cudaEventRecord(ev[3 * b + 2], st);
     }
     NRT_CUDA(cudaGetLastError());
     NRT_CUDA(cudaStreamSynchronize(st));
-    float tot = 0;
+    float tot = 0, shade = 0;
     for (int b = 0; b < iters; ++b) {
-        float ms = 0;
-        cudaEventElapsedTime(&ms, ev[2 * b], ev[2 * b + 1]);
+        float ms = 0, ms2 = 0;
+        cudaEventElapsedTime(&ms, ev[3 * b], ev[3 * b + 1]);
+        cudaEventElapsedTime(&ms2, ev[3 * b + 1], ev[3 * b + 2]);
         tot += ms;
+        shade += ms2;
     }
-    for (int i = 0; i < 2 * iters; ++i) cudaEventDestroy(ev[i]);
+    if (getenv("NRT_PHASES")) fprintf(stderr, "[nrt] bounces: trace %.3f ms shade %.3f ms\n", tot, shade);
+    for (int i = 0; i < 3 * iters; ++i) cudaEventDestroy(ev[i]);
     *ms_trace = tot;
     return NRT_OK;
 }
@@ -857,6 +1038,8 @@ static nrt_status run_bounces(const TP& P, Wave& W, int iters, int dev, bool cou
 nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out,
                           int64_t* n_raw, nrt_event_rec** ev_out, int64_t* n_ev,
                           uint64_t* bounces, KernelStats* stats, cudaStream_t st) {
+    if (getenv("NRT_PHASES")) cudaStreamSynchronize(st);
+    const auto t_start = std::chrono::steady_clock::now();
     TP P = make_tp(s, a);
     const uint64_t n_shard =
         a.n_rays > a.desc.rank ? ((uint64_t)a.n_rays - a.desc.rank + a.desc.world - 1) / a.desc.world
@@ -871,7 +1054,18 @@ nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw
     Counters* dc = nullptr;
     NRT_CUDA(cudaMallocAsync(&dc, sizeof(Counters), st));
     Wave W{};
-    NRT_TRY(alloc_wave(W, n_shard, st));
+    WaveGuard wg{&W, st};
+    NRT_TRY(alloc_wave(W, n_shard < kBatch ? n_shard : kBatch, s->device, st));
+    if (getenv("NRT_PHASES")) {
+        cudaStreamSynchronize(st);
+        cudaMemPool_t pool;
+        size_t res = 0, used = 0;
+        cudaDeviceGetDefaultMemPool(&pool, s->device);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        fprintf(stderr, "[nrt] wave alloc %.3f ms (pool reserved %.2f GB used %.2f GB)\n",
+                host_ms_since(t_start), res / 1e9, used / 1e9);
+    }
     W.n_alive = dc->n_alive;
     W.ctr = dc->ctr;
     nrt_coarse_rec* raw = nullptr;
@@ -889,38 +1083,23 @@ nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw
         P.ev_n = &dc->ev_n;
         P.bounces = &dc->bounces;
         P.counters = &dc->tests;
-        if (n_shard > 0) {
-            unsigned gb = (unsigned)((n_shard + 255) / 256);
+        // primary rays in batches of kBatch (bounded wavefront state: 290 B per ray in flight);
+        // records, events and counters accumulate across batches
+        stats->ms_kernel = 0.0f;
+        for (uint64_t j0 = 0; j0 < n_shard; j0 += kBatch) {
+            const uint64_t nb = n_shard - j0 < kBatch ? n_shard - j0 : kBatch;
+            NRT_CUDA(cudaMemsetAsync(dc->n_alive, 0, sizeof(dc->n_alive) + sizeof(dc->ctr), st));
+            unsigned gb = (unsigned)((nb + 255) / 256);
             if (gb > (unsigned)sm_count(s->device) * 16) gb = (unsigned)sm_count(s->device) * 16;
-            k_gen_primary<<<gb, 256, 0, st>>>(P, W, n_shard);
+            k_gen_primary<<<gb, 256, 0, st>>>(P, W, nb, j0);
             ::nrt::count_launch();
-            const char* eb = getenv("NRT_SORT_BAND");
-            const uint64_t band = eb ? (uint64_t)atoll(eb) : 0;
-            if (band > 0 && n_shard > 1) {  // coherent processing order (alive list permutation)
-                unsigned long long *k0 = nullptr, *k1 = nullptr;
-                unsigned* v1 = nullptr;
-                NRT_CUDA(cudaMallocAsync(&k0, n_shard * 8, st));
-                NRT_CUDA(cudaMallocAsync(&k1, n_shard * 8, st));
-                NRT_CUDA(cudaMallocAsync(&v1, n_shard * 4, st));
-                k_order_keys<<<gb, 256, 0, st>>>(W.d, n_shard, band, k0, W.alive[1]);
-                ::nrt::count_launch();
-                int bits = 17;
-                while (bits < 64 && ((n_shard / band) >> (bits - 16)) > 0) ++bits;
-                cub::DoubleBuffer<unsigned long long> kb(k0, k1);
-                cub::DoubleBuffer<unsigned> vb(W.alive[1], v1);
-                size_t tbs = 0;
-                void* tmp = nullptr;
-                cub::DeviceRadixSort::SortPairs(nullptr, tbs, kb, vb, (int)n_shard, 0, bits, st);
-                NRT_CUDA(cudaMallocAsync(&tmp, tbs, st));
-                cub::DeviceRadixSort::SortPairs(tmp, tbs, kb, vb, (int)n_shard, 0, bits, st);
-                NRT_CUDA(cudaMemcpyAsync(W.alive[0], vb.Current(), n_shard * 4, cudaMemcpyDeviceToDevice, st));
-                cudaFreeAsync(tmp, st);
-                cudaFreeAsync(k0, st);
-                cudaFreeAsync(k1, st);
-                cudaFreeAsync(v1, st);
+            if (getenv("NRT_PHASES")) {
+                cudaStreamSynchronize(st);
+                fprintf(stderr, "[nrt] gen done %.3f ms\n", host_ms_since(t_start));
             }
-            NRT_TRY(run_bounces(P, W, a.max_refl + 1, s->device, a.desc.counters != 0,
-                                &stats->ms_kernel, st));
+            float ms = 0.0f;
+            NRT_TRY(run_bounces(P, W, a.max_refl + 1, s->device, a.desc.counters != 0, &ms, st));
+            stats->ms_kernel += ms;
         }
         NRT_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, st));
         NRT_CUDA(cudaStreamSynchronize(st));
@@ -942,6 +1121,10 @@ nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw
     }
     free_wave(W, st);
     cudaFreeAsync(dc, st);
+    if (getenv("NRT_PHASES")) {
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "[nrt] primary done %.3f ms\n", host_ms_since(t_start));
+    }
     *raw_out = raw;
     *n_raw = (int64_t)hc.raw_n;
     *ev_out = ev;
@@ -983,7 +1166,8 @@ nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev
     nrt_coarse_rec* raw = nullptr;
     Counters hc{};
     Wave W{};
-    if (total > 0) NRT_TRY(alloc_wave(W, total, st));
+    WaveGuard wg{&W, st};
+    if (total > 0) NRT_TRY(alloc_wave(W, total, s->device, st));
     W.n_alive = dc->n_alive;
     W.ctr = dc->ctr;
     for (int attempt = 0; attempt < 3 && total > 0; ++attempt) {
@@ -1015,7 +1199,7 @@ nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev
         cudaFreeAsync(raw, st);
         raw_cap = hc.raw_n;
     }
-    if (total > 0) free_wave(W, st);
+    free_wave(W, st);
     cudaFreeAsync(dc, st);
     cudaFreeAsync(cnt, st);
     cudaFreeAsync(off, st);

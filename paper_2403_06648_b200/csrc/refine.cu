@@ -39,7 +39,7 @@ namespace {
 #endif
 constexpr int NW = NRT_REFINE_WARPS;      // warps per path
 constexpr int kMaxDim = 3 * NRT_MAX_INT;
-constexpr int kCapS = 512;                // shared-memory candidates per reflection vertex
+constexpr int kCapS = 768;                // shared-memory candidates per reflection vertex
 constexpr double kC = 299792458.0;
 constexpr double kH = 1e-7;               // central-difference step (m)
 
@@ -943,7 +943,9 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
         P.cos_ex = cs;
     }
     P.rq = fmax(4.0 * P.sigma, (double)s->r_max + d->tau);
-    P.rg = P.rq + (getenv("NRT_REFINE_MARGIN") ? atof(getenv("NRT_REFINE_MARGIN")) : fmax(0.05, 2.0 * P.sigma));
+    // gather margin: iterates may drift half of it before a re-gather; 1.5 sigma keeps the
+    // lists of dense clouds (RR: 5e4 /m^2) within kCapS while sparse ones re-gather rarely
+    P.rg = P.rq + (getenv("NRT_REFINE_MARGIN") ? atof(getenv("NRT_REFINE_MARGIN")) : fmax(0.01, 1.5 * P.sigma));
     P.tol = d->tol_m;
     P.alpha = d->alpha;
     P.beta = d->beta;

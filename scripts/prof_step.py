@@ -18,10 +18,14 @@ def main():
     import paper_2403_06648_b200 as N
     cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-    voxel = float(sys.argv[3]) if len(sys.argv) > 3 else None
+    voxel = float(sys.argv[3]) if len(sys.argv) > 3 and float(sys.argv[3]) > 0 else None
     case = G.case(cfg)
     if voxel:
         case.voxel = voxel
+    if len(sys.argv) > 4:
+        case.n_rays = int(float(sys.argv[4]))
+    if os.environ.get("NRT_PROF_NO_REFINE"):
+        globals()["_no_refine"] = True
     s = case.scene
     dev = torch.device("cuda", 0)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
@@ -39,6 +43,11 @@ def main():
         torch.cuda.synchronize()
         t2 = time.perf_counter()
         info = p.info()
+        if globals().get("_no_refine"):
+            out.append({"build_ms": 1e3 * (t1 - t0), "launch_ms": 1e3 * (t2 - t1),
+                        **{k: info[k] for k in ("ms_trace", "ms_fans", "bounces", "n",
+                                                "surfel_tests", "cells_visited")}})
+            continue
         rf = N.nrt_refine_ex(sc, p, xi=case.xi, r_s=case.r_s, tau=case.tau, keep_invalid=1,
                              stream=st)
         torch.cuda.synchronize()

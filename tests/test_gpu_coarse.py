@@ -240,3 +240,29 @@ def test_north_star_four_arg_build(N, O):
     ref, _, nb = O.launch_phased(c, procs=NPROC)
     assert p.info()["bounces"] == nb
     assert_same_records(got, ref, "4-arg build")
+
+
+# ------------------------------------------------------------------ RR room, many RX ----
+@pytest.mark.parametrize("name", ["C4s", "C5s"])
+def test_rr_small_many_rx_bit_exact(N, O, name):
+    """Reconstructed-room-like clouds (clutter, holes, split labels, outliers, plane-fit
+    normals) with 85 / 879 receivers: the receiver grid path must give the brute-force set."""
+    case = G.case(name)
+    assert len(case.rx) > 16
+    got, info, _ = run_gpu(N, case)
+    ref, n_raw, nb = O.launch_phased(case, procs=NPROC)
+    assert info["bounces"] == nb
+    assert info["n_raw"] == n_raw
+    assert_same_records(got, ref, name)
+    assert len(np.unique(got["rx"])) > 5
+
+
+def test_rx_grid_equals_all_pairs(N, monkeypatch):
+    case = G.case("C5s", n_rays=6000)
+    a, _, _ = run_gpu(N, case)
+    monkeypatch.setenv("NRT_RX_GRID_MIN", "1000000")  # force the all-receivers loop
+    b, _, _ = run_gpu(N, case)
+    monkeypatch.setenv("NRT_RX_GRID_MIN", "2")
+    monkeypatch.setenv("NRT_RX_GRID_V", "0.17")       # another cell size
+    c, _, _ = run_gpu(N, case)
+    assert a.tobytes() == b.tobytes() == c.tobytes()
