@@ -38,6 +38,9 @@ namespace {
 #define NRT_REFINE_WARPS 8
 #endif
 constexpr int NW = NRT_REFINE_WARPS;      // warps per path
+#ifndef NRT_MLS_ILP
+#define NRT_MLS_ILP 1
+#endif
 constexpr int kMaxDim = 3 * NRT_MAX_INT;
 constexpr int kCapS = 768;                // shared-memory candidates per reflection vertex
 constexpr double kC = 299792458.0;
@@ -95,16 +98,27 @@ struct Trial {  // one warp's residual evaluation result
 };
 
 struct Smem {
+    Path D;  // the path being refined (one copy per block)
     double J[kMaxDim * kMaxDim];
-    double A[kMaxDim * kMaxDim];
+    union {
+        struct {
+            double A[kMaxDim * kMaxDim];  // normal equations (solve phase)
+            Trial tr[NW];                 // residual evaluations (line search, checks)
+        };
+        double Rpm[2 * kMaxDim * kMaxDim];  // perturbed residuals, row 2j (+h), 2j+1 (-h)
+    };
     double z[kMaxDim], r[kMaxDim], b[kMaxDim];
     double pb[NRT_MAX_INT][3], nb[NRT_MAX_INT][3];
-    Trial tr[NW];
+    double zw[NW][kMaxDim];  // per-warp trial point
+    double I[NRT_MAX_INT + 2][3];
     Vtx V[NRT_MAX_INT];
     int flag[NW];
     double dval;
     unsigned long long q;
 };
+static_assert(sizeof(double) * kMaxDim * kMaxDim + sizeof(Trial) * NW >=
+                  sizeof(double) * 2 * kMaxDim * kMaxDim,
+              "Rpm must not spill past A + tr");
 
 __device__ __forceinline__ double ddot(const double a[3], const double b[3]) {
     return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
@@ -270,9 +284,34 @@ __device__ bool mls(const RP& P, const Path& D, int k, const double x[3], const 
         Nz += w * sg * n2;
     };
     if (use_list) {
-        for (int j = lane; j < V.n; j += 32) {
-            const float* e = list + 6 * j;
-            acc(e[0], e[1], e[2], e[3], e[4], e[5]);
+        // NRT_MLS_ILP candidates per lane and round (1 measured fastest: FP64 issue, not exp
+        // latency, bounds the loop); each lane adds its candidates j = lane, lane + 32, ... in
+        // that order, and a candidate outside 4 sigma adds w = 0 (every sum bitwise unchanged)
+        const int n = V.n;
+        for (int j0 = lane; j0 < n; j0 += 32 * NRT_MLS_ILP) {
+            double wv[NRT_MLS_ILP], sgv[NRT_MLS_ILP];
+            float e[NRT_MLS_ILP][6];
+#pragma unroll
+            for (int u = 0; u < NRT_MLS_ILP; ++u) {
+                const int j = j0 + 32 * u;
+                for (int a = 0; a < 6; ++a) e[u][a] = j < n ? list[6 * j + a] : 0.0f;
+                const double d0 = (double)e[u][0] - x[0], d1 = (double)e[u][1] - x[1], d2 = (double)e[u][2] - x[2];
+                const double dd = (d0 * d0 + d1 * d1) + d2 * d2;
+                const double w = exp(-dd * inv2s2);
+                wv[u] = (j < n && dd <= r2) ? w : 0.0;
+                sgv[u] = (((double)e[u][3] * ns[0] + (double)e[u][4] * ns[1]) + (double)e[u][5] * ns[2]) < 0.0 ? -1.0 : 1.0;
+            }
+#pragma unroll
+            for (int u = 0; u < NRT_MLS_ILP; ++u) {
+                const double w = wv[u], sg = sgv[u];
+                W += w;
+                Px += w * (double)e[u][0];
+                Py += w * (double)e[u][1];
+                Pz += w * (double)e[u][2];
+                Nx += w * sg * (double)e[u][3];
+                Ny += w * sg * (double)e[u][4];
+                Nz += w * sg * (double)e[u][5];
+            }
         }
     } else {
         const int32_t label = D.label[k];
@@ -480,7 +519,10 @@ __device__ bool supported(const RP& P, int32_t label, const double x[3], int lan
     return __any_sync(0xffffffffu, s);
 }
 
-__global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
+#ifndef NRT_REFINE_MINB
+#define NRT_REFINE_MINB 3
+#endif
+__global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
     extern __shared__ __align__(16) unsigned char dyn[];
     Smem& S = *reinterpret_cast<Smem*>(dyn);
     float* cand = reinterpret_cast<float*>(dyn + ((sizeof(Smem) + 15) & ~size_t(15)));
@@ -500,37 +542,41 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
         const int64_t jq = n_mine - 1 - (int64_t)q;
         const int64_t pi = P.rank + jq * P.world;
         const nrt_coarse_rec& c = P.in[pi];
-        // ---- the path and its unknowns at the coarse seed (every thread holds D)
-        Path D;
-        D.n = c.n_int;
-        int m = 0, nslot = 0;
-        for (int a = 0; a < 3; ++a) D.rxp[a] = (double)P.rx[3 * (size_t)c.rx + a];
-        for (int k = 0; k < D.n; ++k) {
-            D.kind[k] = (c.kinds >> k) & 1u;
-            D.label[k] = c.label[k];
-            D.prim[k] = c.prim[k];
-            D.col[k] = m;
-            D.slot[k] = -1;
-            if (D.kind[k] == 0) {
-                const float4 nv = __ldg(&P.sn[c.prim[k]]);
-                D.nseed[k][0] = nv.x;
-                D.nseed[k][1] = nv.y;
-                D.nseed[k][2] = nv.z;
-                D.slot[k] = nslot++;
-                m += 3;
-            } else {
-                const DevEdge& E = P.edges[c.prim[k]];
-                const double ev[3] = {(double)E.b_[0] - E.a[0], (double)E.b_[1] - E.a[1], (double)E.b_[2] - E.a[2]};
-                const double l = sqrt(ddot(ev, ev));
-                for (int a = 0; a < 3; ++a) {
-                    D.ea[k][a] = E.a[a];
-                    D.ee[k][a] = ev[a] / l;
+        // ---- the path and its unknowns at the coarse seed (shared, built by thread 0)
+        Path& D = S.D;
+        if (tid == 0) {
+            D.n = c.n_int;
+            int m0 = 0, nslot = 0;
+            for (int a = 0; a < 3; ++a) D.rxp[a] = (double)P.rx[3 * (size_t)c.rx + a];
+            for (int k = 0; k < D.n; ++k) {
+                D.kind[k] = (c.kinds >> k) & 1u;
+                D.label[k] = c.label[k];
+                D.prim[k] = c.prim[k];
+                D.col[k] = m0;
+                D.slot[k] = -1;
+                if (D.kind[k] == 0) {
+                    const float4 nv = __ldg(&P.sn[c.prim[k]]);
+                    D.nseed[k][0] = nv.x;
+                    D.nseed[k][1] = nv.y;
+                    D.nseed[k][2] = nv.z;
+                    D.slot[k] = nslot++;
+                    m0 += 3;
+                } else {
+                    const DevEdge& E = P.edges[c.prim[k]];
+                    const double ev[3] = {(double)E.b_[0] - E.a[0], (double)E.b_[1] - E.a[1], (double)E.b_[2] - E.a[2]};
+                    const double l = sqrt(ddot(ev, ev));
+                    for (int a = 0; a < 3; ++a) {
+                        D.ea[k][a] = E.a[a];
+                        D.ee[k][a] = ev[a] / l;
+                    }
+                    D.elen[k] = l;
+                    m0 += 1;
                 }
-                D.elen[k] = l;
-                m += 1;
             }
+            D.dim = m0;
         }
-        D.dim = m;
+        __syncthreads();
+        const int m = D.dim;
         if (tid == 0)
             for (int k = 0; k < D.n; ++k) {
                 if (D.kind[k] == 0) {
@@ -593,46 +639,41 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
                         }
                     }
                     phase(8);
-                    // ---- Jacobian: column j on warp j mod NW (only vertex k's MLS moves)
+                    // ---- Jacobian: the 2m perturbed residuals (task t = 2j + sign) spread over
+                    // the warps (only vertex k's MLS moves), then J = (r+ - r-) / 2h by the block
                     if (tid < NW) S.flag[tid] = 1;
                     __syncthreads();
-                    for (int j = wid; j < m; j += NW) {
+                    for (int t = wid; t < 2 * m; t += NW) {
+                        const int j = t >> 1, sgn = t & 1;
                         int k = 0;
                         while (k + 1 < D.n && D.col[k + 1] <= j) ++k;
-                        Trial& T = S.tr[wid];
+                        double* zz = S.zw[wid];
+                        if (lane < m) zz[lane] = S.z[lane];
+                        __syncwarp();
+                        if (lane == 0) zz[j] = sgn == 0 ? S.z[j] + kH : S.z[j] - kH;
+                        __syncwarp();
                         bool okj = true;
-                        for (int sgn = 0; sgn < 2 && okj; ++sgn) {
-                            double zz[kMaxDim];
-                            for (int i = 0; i < m; ++i) zz[i] = S.z[i];
-                            zz[j] = sgn == 0 ? S.z[j] + kH : S.z[j] - kH;
-                            double pbk[3] = {0, 0, 0}, nbk[3] = {0, 0, 0};
-                            if (D.kind[k] == 0) {
-                                double x[3];
-                                vpoint(P, D, zz, k, x);
-                                okj = mls(P, D, k, x, cand_ptr(cand, D.slot[k]), S.V[D.slot[k]], pbk, nbk, lane);
-                            }
-                            // only vertices k-1, k, k+1 see unknown j; the rest keep r(z)
-                            double* rr = sgn == 0 ? T.r : T.pb[0];  // T.pb as scratch (24 doubles)
-                            bool okv = true;
-                            if (okj && lane < D.n) {
-                                const int q2 = lane;
-                                if (q2 >= k - 1 && q2 <= k + 1) {
-                                    const bool mine = q2 == k && D.kind[k] == 0;
-                                    okv = vertex_residual(P, D, zz, q2, mine ? pbk : S.pb[q2], mine ? nbk : S.nb[q2], rr);
-                                } else {
-                                    const int c0 = D.col[q2], c1 = q2 + 1 < D.n ? D.col[q2 + 1] : m;
-                                    for (int i = c0; i < c1; ++i) rr[i] = S.r[i];
-                                }
-                            }
-                            okj = okj && __all_sync(0xffffffffu, okv);
-                            __syncwarp();
+                        double pbk[3] = {0, 0, 0}, nbk[3] = {0, 0, 0};
+                        if (D.kind[k] == 0) {
+                            double x[3];
+                            vpoint(P, D, zz, k, x);
+                            okj = mls(P, D, k, x, cand_ptr(cand, D.slot[k]), S.V[D.slot[k]], pbk, nbk, lane);
                         }
-                        if (lane == 0) {
-                            if (okj)
-                                for (int i = 0; i < m; ++i) S.J[i * m + j] = (T.r[i] - (&T.pb[0][0])[i]) / (2.0 * kH);
-                            else
-                                S.flag[wid] = 0;
+                        // only vertices k-1, k, k+1 see unknown j; the rest keep r(z)
+                        double* rr = S.Rpm + t * kMaxDim;
+                        bool okv = true;
+                        if (okj && lane < D.n) {
+                            const int q2 = lane;
+                            if (q2 >= k - 1 && q2 <= k + 1) {
+                                const bool mine = q2 == k && D.kind[k] == 0;
+                                okv = vertex_residual(P, D, zz, q2, mine ? pbk : S.pb[q2], mine ? nbk : S.nb[q2], rr);
+                            } else {
+                                const int c0 = D.col[q2], c1 = q2 + 1 < D.n ? D.col[q2 + 1] : m;
+                                for (int i = c0; i < c1; ++i) rr[i] = S.r[i];
+                            }
                         }
+                        okj = okj && __all_sync(0xffffffffu, okv);
+                        if (!okj && lane == 0) S.flag[wid] = 0;
                         __syncwarp();
                     }
                     __syncthreads();
@@ -642,6 +683,11 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
                         status = NRT_REF_NO_SUPPORT;
                         break;
                     }
+                    for (int e = tid; e < m * m; e += blockDim.x) {
+                        const int i = e / m, j = e % m;
+                        S.J[i * m + j] = (S.Rpm[(2 * j) * kMaxDim + i] - S.Rpm[(2 * j + 1) * kMaxDim + i]) / (2.0 * kH);
+                    }
+                    __syncthreads();
                     phase(9);
                     // ---- normal equations (whole block) + Cholesky solve (warp 0), m <= 24
                     for (int e = tid; e < m * m + m; e += blockDim.x) {
@@ -709,11 +755,11 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
                     }
                     if (dmax < P.tol) {  // converged: take the (tiny) full step
                         if (wid == 0) {
-                            double zt[kMaxDim];
-                            for (int i = 0; i < m; ++i) zt[i] = S.z[i] + S.b[i];
+                            double* zt = S.zw[0];
+                            if (lane < m) zt[lane] = S.z[lane] + S.b[lane];
+                            __syncwarp();
                             residual_all(P, D, zt, cand, S.V, S.tr[0], lane);
-                            if (S.tr[0].ok && lane == 0)
-                                for (int i = 0; i < m; ++i) S.z[i] = zt[i];
+                            if (S.tr[0].ok && lane < m) S.z[lane] = zt[lane];
                         }
                         status = NRT_REF_OK;
                         __syncthreads();
@@ -733,8 +779,9 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
                         for (int e = 0; e < round * NW + wid; ++e) gam *= P.beta;
                         const bool live = gam > 1e-12;
                         if (live) {
-                            double zt[kMaxDim];
-                            for (int i = 0; i < m; ++i) zt[i] = S.z[i] + gam * S.b[i];
+                            double* zt = S.zw[wid];
+                            if (lane < m) zt[lane] = S.z[lane] + gam * S.b[lane];
+                            __syncwarp();
                             residual_all(P, D, zt, cand, S.V, S.tr[wid], lane);
                             if (lane == 0)
                                 S.flag[wid] = S.tr[wid].ok && S.tr[wid].f <= (1.0 - 2.0 * P.alpha * gam) * f0;
@@ -755,18 +802,15 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
                             }
                         }
                         if (first >= 0) {
-                            if (tid == 0) {
+                            if (tid < m) {
                                 double gm = 1.0;
                                 for (int e = 0; e < round * NW + first; ++e) gm *= P.beta;
-                                for (int i = 0; i < m; ++i) {
-                                    S.z[i] = S.z[i] + gm * S.b[i];
-                                    S.r[i] = S.tr[first].r[i];
-                                }
-                                for (int k = 0; k < D.n; ++k)
-                                    for (int a = 0; a < 3; ++a) {
-                                        S.pb[k][a] = S.tr[first].pb[k][a];
-                                        S.nb[k][a] = S.tr[first].nb[k][a];
-                                    }
+                                S.z[tid] = S.z[tid] + gm * S.b[tid];
+                                S.r[tid] = S.tr[first].r[tid];
+                            } else if (tid >= 32 && tid < 32 + 3 * D.n) {
+                                const int k = (tid - 32) / 3, a = (tid - 32) % 3;
+                                S.pb[k][a] = S.tr[first].pb[k][a];
+                                S.nb[k][a] = S.tr[first].nb[k][a];
                             }
                             accepted = first;
                         } else if (exhausted) {
@@ -786,8 +830,9 @@ __global__ void __launch_bounds__(32 * NW) k_refine(RP P) {
         __syncthreads();
         // ---- final residual, gradient norm, validity (warp 0)
         if (wid == 0) {
-            double I[NRT_MAX_INT + 2][3];
-            for (int k = -1; k <= D.n; ++k) vpoint(P, D, S.z, k, I[k + 1]);
+            double (*I)[3] = S.I;
+            if (lane <= D.n + 1) vpoint(P, D, S.z, lane - 1, I[lane]);
+            __syncwarp();
             double gsq = 0, rmax = 0;
             Trial& T = S.tr[0];
             if (status == NRT_REF_OK && m > 0) {
@@ -961,6 +1006,7 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     P.nv_max = nv;
     const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) + (size_t)nv * kCapS * 6 * sizeof(float);
     NRT_CUDA(cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NRT_CUDA(cudaFuncSetAttribute(k_refine, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     const int64_t n_mine = n > d->rank ? (n - d->rank + d->world - 1) / d->world : 0;
     float* d_rx = nullptr;
     const size_t nrx = coarse->rx.size();
