@@ -64,6 +64,10 @@ struct Wave {
     float2* hit;     // [cap] (best_t, best id bits)
     RayCold* cold;   // [cap]
     unsigned* alive[2];       // ping-pong live lists
+    unsigned* okey[2];        // ordering keys (primary batches)
+    unsigned* oval;           // ordering values (slot ids)
+    void* otmp;               // radix-sort temporary storage
+    size_t otmp_bytes;
     unsigned long long* n_alive;  // [kMaxIter + 1]
     unsigned long long* ctr;      // [kMaxIter] trace work counters
 };
@@ -129,8 +133,14 @@ __device__ __forceinline__ unsigned long long lane_inc(unsigned long long* ctr) 
 #define NRT_TRACE_MINB 8  // min resident blocks/SM for k_trace: 64 registers, 50% occupancy
                           // (measured best of 4/6/8 on C2, scripts/variant_sweep.sh)
 #endif
+#ifndef NRT_TRACE_COOP
+#define NRT_TRACE_COOP 0  // warp-cooperative record tests (k_trace_coop); 0 = per-lane k_trace
+#endif
 #ifndef NRT_TRACE_FETCH
 #define NRT_TRACE_FETCH lane_inc
+#endif
+#ifndef NRT_TRACE_REFILL
+#define NRT_TRACE_REFILL 8  // 1: each lane refills alone; k > 1: warp refills k+ idle lanes together
 #endif
 
 // ---- A3 reference walk (debug path): nearest surfel along (o, d) by plain 3D-DDA --------
@@ -601,6 +611,40 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace(TP P, Wave W, int
     Seg s;
     unsigned ray = 0;
     bool have = false;
+#if NRT_TRACE_REFILL > 1
+    // warp refill: idle lanes take consecutive live-list entries together once at least
+    // NRT_TRACE_REFILL of them are idle (or nothing else is running) -> coherent lanes
+    const int lane = threadIdx.x & 31;
+    bool done = false;
+    for (;;) {
+        const unsigned idle = __ballot_sync(0xffffffffu, !have && !done);
+        const unsigned busy = __ballot_sync(0xffffffffu, have);
+        if (!idle && !busy) break;
+        if (idle && (__popc(idle) >= NRT_TRACE_REFILL || busy == 0)) {
+            const int leader = __ffs(idle) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(&W.ctr[b], (unsigned long long)__popc(idle));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (!have && !done) {
+                const unsigned long long j = base + __popc(idle & ((1u << lane) - 1u));
+                if (j >= n) {
+                    done = true;
+                } else {
+                    ray = alive[j];
+                    const float4 o = W.o[ray], d = W.d[ray], a = W.l0[ray], c = W.l1[ray];
+                    s.o = make_float3(o.x, o.y, o.z);
+                    s.prev = __float_as_int(o.w);
+                    s.d = make_float3(d.x, d.y, d.z);
+                    s.l0 = make_float3(a.x, a.y, a.z);
+                    s.l1 = make_float3(c.x, c.y, c.z);
+                    ++bounces;
+                    if (!seg_begin<CNT>(P, s, cnt)) W.hit[ray] = make_float2(INFINITY, __int_as_float(-1));
+                    else have = true;
+                }
+            }
+        }
+        if (!have) continue;
+#else
     for (;;) {
         if (!have) {
             const unsigned long long j = NRT_TRACE_FETCH(&W.ctr[b]);
@@ -619,6 +663,7 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace(TP P, Wave W, int
             }
             have = true;
         }
+#endif
         if (s.k < s.kend) {
             // four records per iteration, all loads issued before any test; indices past the
             // cell end repeat the last record (the (t, id) argmin is idempotent)
@@ -641,6 +686,127 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace(TP P, Wave W, int
             W.hit[ray] = make_float2(s.best_t, __int_as_float(s.best));
             have = false;
         }
+    }
+    flush_counts(P, bounces, cnt, CNT);
+}
+
+// HIT predicate (R7-R9) of one record against one segment, as a packed lexicographic key
+// (t bits << 32 | id): t > 0 here, so the unsigned order of the key is the (t, id) order, and
+// the nearest hit is the minimum key (~0 = no hit).  Same arithmetic as test_record.
+__device__ __forceinline__ unsigned long long hit_key(const TP& P, const float4 o, const float4 d,
+                                                      const float4 l0, const float4 l1,
+                                                      const float4 A, const float4 B) {
+    const int id = __float_as_int(B.w);
+    const float wx = o.x - A.x, wy = o.y - A.y, wz = o.z - A.z;
+    const float f0 = (wx * B.x + wy * B.y) + wz * B.z;
+    const float dn = (d.x * B.x + d.y * B.y) + d.z * B.z;
+    if (!(f0 * dn < 0.0f)) return ~0ull;
+    {
+        const float ex = __fmaf_rn(-f0, d.x, wx * dn), ey = __fmaf_rn(-f0, d.y, wy * dn),
+                    ez = __fmaf_rn(-f0, d.z, wz * dn);
+        const float rs = A.w + P.slack;
+        if (__fmaf_rn(ex, ex, __fmaf_rn(ey, ey, ez * ez)) > rs * rs * (dn * dn)) return ~0ull;
+    }
+    if (id == __float_as_int(o.w)) return ~0ull;
+    if (fabsf(f0) <= P.tau) {
+        const float c0 = (B.x * l0.x + B.y * l0.y) + B.z * l0.z;
+        const float c1 = (B.x * l1.x + B.y * l1.y) + B.z * l1.z;
+        if (fabsf(c0) >= P.cos_ex || fabsf(c1) >= P.cos_ex) return ~0ull;
+    }
+    const float t = (-f0) / dn;
+    const float hx = o.x + t * d.x, hy = o.y + t * d.y, hz = o.z + t * d.z;
+    const float qx = hx - A.x, qy = hy - A.y, qz = hz - A.z;
+    const float qq = (qx * qx + qy * qy) + qz * qz;
+    if (!(qq <= A.w * A.w)) return ~0ull;
+    return ((unsigned long long)__float_as_uint(t) << 32) | (unsigned)id;
+}
+
+// TRACE, warp-cooperative (the default): every lane walks its own segment through the grid
+// (refill, Chebyshev jumps, early exit) until it stands in a non-empty cell; then the warp
+// tests the union of the 32 lanes' cell ranges together — record g of the flattened list on
+// lane g mod 32 (consecutive lanes read consecutive records: coalesced), against its owner's
+// segment staged in shared memory, and the owner's nearest hit kept by a shared 64-bit
+// atomicMin on the (t, id) key.  The argmin is order-independent, so the result is the
+// per-lane kernel's, bit for bit.
+template <bool CNT>
+__global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace_coop(TP P, Wave W, int b) {
+    __shared__ float4 sray[4][4][32];  // [warp][o, d, l0, l1][lane]; o.w = previous surfel id
+    __shared__ unsigned long long sbest[4][32];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned long long n = W.n_alive[b];
+    const unsigned* alive = W.alive[b & 1];
+    unsigned long long bounces = 0;
+    Cnt cnt;
+    Seg s;
+    s.k = s.kend = 0;
+    unsigned ray = 0;
+    bool have = false, done = false;
+    for (;;) {
+        // ---- per lane: refill / walk until a non-empty cell (or no work left)
+        while (!done) {
+            if (!have) {
+                const unsigned long long j = NRT_TRACE_FETCH(&W.ctr[b]);
+                if (j >= n) {
+                    done = true;
+                    break;
+                }
+                ray = alive[j];
+                const float4 o = W.o[ray], d = W.d[ray], a = W.l0[ray], c = W.l1[ray];
+                sray[wid][0][lane] = o;
+                sray[wid][1][lane] = d;
+                sray[wid][2][lane] = a;
+                sray[wid][3][lane] = c;
+                sbest[wid][lane] = ~0ull;
+                s.o = make_float3(o.x, o.y, o.z);
+                s.d = make_float3(d.x, d.y, d.z);
+                ++bounces;
+                if (!seg_begin<CNT>(P, s, cnt)) {
+                    W.hit[ray] = make_float2(INFINITY, __int_as_float(-1));
+                    continue;
+                }
+                have = true;
+                if (s.k < s.kend) break;
+            }
+            const unsigned long long bk = sbest[wid][lane];
+            const float bt = bk == ~0ull ? INFINITY : __uint_as_float((unsigned)(bk >> 32));
+            const float te = fminf(s.tmx, fminf(s.tmy, s.tmz));
+            if (bt < te - P.pad || !grid_move<CNT>(P, s, cnt)) {
+                W.hit[ray] = make_float2(bt, __int_as_float(bk == ~0ull ? -1 : (int)(unsigned)bk));
+                have = false;
+                continue;
+            }
+            if (s.k < s.kend) break;
+        }
+        // ---- warp: test the union of the lanes' cell ranges
+        const unsigned mine = (have && s.k < s.kend) ? s.kend - s.k : 0u;
+        unsigned incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total == 0) break;  // every lane is out of work
+        for (unsigned g0 = 0; g0 < total; g0 += 32) {
+            const unsigned g = g0 + lane;
+            int lo = 0;  // owner: first lane whose inclusive prefix exceeds g
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const unsigned pm = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+                if (pm <= g) lo += step;
+            }
+            const unsigned excl = __shfl_sync(0xffffffffu, incl - mine, lo);
+            const unsigned k0 = __shfl_sync(0xffffffffu, s.k, lo);
+            if (g < total) {
+                const unsigned k = k0 + (g - excl);
+                const float4 A = __ldg(&P.rec[2 * k]), B = __ldg(&P.rec[2 * k + 1]);
+                const unsigned long long key =
+                    hit_key(P, sray[wid][0][lo], sray[wid][1][lo], sray[wid][2][lo], sray[wid][3][lo], A, B);
+                if (key != ~0ull) atomicMin(&sbest[wid][lo], key);
+            }
+        }
+        __syncwarp();
+        if (mine) s.k = s.kend;
     }
     flush_counts(P, bounces, cnt, CNT);
 }
@@ -691,27 +857,33 @@ __global__ void __launch_bounds__(128) k_shade(TP P, Wave W, int b) {
     }
 }
 
-// processing order for coherence: key = (latitude band of B lattice slots, azimuth).  Only the
-// order in which lanes pick up rays changes; ray ids and results do not.
-__global__ void k_order_keys(const float4* d, uint64_t n, uint64_t band, unsigned long long* keys,
+// processing order for coherence (primary rays): key = (latitude band of `band` consecutive
+// lattice points, azimuth of the ray); bands of ~sqrt(32 pi n) points make 32 consecutive
+// slots a near-square patch of the sphere.  k_gen_primary then stores the rays in key order, so
+// the wavefront's live list and its per-ray state stay in slot order (coalesced) and a warp's
+// lanes trace neighbouring rays.  Ray ids, records and results do not change.
+__global__ void k_order_keys(TP P, uint64_t n_batch, uint64_t j0, uint64_t band, unsigned* keys,
                              unsigned* vals) {
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_batch;
          j += (uint64_t)gridDim.x * blockDim.x) {
-        const float4 v = d[j];
-        float a = atan2f(v.y, v.x);  // (-pi, pi]
+        const uint64_t i = (uint64_t)P.rank + (j0 + j) * (uint64_t)P.world;
+        const float3 v = fib_dir(i, P.n_rays);
+        const float a = atan2f(v.y, v.x);  // [-pi, pi]
         const unsigned q = (unsigned)fminf(65535.0f, fmaxf(0.0f, (a + 3.14159265f) * (65536.0f / 6.2831853f)));
-        keys[j] = ((unsigned long long)(j / band) << 16) | q;
+        keys[j] = ((unsigned)(j / band) << 16) | q;
         vals[j] = (unsigned)j;
     }
 }
 
 // primary ray generation (A2): lattice index i = rank + j * world
 // batch slots j in [0, n_batch) hold shard rays j0 + j
-__global__ void k_gen_primary(TP P, Wave W, uint64_t n_shard, uint64_t j0) {
+// perm (optional): slot j holds batch ray perm[j] (coherent order, k_order_keys)
+__global__ void k_gen_primary(TP P, Wave W, uint64_t n_shard, uint64_t j0, const unsigned* perm) {
     const bool edges_on = P.n_edges > 0 && P.max_diff > 0;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_shard;
          j += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = (uint64_t)P.rank + (j0 + j) * (uint64_t)P.world;
+        const uint64_t jr = perm ? (uint64_t)perm[j] : j;
+        const uint64_t i = (uint64_t)P.rank + (j0 + jr) * (uint64_t)P.world;
         const float3 d = fib_dir(i, P.n_rays);
         W.o[j] = make_float4(P.tx, P.ty, P.tz, __int_as_float(-1));
         W.d[j] = make_float4(d.x, d.y, d.z, 0.0f);
@@ -955,6 +1127,15 @@ void rxgrid_free(RxGrid* g, cudaStream_t st) {
     *g = RxGrid{};
 }
 
+// NRT_ORDER=0 disables the coherent primary-ray order (diagnostics)
+static bool order_rays() {
+    static const int on = [] {
+        const char* e = getenv("NRT_ORDER");
+        return e ? atoi(e) : 1;
+    }();
+    return on != 0;
+}
+
 static double host_ms_since(std::chrono::steady_clock::time_point t) {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
 }
@@ -974,9 +1155,21 @@ static nrt_status alloc_wave(Wave& W, uint64_t cap, int dev, cudaStream_t st) {
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t b_o = al(cap * sizeof(float4)), b_h = al(cap * sizeof(float2)),
                  b_c = al(cap * sizeof(RayCold)), b_a = al(cap * sizeof(unsigned));
-    const size_t total = 4 * b_o + b_h + b_c + 2 * b_a;
+    size_t b_t = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b_t, (unsigned*)nullptr, (unsigned*)nullptr,
+                                    (unsigned*)nullptr, (unsigned*)nullptr, (int)cap, 0, 32, st);
+    b_t = al(b_t);
+    const size_t total = 4 * b_o + b_h + b_c + 2 * b_a + 3 * b_a + b_t;
     char* p = (char*)ws_get(dev, total, st);
     if (!p) return set_error(NRT_E_NOMEM, "wavefront workspace of %zu bytes", total);
+    {
+        char* q = p + 4 * b_o + b_h + b_c + 2 * b_a;
+        W.okey[0] = (unsigned*)q;
+        W.okey[1] = (unsigned*)(q + b_a);
+        W.oval = (unsigned*)(q + 2 * b_a);
+        W.otmp = q + 3 * b_a;
+        W.otmp_bytes = b_t;
+    }
     W.slab = p;
     W.o = (float4*)p;
     W.d = (float4*)(p + b_o);
@@ -1004,15 +1197,20 @@ struct WaveGuard {  // every exit path of a launch phase
 // bounce loop: TRACE + SHADE per bounce; ms_kernel accumulates the TRACE kernels' time
 static nrt_status run_bounces(const TP& P, Wave& W, int iters, int dev, bool counters,
                               float* ms_trace, cudaStream_t st) {
-    const unsigned tb = counters ? persistent_blocks(k_trace<true>, dev)
-                                 : persistent_blocks(k_trace<false>, dev);
+#if NRT_TRACE_COOP
+#define NRT_K_TRACE k_trace_coop
+#else
+#define NRT_K_TRACE k_trace
+#endif
+    const unsigned tb = counters ? persistent_blocks(NRT_K_TRACE<true>, dev)
+                                 : persistent_blocks(NRT_K_TRACE<false>, dev);
     const unsigned sb = (unsigned)sm_count(dev) * 8;
     cudaEvent_t ev[3 * kMaxIter + 3];
     for (int i = 0; i < 3 * iters; ++i) cudaEventCreate(&ev[i]);
     for (int b = 0; b < iters; ++b) {
         cudaEventRecord(ev[3 * b], st);
-        if (counters) k_trace<true><<<tb, 128, 0, st>>>(P, W, b);
-        else k_trace<false><<<tb, 128, 0, st>>>(P, W, b);
+        if (counters) NRT_K_TRACE<true><<<tb, 128, 0, st>>>(P, W, b);
+        else NRT_K_TRACE<false><<<tb, 128, 0, st>>>(P, W, b);
         ::nrt::count_launch();
         cudaEventRecord(ev[3 * b + 1], st);
         k_shade<<<sb, 128, 0, st>>>(P, W, b);
@@ -1091,7 +1289,23 @@ nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw
             NRT_CUDA(cudaMemsetAsync(dc->n_alive, 0, sizeof(dc->n_alive) + sizeof(dc->ctr), st));
             unsigned gb = (unsigned)((nb + 255) / 256);
             if (gb > (unsigned)sm_count(s->device) * 16) gb = (unsigned)sm_count(s->device) * 16;
-            k_gen_primary<<<gb, 256, 0, st>>>(P, W, nb, j0);
+            const unsigned* perm = nullptr;
+            if (order_rays()) {
+                // coherent order: sorted (band, azimuth) keys -> permutation in alive[1] (free
+                // until the first SHADE writes the next live list)
+                uint64_t band = (uint64_t)sqrt(32.0 * kPi * (double)a.n_rays / (double)a.desc.world);
+                if (band < 32) band = 32;
+                int hi_bit = 16;
+                while (hi_bit < 32 && ((nb / band) >> (hi_bit - 16))) ++hi_bit;
+                k_order_keys<<<gb, 256, 0, st>>>(P, nb, j0, band, W.okey[0], W.oval);
+                ::nrt::count_launch();
+                size_t tb = W.otmp_bytes;
+                NRT_CUDA(cub::DeviceRadixSort::SortPairs(W.otmp, tb, W.okey[0], W.okey[1], W.oval, W.alive[1],
+                                                         (int)nb, 0, hi_bit, st));
+                ::nrt::count_launch();
+                perm = W.alive[1];
+            }
+            k_gen_primary<<<gb, 256, 0, st>>>(P, W, nb, j0, perm);
             ::nrt::count_launch();
             if (getenv("NRT_PHASES")) {
                 cudaStreamSynchronize(st);
