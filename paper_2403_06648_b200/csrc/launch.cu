@@ -45,6 +45,10 @@ float cRw_of(float c_R, int64_t n_rays) {
 namespace {
 
 constexpr int kMaxIter = NRT_MAX_INT + 1;  // bounce iterations per wavefront launch
+constexpr int kShadeEdges = 1024;  // edge tables up to this size are staged in SHADE's smem
+#ifndef NRT_SHADE_RX
+#define NRT_SHADE_RX 32  // receiver sets up to this size are staged in smem (else receiver grid)
+#endif
 
 // per-ray state that only the shade kernel touches
 struct RayCold {
@@ -97,6 +101,7 @@ struct TP {  // trace parameters (by value into the kernels)
     int rxg_n[3];
     const DevEdge* edges;
     int n_edges;
+    int shade_rx, shade_edges;  // receivers / edge cull spheres staged in SHADE's shared memory
     // outputs
     nrt_coarse_rec* raw;
     unsigned long long raw_cap;
@@ -319,7 +324,70 @@ __device__ void rx_captures(const TP& P, const Hist& h, float3 o, float3 d, floa
     }
 }
 
+// receivers staged in shared memory (x, y, z, index bits): the all-receivers loop of
+// rx_captures with a warp-uniform trip count (lanes stay converged, so each receiver is one
+// broadcast read); `on` masks lanes without a segment.  Same tests, same order.
+__device__ __forceinline__ void rx_captures_staged(const TP& P, const float4* srx, bool on, const Hist& h,
+                                                   float3 o, float3 d, float t_hit, float L, float Ls,
+                                                   float kR, float R0, bool after_diff, uint64_t ray_id) {
+    for (int q = 0; q < P.shade_rx; ++q) {
+        const float4 r = srx[q];
+        if (on) rx_test(P, h, o, d, t_hit, L, Ls, kR, R0, after_diff, ray_id, __float_as_int(r.w), r.x, r.y, r.z);
+        __syncwarp();
+    }
+}
+
 // ---- A6: edge capture -> diffraction events (R13) --------------------------------------
+// the capture test of edge j (R13) after the cull, and the event record
+__device__ __forceinline__ void edge_event(const TP& P, const Hist& h, float3 o, float3 d, float t_hit,
+                                           float L, uint64_t ray_id, int j) {
+    const DevEdge& E = P.edges[j];
+    const float b = (d.x * E.e[0] + d.y * E.e[1]) + d.z * E.e[2];
+    const float w0x = o.x - E.a[0], w0y = o.y - E.a[1], w0z = o.z - E.a[2];
+    const float den = 1.0f - b * b;
+    if (!(den > 1e-12f)) return;
+    const float de = (E.e[0] * w0x + E.e[1] * w0y) + E.e[2] * w0z;
+    const float dd = (d.x * w0x + d.y * w0y) + d.z * w0z;
+    const float te = (b * de - dd) / den;
+    const float s = (de - b * dd) / den;
+    if (!(s >= 0.0f && s <= E.len)) return;
+    if (!(te > 0.0f && te < t_hit + P.b_e)) return;
+    const float pcx = o.x + te * d.x, pcy = o.y + te * d.y, pcz = o.z + te * d.z;
+    const float pex = E.a[0] + s * E.e[0], pey = E.a[1] + s * E.e[1], pez = E.a[2] + s * E.e[2];
+    const float dx = pcx - pex, dy = pcy - pey, dz = pcz - pez;
+    const float dist2 = (dx * dx + dy * dy) + dz * dz;
+    const float R = P.cRw * (L + te);
+    if (!(dist2 <= R * R)) return;
+    unsigned long long slot = agg_inc(P.ev_n);
+    if (slot >= P.ev_cap) return;
+    nrt_event_rec e;
+    e.n_hist = h.n;
+    e.n_diff = h.n_diff;
+    e.kinds = (uint16_t)h.kinds;
+    e.pad_ = 0;
+#pragma unroll
+    for (int k = 0; k < NRT_MAX_INT; ++k) {
+        bool on = k < h.n;
+        e.label[k] = on ? h.label[k] : 0;
+        e.prim[k] = on ? h.prim[k] : 0u;
+        e.v[k][0] = on ? h.v[k][0] : 0.0f;
+        e.v[k][1] = on ? h.v[k][1] : 0.0f;
+        e.v[k][2] = on ? h.v[k][2] : 0.0f;
+    }
+    e.s_edge = h.s_edge;
+    e.edge = (uint32_t)j;
+    e.sbin = (int32_t)floorf(s / P.edge_bin);
+    e.s = s;
+    e.d[0] = d.x;
+    e.d[1] = d.y;
+    e.d[2] = d.z;
+    e.L = L + te;
+    e.dist2 = dist2;
+    e.ray_id = ray_id;
+    P.ev[slot] = e;
+}
+
+// all edges from global memory (edge tables larger than the shared staging)
 __device__ void edge_captures(const TP& P, const Hist& h, float3 o, float3 d, float t_hit,
                               float L, uint64_t ray_id) {
     // conservative cull: a capture needs a ray point at t < t_hit + b_e within
@@ -328,56 +396,31 @@ __device__ void edge_captures(const TP& P, const Hist& h, float3 o, float3 d, fl
     const float Rmax = P.cRw * (L + T) * 1.001f + 1e-4f;
     for (int j = 0; j < P.n_edges; ++j) {
         const DevEdge& E = P.edges[j];
-        {
-            const float cx = E.c[0] - o.x, cy = E.c[1] - o.y, cz = E.c[2] - o.z;
+        const float cx = E.c[0] - o.x, cy = E.c[1] - o.y, cz = E.c[2] - o.z;
+        const float tc = fminf(fmaxf(cx * d.x + cy * d.y + cz * d.z, 0.0f), T);
+        const float ux = cx - tc * d.x, uy = cy - tc * d.y, uz = cz - tc * d.z;
+        const float lim = E.hl + Rmax;
+        if (ux * ux + uy * uy + uz * uz > lim * lim) continue;
+        edge_event(P, h, o, d, t_hit, L, ray_id, j);
+    }
+}
+
+// edges with their cull spheres (c, hl) staged in shared memory; warp-uniform loop as above
+__device__ __forceinline__ void edge_captures_staged(const TP& P, const float4* sed, bool on, const Hist& h,
+                                                     float3 o, float3 d, float t_hit, float L,
+                                                     uint64_t ray_id) {
+    const float T = fminf(t_hit + P.b_e, 1e4f);
+    const float Rmax = P.cRw * (L + T) * 1.001f + 1e-4f;
+    for (int j = 0; j < P.shade_edges; ++j) {
+        const float4 c4 = sed[j];
+        if (on) {
+            const float cx = c4.x - o.x, cy = c4.y - o.y, cz = c4.z - o.z;
             const float tc = fminf(fmaxf(cx * d.x + cy * d.y + cz * d.z, 0.0f), T);
             const float ux = cx - tc * d.x, uy = cy - tc * d.y, uz = cz - tc * d.z;
-            const float lim = E.hl + Rmax;
-            if (ux * ux + uy * uy + uz * uz > lim * lim) continue;
+            const float lim = c4.w + Rmax;
+            if (ux * ux + uy * uy + uz * uz <= lim * lim) edge_event(P, h, o, d, t_hit, L, ray_id, j);
         }
-        const float b = (d.x * E.e[0] + d.y * E.e[1]) + d.z * E.e[2];
-        const float w0x = o.x - E.a[0], w0y = o.y - E.a[1], w0z = o.z - E.a[2];
-        const float den = 1.0f - b * b;
-        if (!(den > 1e-12f)) continue;
-        const float de = (E.e[0] * w0x + E.e[1] * w0y) + E.e[2] * w0z;
-        const float dd = (d.x * w0x + d.y * w0y) + d.z * w0z;
-        const float te = (b * de - dd) / den;
-        const float s = (de - b * dd) / den;
-        if (!(s >= 0.0f && s <= E.len)) continue;
-        if (!(te > 0.0f && te < t_hit + P.b_e)) continue;
-        const float pcx = o.x + te * d.x, pcy = o.y + te * d.y, pcz = o.z + te * d.z;
-        const float pex = E.a[0] + s * E.e[0], pey = E.a[1] + s * E.e[1], pez = E.a[2] + s * E.e[2];
-        const float dx = pcx - pex, dy = pcy - pey, dz = pcz - pez;
-        const float dist2 = (dx * dx + dy * dy) + dz * dz;
-        const float R = P.cRw * (L + te);
-        if (!(dist2 <= R * R)) continue;
-        unsigned long long slot = agg_inc(P.ev_n);
-        if (slot >= P.ev_cap) continue;
-        nrt_event_rec e;
-        e.n_hist = h.n;
-        e.n_diff = h.n_diff;
-        e.kinds = (uint16_t)h.kinds;
-        e.pad_ = 0;
-#pragma unroll
-        for (int k = 0; k < NRT_MAX_INT; ++k) {
-            bool on = k < h.n;
-            e.label[k] = on ? h.label[k] : 0;
-            e.prim[k] = on ? h.prim[k] : 0u;
-            e.v[k][0] = on ? h.v[k][0] : 0.0f;
-            e.v[k][1] = on ? h.v[k][1] : 0.0f;
-            e.v[k][2] = on ? h.v[k][2] : 0.0f;
-        }
-        e.s_edge = h.s_edge;
-        e.edge = (uint32_t)j;
-        e.sbin = (int32_t)floorf(s / P.edge_bin);
-        e.s = s;
-        e.d[0] = d.x;
-        e.d[1] = d.y;
-        e.d[2] = d.z;
-        e.L = L + te;
-        e.dist2 = dist2;
-        e.ray_id = ray_id;
-        P.ev[slot] = e;
+        __syncwarp();
     }
 }
 
@@ -811,26 +854,57 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace_coop(TP P, Wave W
     flush_counts(P, bounces, cnt, CNT);
 }
 
-// SHADE: captures, edge events, reflection; compacts the live list for bounce b+1
+// SHADE: captures, edge events, reflection; compacts the live list for bounce b+1.
+// Receivers (few) and edge cull spheres are staged in shared memory and looped over with a
+// warp-uniform trip count (one broadcast read per receiver/edge for the whole warp).
 __global__ void __launch_bounds__(128) k_shade(TP P, Wave W, int b) {
+    extern __shared__ float4 sh[];
+    float4* srx = sh;
+    float4* sed = sh + P.shade_rx;
+    for (int i = threadIdx.x; i < P.shade_rx; i += blockDim.x)
+        srx[i] = make_float4(P.rx[3 * i], P.rx[3 * i + 1], P.rx[3 * i + 2], __int_as_float(i));
+    for (int i = threadIdx.x; i < P.shade_edges; i += blockDim.x) {
+        const DevEdge& E = P.edges[i];
+        sed[i] = make_float4(E.c[0], E.c[1], E.c[2], E.hl);
+    }
+    __syncthreads();
     const unsigned long long n = W.n_alive[b];
     const unsigned* alive = W.alive[b & 1];
     unsigned* next = W.alive[(b + 1) & 1];
-    for (unsigned long long j = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-         j += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned ray = alive[j];
-        const float4 o4 = W.o[ray], d4 = W.d[ray];
-        const float2 hit = W.hit[ray];
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned long long warps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+    const unsigned long long gw = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (unsigned long long base = gw * 32; base < n; base += warps * 32) {  // warp-uniform
+        const unsigned long long j = base + lane;
+        const bool on = j < n;
+        const unsigned ray = on ? alive[j] : 0u;
+        float4 o4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f), d4 = o4;
+        float2 hit = make_float2(-1.0f, __int_as_float(-1));
+        if (on) {
+            o4 = W.o[ray];
+            d4 = W.d[ray];
+            hit = W.hit[ray];
+        }
         const float3 o = make_float3(o4.x, o4.y, o4.z), d = make_float3(d4.x, d4.y, d4.z);
         const float th = hit.x;
         const int sid = __float_as_int(hit.y);
-        RayCold& c = W.cold[ray];
-        const int flags = c.flags;
-        const float L = c.L, Ls = c.Ls;
-        rx_captures(P, c.h, o, d, th, L, Ls, c.kR, c.R0, (flags & 2) != 0, c.rid);
-        if ((flags & 1) && c.h.n_diff < P.max_diff && c.h.n < NRT_MAX_INT)
-            edge_captures(P, c.h, o, d, th, L, c.rid);
-        if (sid >= 0 && c.seg < c.budget) {
+        RayCold& c = W.cold[on ? ray : 0u];
+        const int flags = on ? c.flags : 0;
+        const float L = on ? c.L : 0.0f, Ls = on ? c.Ls : 0.0f;
+        const float kR = on ? c.kR : 0.0f, R0 = on ? c.R0 : 0.0f;
+        const uint64_t rid = on ? c.rid : 0ull;
+        if (P.rxg_cell) {
+            if (on) rx_captures(P, c.h, o, d, th, L, Ls, kR, R0, (flags & 2) != 0, rid);
+        } else if (__any_sync(0xffffffffu, on)) {
+            rx_captures_staged(P, srx, on, c.h, o, d, th, L, Ls, kR, R0, (flags & 2) != 0, rid);
+        }
+        const bool edges = on && (flags & 1) && c.h.n_diff < P.max_diff && c.h.n < NRT_MAX_INT;
+        if (P.shade_edges > 0 || P.n_edges == 0) {
+            if (__any_sync(0xffffffffu, edges)) edge_captures_staged(P, sed, edges, c.h, o, d, th, L, rid);
+        } else if (edges) {
+            edge_captures(P, c.h, o, d, th, L, rid);
+        }
+        if (on && sid >= 0 && c.seg < c.budget) {
             // A4: reflect at the hit surfel: d' = d - (2 d.n) n, normalised
             const float3 hp = make_float3(o.x + th * d.x, o.y + th * d.y, o.z + th * d.z);
             const float4 nv = __ldg(&P.sn[sid]);
@@ -1023,6 +1097,8 @@ TP make_tp(nrt_scene s, const LaunchArgs& a) {
     P.rxg_v = a.rxg.v;
     P.rxg_inv = a.rxg.v > 0 ? 1.0f / a.rxg.v : 0.0f;
     P.rxg_tmax = a.rxg.tmax;
+    P.shade_rx = a.rxg.cell ? 0 : a.n_rx;
+    P.shade_edges = s->n_edges <= kShadeEdges ? s->n_edges : 0;
     return P;
 }
 
@@ -1051,7 +1127,7 @@ nrt_status rxgrid_build(nrt_scene s, const float* rx, int32_t n_rx, float rreg, 
                         cudaStream_t st) {
     *g = RxGrid{};
     const char* e = getenv("NRT_RX_GRID_MIN");
-    const int min_rx = e ? atoi(e) : 16;
+    const int min_rx = e ? atoi(e) : NRT_SHADE_RX + 1;
     const char* ev = getenv("NRT_RX_GRID_V");
     const float v = ev ? (float)atof(ev) : 0.5f;
     // few receivers, or capture balls larger than the cells: the all-receivers loop is cheaper
@@ -1205,6 +1281,9 @@ static nrt_status run_bounces(const TP& P, Wave& W, int iters, int dev, bool cou
     const unsigned tb = counters ? persistent_blocks(NRT_K_TRACE<true>, dev)
                                  : persistent_blocks(NRT_K_TRACE<false>, dev);
     const unsigned sb = (unsigned)sm_count(dev) * 8;
+    const size_t shade_smem = (size_t)(P.shade_rx + P.shade_edges) * sizeof(float4);
+    if (shade_smem > 48 * 1024)
+        NRT_CUDA(cudaFuncSetAttribute(k_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shade_smem));
     cudaEvent_t ev[3 * kMaxIter + 3];
     for (int i = 0; i < 3 * iters; ++i) cudaEventCreate(&ev[i]);
     for (int b = 0; b < iters; ++b) {
@@ -1213,7 +1292,7 @@ static nrt_status run_bounces(const TP& P, Wave& W, int iters, int dev, bool cou
         else NRT_K_TRACE<false><<<tb, 128, 0, st>>>(P, W, b);
         ::nrt::count_launch();
         cudaEventRecord(ev[3 * b + 1], st);
-        k_shade<<<sb, 128, 0, st>>>(P, W, b);
+        k_shade<<<sb, 128, shade_smem, st>>>(P, W, b);
         ::nrt::count_launch();
         cudaEventRecord(ev[3 * b + 2], st);
     }
