@@ -18,7 +18,10 @@
  * Jacobian: central differences, h = 1e-7 m.  Step D = -(J^T J + lam I)^-1 J^T r,
  * lam = 1e-12 tr(J^T J)/dim.  Backtracking (Eq. 12 in its Armijo form, R24):
  * gamma <- beta*gamma while |r(z + gamma D)|^2 > (1 - 2 alpha gamma) |r(z)|^2.
- * Converged when |D|_inf < tol.  Then validity (R25): on-edge, same side, support,
+ * Converged when |D|_inf < tol.  Stalled (NO_CONVERGE, reading R23b) when the accepted step
+ * moved the iterate by less than tol, |gamma D|_inf < tol, while |D|_inf >= tol: the iterate
+ * is then frozen at a non-root (a residual minimum with r != 0), and every further iteration
+ * repeats the same step.  Then validity (R25): on-edge, same side, support,
  * visibility (FP64 shadow rays with sheet exclusions); delay = L / c (R26); angles (R27).
  */
 #include <math.h>
@@ -347,6 +350,10 @@ static void refine_one(const rctx_t* C, const or_coarse* c, or_refined* out) {
                 gam *= R->beta;
             }
             if (!acc) {
+                status = NRT_OR_NO_CONVERGE;
+                break;
+            }
+            if (gam * dmax < R->tol_m) { /* R23b: stalled at a non-root */
                 status = NRT_OR_NO_CONVERGE;
                 break;
             }

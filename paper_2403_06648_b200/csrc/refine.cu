@@ -7,7 +7,8 @@
 //   diffraction k: r_k = g.e (Eq. 11, I_k = a + t_k e, Eq. 8).
 // reached by damped Gauss-Newton with a central-difference Jacobian (h = 1e-7), step
 // -(J^T J + lam I)^-1 J^T r, Armijo backtracking (Eq. 12 form, R24), converged at |D|_inf <
-// tol.  Then validity (R25): on-edge, same side, support, FP64 visibility; delay = L/c (R26).
+// tol, stalled (NO_CONVERGE, R23b) once an accepted step |gamma D|_inf < tol.  Then validity
+// (R25): on-edge, same side, support, FP64 visibility; delay = L/c (R26).
 //
 // B200 mapping.  Refinement is latency-bound (a few thousand small solves), so
 // one block of NW warps works on one path and spreads the independent pieces of each GN
@@ -113,6 +114,7 @@ struct Smem {
     double I[NRT_MAX_INT + 2][3];
     Vtx V[NRT_MAX_INT];
     int flag[NW];
+    int okv[NRT_MAX_INT];
     double dval;
     unsigned long long q;
 };
@@ -441,6 +443,43 @@ __device__ void residual_all(const RP& P, const Path& D, const double* z, const 
     }
     if (lane == 0) T.ok = ok;
     __syncwarp();
+}
+
+// whole block: the same residual as residual_all, with the MLS of reflection vertex k on warp
+// (k mod NW) — every MLS sum is formed exactly as in residual_all (one warp, same lanes, same
+// order), so T is bitwise the same; the vertex residuals then run on warp 0.  Ends synced.
+__device__ void residual_coop(const RP& P, const Path& D, const double* z, const float* cand,
+                              const Vtx* V, Trial& T, int* okv_s, int wid, int lane) {
+    for (int k = wid; k < D.n; k += NW) {
+        int ok = 1;
+        if (D.kind[k] == 0) {
+            double x[3], pb[3], nb[3];
+            vpoint(P, D, z, k, x);
+            ok = mls(P, D, k, x, cand_ptr(const_cast<float*>(cand), D.slot[k]), V[D.slot[k]], pb, nb, lane);
+            if (ok && lane == 0)
+                for (int a = 0; a < 3; ++a) {
+                    T.pb[k][a] = pb[a];
+                    T.nb[k][a] = nb[a];
+                }
+        }
+        if (lane == 0) okv_s[k] = ok;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        bool ok = true;
+        for (int k = 0; k < D.n; ++k) ok = ok && okv_s[k];
+        bool okv = true;
+        if (ok && lane < D.n) okv = vertex_residual(P, D, z, lane, T.pb[lane], T.nb[lane], T.r);
+        ok = ok && __all_sync(0xffffffffu, okv);
+        __syncwarp();
+        if (ok && lane == 0) {
+            double f = 0;
+            for (int i = 0; i < D.dim; ++i) f += T.r[i] * T.r[i];
+            T.f = f;
+        }
+        if (lane == 0) T.ok = ok;
+    }
+    __syncthreads();
 }
 
 // FP64 occlusion of segment x0 -> x1 (R25 d): one warp walks the grid cells the segment
@@ -773,10 +812,30 @@ __global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
                         return s;
                     }();
                     int accepted = -1;
+                    double gacc = 0.0;  // accepted gamma (block-uniform)
+                    // trial 0 (gamma = 1, accepted in most iterations) by the whole block, the
+                    // vertices' MLS spread over the warps; then rounds of NW trials, warp w
+                    // evaluating gamma = beta^(1 + round NW + w)
+                    if (wid == 0 && lane < m) S.zw[0][lane] = S.z[lane] + 1.0 * S.b[lane];
+                    __syncthreads();
+                    residual_coop(P, D, S.zw[0], cand, S.V, S.tr[0], S.okv, wid, lane);
+                    if (S.tr[0].ok && S.tr[0].f <= (1.0 - 2.0 * P.alpha * 1.0) * f0) {
+                        if (tid < m) {
+                            S.z[tid] = S.zw[0][tid];
+                            S.r[tid] = S.tr[0].r[tid];
+                        } else if (tid >= 32 && tid < 32 + 3 * D.n) {
+                            const int k = (tid - 32) / 3, a = (tid - 32) % 3;
+                            S.pb[k][a] = S.tr[0].pb[k][a];
+                            S.nb[k][a] = S.tr[0].nb[k][a];
+                        }
+                        accepted = 0;
+                        gacc = 1.0;
+                    }
+                    __syncthreads();
                     for (int round = 0; accepted < 0; ++round) {
                         if (P.cycles && tid == 0) atomicAdd(&g_dbg[2], 1ull);
                         double gam = 1.0;
-                        for (int e = 0; e < round * NW + wid; ++e) gam *= P.beta;
+                        for (int e = 0; e < 1 + round * NW + wid; ++e) gam *= P.beta;
                         const bool live = gam > 1e-12;
                         if (live) {
                             double* zt = S.zw[wid];
@@ -802,9 +861,10 @@ __global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
                             }
                         }
                         if (first >= 0) {
+                            double gm = 1.0;  // the sequential loop's gamma, same products
+                            for (int e = 0; e < 1 + round * NW + first; ++e) gm *= P.beta;
+                            gacc = gm;
                             if (tid < m) {
-                                double gm = 1.0;
-                                for (int e = 0; e < round * NW + first; ++e) gm *= P.beta;
                                 S.z[tid] = S.z[tid] + gm * S.b[tid];
                                 S.r[tid] = S.tr[first].r[tid];
                             } else if (tid >= 32 && tid < 32 + 3 * D.n) {
@@ -820,6 +880,10 @@ __global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
                     }
                     phase(11);
                     if (accepted == NW) {
+                        status = NRT_REF_NO_CONVERGE;
+                        break;
+                    }
+                    if (gacc * dmax < P.tol) {  // R23b: stalled at a non-root
                         status = NRT_REF_NO_CONVERGE;
                         break;
                     }
