@@ -115,6 +115,10 @@ struct Smem {
     Vtx V[NRT_MAX_INT];
     int flag[NW];
     int okv[NRT_MAX_INT];
+    int vstat;
+    int vflag[2 * NRT_MAX_INT + 1];  // validity: support failures [0, n), occlusions [n, 2n+1)
+    double nbv[NRT_MAX_INT][3];      // final MLS normals (validity)
+    double gsq, rmax;
     double dval;
     unsigned long long q;
 };
@@ -482,8 +486,14 @@ __device__ void residual_coop(const RP& P, const Path& D, const double* z, const
     __syncthreads();
 }
 
-// FP64 occlusion of segment x0 -> x1 (R25 d): one warp walks the grid cells the segment
-// crosses, lanes split each cell's records, any-hit by ballot
+// FP64 occlusion of segment x0 -> x1 (R25 d), one warp.  The segment's t-range [0, len + pad]
+// is cut into 32 equal pieces and lane j walks the grid cells of piece j by 3D-DDA (so the
+// dependent header loads form 32 short chains instead of one long one); each round, every lane
+// stops at its next non-empty cell and the warp tests the union of those cells' records
+// together (flattened over the lanes, consecutive lanes on consecutive records).  The pieces'
+// cells cover the cells the whole-segment walk visits (a piece starts in the cell holding its
+// first point; boundary rounding is covered by the registration pad), and each
+// record test is the exact per-record predicate, so the any-hit answer is the same.
 __device__ bool occluded(const RP& P, const double x0[3], const double x1[3], const double* lam0,
                          int n0, const double* lam1, int n1, int lane) {
     const double dv[3] = {x1[0] - x0[0], x1[1] - x0[1], x1[2] - x0[2]};
@@ -493,50 +503,98 @@ __device__ bool occluded(const RP& P, const double x0[3], const double x1[3], co
     const float df[3] = {(float)d[0], (float)d[1], (float)d[2]};
     const float g0[3] = {P.ox, P.oy, P.oz};
     const int dims[3] = {P.nx, P.ny, P.nz};
+    const float tend = (float)len + P.pad;
+    const float piece = tend * (1.0f / 32.0f);
+    const float ts = (float)lane * piece, te = lane == 31 ? tend : (float)(lane + 1) * piece;
     int ic[3];
     float tm[3], inv[3];
     for (int a = 0; a < 3; ++a) {
-        ic[a] = min(dims[a] - 1, max(0, (int)floorf((of[a] - g0[a]) * P.inv_v)));
+        const float pa = of[a] + ts * df[a];
+        ic[a] = min(dims[a] - 1, max(0, (int)floorf((pa - g0[a]) * P.inv_v)));
         inv[a] = 1.0f / df[a];
         tm[a] = df[a] != 0.0f ? ((g0[a] + (float)(ic[a] + (df[a] > 0.0f)) * P.v) - of[a]) * inv[a] : INFINITY;
     }
-    const float tend = (float)len + P.pad;
+    bool walking = true;
     for (;;) {
-        const uint2 rg = __ldg(&P.cell[ic[0] + P.nx * (ic[1] + P.ny * ic[2])]);
+        // advance this lane to its next non-empty cell (the cell it stands in first)
+        uint2 rg = make_uint2(0, 0);
+        while (walking) {
+            rg = __ldg(&P.cell[ic[0] + P.nx * (ic[1] + P.ny * ic[2])]);
+            if (rg.y > rg.x) break;
+            int a = 0;
+            if (tm[1] < tm[a]) a = 1;
+            if (tm[2] < tm[a]) a = 2;
+            if (tm[a] > te) {
+                walking = false;
+                break;
+            }
+            ic[a] += df[a] > 0.0f ? 1 : -1;
+            if (ic[a] < 0 || ic[a] >= dims[a]) {
+                walking = false;
+                break;
+            }
+            tm[a] = ((g0[a] + (float)(ic[a] + (df[a] > 0.0f)) * P.v) - of[a]) * inv[a];
+        }
+        const unsigned cnt = walking ? rg.y - rg.x : 0u;
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total == 0) return false;  // no lane has a cell left
         bool hit = false;
-        if (rg.y > rg.x) {
-            for (unsigned k = rg.x + lane; k < rg.y; k += 32) {
+        for (unsigned g0i = 0; g0i < total; g0i += 32) {
+            const unsigned g = g0i + lane;
+            int lo = 0;  // owner lane: first lane whose inclusive prefix exceeds g
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const unsigned pm = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+                if (pm <= g) lo += step;
+            }
+            const unsigned excl = __shfl_sync(0xffffffffu, incl - cnt, lo);
+            const unsigned st = __shfl_sync(0xffffffffu, rg.x, lo);
+            if (g < total) {
+                const unsigned k = st + (g - excl);
                 const float4 A = __ldg(&P.rec[2 * k]);
                 const float4 B = __ldg(&P.rec[2 * k + 1]);
                 const double p[3] = {A.x, A.y, A.z}, n[3] = {B.x, B.y, B.z};
                 const double r = A.w;
                 const double w[3] = {x0[0] - p[0], x0[1] - p[1], x0[2] - p[2]};
                 const double f0 = ddot(w, n), dn = ddot(d, n);
-                if (!(f0 * dn < 0.0)) continue;
-                const double t = -f0 / dn;
-                if (!(t < len)) continue;
-                const double h[3] = {x0[0] + t * d[0] - p[0], x0[1] + t * d[1] - p[1], x0[2] + t * d[2] - p[2]};
-                if (!(ddot(h, h) <= r * r)) continue;
-                bool ex = false;
-                if (fabs(f0) <= P.tau)
-                    for (int q = 0; q < n0; ++q)
-                        if (fabs(ddot(n, lam0 + 3 * q)) >= P.cos_ex) ex = true;
-                const double w1[3] = {x1[0] - p[0], x1[1] - p[1], x1[2] - p[2]};
-                const double f1 = ddot(w1, n);
-                if (!ex && fabs(f1) <= P.tau)
-                    for (int q = 0; q < n1; ++q)
-                        if (fabs(ddot(n, lam1 + 3 * q)) >= P.cos_ex) ex = true;
-                if (!ex) hit = true;
+                if (f0 * dn < 0.0) {
+                    const double t = -f0 / dn;
+                    const double h[3] = {x0[0] + t * d[0] - p[0], x0[1] + t * d[1] - p[1], x0[2] + t * d[2] - p[2]};
+                    if (t < len && ddot(h, h) <= r * r) {
+                        bool ex = false;
+                        if (fabs(f0) <= P.tau)
+                            for (int q = 0; q < n0; ++q)
+                                if (fabs(ddot(n, lam0 + 3 * q)) >= P.cos_ex) ex = true;
+                        const double w1[3] = {x1[0] - p[0], x1[1] - p[1], x1[2] - p[2]};
+                        const double f1 = ddot(w1, n);
+                        if (!ex && fabs(f1) <= P.tau)
+                            for (int q = 0; q < n1; ++q)
+                                if (fabs(ddot(n, lam1 + 3 * q)) >= P.cos_ex) ex = true;
+                        if (!ex) hit = true;
+                    }
+                }
             }
         }
         if (__any_sync(0xffffffffu, hit)) return true;
-        int a = 0;
-        if (tm[1] < tm[a]) a = 1;
-        if (tm[2] < tm[a]) a = 2;
-        if (tm[a] > tend) return false;
-        ic[a] += df[a] > 0.0f ? 1 : -1;
-        if (ic[a] < 0 || ic[a] >= dims[a]) return false;
-        tm[a] = ((g0[a] + (float)(ic[a] + (df[a] > 0.0f)) * P.v) - of[a]) * inv[a];
+        // step past the tested cell
+        if (walking) {
+            int a = 0;
+            if (tm[1] < tm[a]) a = 1;
+            if (tm[2] < tm[a]) a = 2;
+            if (tm[a] > te) {
+                walking = false;
+            } else {
+                ic[a] += df[a] > 0.0f ? 1 : -1;
+                if (ic[a] < 0 || ic[a] >= dims[a]) walking = false;
+                else tm[a] = ((g0[a] + (float)(ic[a] + (df[a] > 0.0f)) * P.v) - of[a]) * inv[a];
+            }
+        }
     }
 }
 
@@ -655,6 +713,7 @@ __global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
                         }
                 }
                 __syncthreads();
+                if (P.cycles && tid == 0) atomicAdd(&g_dbg[6], (unsigned long long)(clock64() - t_start));
                 for (it = 1; it <= P.max_iter; ++it) {
                     long long tph = clock64();
                     auto phase = [&](int slot) {
@@ -749,41 +808,41 @@ __global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
                         const double lam = 1e-12 * tr / m;
                         if (lane < m) S.A[lane * m + lane] += lam;
                         __syncwarp();
+                        // Gauss-Jordan on the SPD system, lane i owning row i: no pivoting is
+                        // needed (the pivots are the squared Cholesky diagonals, so a pivot <= 0
+                        // is exactly the Cholesky failure -> DEGENERATE); each elimination step
+                        // is one division per lane plus independent row updates
                         int solved = 1;
-                        for (int j = 0; j < m; ++j) {
-                            double d = S.A[j * m + j];
-                            for (int k = 0; k < j; ++k) d -= S.A[j * m + k] * S.A[j * m + k];
-                            if (!(d > 0.0)) {
+                        double* Ai = S.A + lane * m;
+                        for (int k = 0; k < m; ++k) {
+                            const double pk = S.A[k * m + k];
+                            if (!(pk > 0.0)) {
                                 solved = 0;
                                 break;
                             }
-                            d = sqrt(d);
-                            // rows below the diagonal in parallel (each reads row j, written before)
-                            double s = 0;
-                            const int i = j + 1 + lane;
-                            if (i < m) {
-                                s = S.A[i * m + j];
-                                for (int k = 0; k < j; ++k) s -= S.A[i * m + k] * S.A[j * m + k];
-                            }
+                            const double* Ak = S.A + k * m;
+                            const double bk = S.b[k];
+                            double fi = 0.0;
+                            if (lane < m && lane != k) fi = Ai[k] / pk;
                             __syncwarp();
-                            if (i < m) S.A[i * m + j] = s / d;
-                            if (lane == 0) S.A[j * m + j] = d;
+                            if (lane < m && lane != k) {
+                                for (int j = k + 1; j < m; ++j) Ai[j] -= fi * Ak[j];
+                                Ai[k] = 0.0;
+                                S.b[lane] -= fi * bk;
+                            }
                             __syncwarp();
                         }
                         double dmax = 0;
-                        if (solved && lane == 0) {
-                            for (int i = 0; i < m; ++i) {
-                                double s = S.b[i];
-                                for (int k = 0; k < i; ++k) s -= S.A[i * m + k] * S.b[k];
-                                S.b[i] = s / S.A[i * m + i];
+                        if (solved) {
+                            double di = 0.0;
+                            if (lane < m) {
+                                di = S.b[lane] / Ai[lane];
+                                S.b[lane] = di;
                             }
-                            for (int i = m - 1; i >= 0; --i) {
-                                double s = S.b[i];
-                                for (int k = i + 1; k < m; ++k) s -= S.A[k * m + i] * S.b[k];
-                                S.b[i] = s / S.A[i * m + i];
-                            }
-                            for (int i = 0; i < m; ++i) dmax = fmax(dmax, fabs(S.b[i]));
+                            dmax = fabs(di);
+                            for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
                         }
+                        __syncwarp();
                         if (lane == 0) S.dval = solved ? dmax : -1.0;
                     }
                     __syncthreads();
@@ -892,7 +951,10 @@ __global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
             }
         }
         __syncthreads();
-        // ---- final residual, gradient norm, validity (warp 0)
+        const long long t_valid = clock64();
+        // ---- final residual, gradient norm, validity.  Warp 0: residual, on-edge, same side;
+        // then the support tests (one per reflection vertex) and the shadow rays (one per
+        // segment) run on separate warps; the status is the first failing check in R25 order.
         if (wid == 0) {
             double (*I)[3] = S.I;
             if (lane <= D.n + 1) vpoint(P, D, S.z, lane - 1, I[lane]);
@@ -927,43 +989,71 @@ __global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
                         const double sa = ddot(a, nbf[k]), sb = ddot(b, nbf[k]);
                         if (!((sa > 0 && sb > 0) || (sa < 0 && sb < 0))) status = NRT_REF_WRONG_SIDE;
                     }
-            if (status == NRT_REF_OK)
-                for (int k = 0; k < D.n && status == NRT_REF_OK; ++k)
-                    if (D.kind[k] == 0 && !supported(P, D.label[k], I[k + 1], lane)) status = NRT_REF_NO_SUPPORT;
-            if (status == NRT_REF_OK) {
-                for (int j = 0; j <= D.n && status == NRT_REF_OK; ++j) {
-                    double l0[6], l1[6];
-                    int n0 = 0, n1 = 0;
-                    if (j >= 1) {
-                        const int k = j - 1;
-                        if (D.kind[k] == 0) {
-                            for (int a = 0; a < 3; ++a) l0[a] = nbf[k][a];
-                            n0 = 1;
-                        } else {
-                            const DevEdge& E = P.edges[D.prim[k]];
-                            for (int a = 0; a < 3; ++a) {
-                                l0[a] = E.n0[a];
-                                l0[3 + a] = E.n1[a];
-                            }
-                            n0 = 2;
-                        }
-                    }
-                    if (j + 1 <= D.n) {
-                        const int k = j;
-                        if (D.kind[k] == 0) {
-                            for (int a = 0; a < 3; ++a) l1[a] = nbf[k][a];
-                            n1 = 1;
-                        } else {
-                            const DevEdge& E = P.edges[D.prim[k]];
-                            for (int a = 0; a < 3; ++a) {
-                                l1[a] = E.n0[a];
-                                l1[3 + a] = E.n1[a];
-                            }
-                            n1 = 2;
-                        }
-                    }
-                    if (occluded(P, I[j], I[j + 1], l0, n0, l1, n1, lane)) status = NRT_REF_OCCLUDED;
+            if (lane < 3 * D.n) S.nbv[lane / 3][lane % 3] = nbf[lane / 3][lane % 3];
+            if (lane == 0) {
+                S.vstat = status;
+                S.gsq = gsq;
+                S.rmax = rmax;
+            }
+        }
+        __syncthreads();
+        status = S.vstat;
+        if (status == NRT_REF_OK) {
+            const double (*I)[3] = S.I;
+            const double (*nbf)[3] = S.nbv;
+            for (int t = wid; t < 2 * D.n + 1; t += NW) {
+                if (t < D.n) {  // support of reflection vertex t (R25 c)
+                    const int k = t;
+                    const bool ok = D.kind[k] != 0 || supported(P, D.label[k], I[k + 1], lane);
+                    if (lane == 0) S.vflag[t] = ok ? 0 : 1;
+                    continue;
                 }
+                const int j = t - D.n;  // shadow ray of segment j (R25 d)
+                double l0[6], l1[6];
+                int n0 = 0, n1 = 0;
+                if (j >= 1) {
+                    const int k = j - 1;
+                    if (D.kind[k] == 0) {
+                        for (int a = 0; a < 3; ++a) l0[a] = nbf[k][a];
+                        n0 = 1;
+                    } else {
+                        const DevEdge& E = P.edges[D.prim[k]];
+                        for (int a = 0; a < 3; ++a) {
+                            l0[a] = E.n0[a];
+                            l0[3 + a] = E.n1[a];
+                        }
+                        n0 = 2;
+                    }
+                }
+                if (j + 1 <= D.n) {
+                    const int k = j;
+                    if (D.kind[k] == 0) {
+                        for (int a = 0; a < 3; ++a) l1[a] = nbf[k][a];
+                        n1 = 1;
+                    } else {
+                        const DevEdge& E = P.edges[D.prim[k]];
+                        for (int a = 0; a < 3; ++a) {
+                            l1[a] = E.n0[a];
+                            l1[3 + a] = E.n1[a];
+                        }
+                        n1 = 2;
+                    }
+                }
+                const bool occ = occluded(P, I[j], I[j + 1], l0, n0, l1, n1, lane);
+                if (lane == 0) S.vflag[t] = occ ? 1 : 0;
+            }
+        }
+        __syncthreads();
+        if (wid == 0) {
+            double (*I)[3] = S.I;
+            const double (*nbf)[3] = S.nbv;
+            const double gsq = S.gsq, rmax = S.rmax;
+            if (status == NRT_REF_OK) {
+                for (int k = 0; k < D.n; ++k)
+                    if (S.vflag[k]) status = NRT_REF_NO_SUPPORT;
+                if (status == NRT_REF_OK)
+                    for (int j = 0; j <= D.n; ++j)
+                        if (S.vflag[D.n + j]) status = NRT_REF_OCCLUDED;
             }
             if (lane == 0 && (P.keep_invalid || status == NRT_REF_OK)) {
                 nrt_refined_rec o;
@@ -1003,7 +1093,10 @@ __global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
                 o.iters = it;
                 o.resid = m ? rmax : 0.0;
                 o.gradsq = gsq;
-                if (P.cycles) P.cycles[jq] = clock64() - t_start;
+                if (P.cycles) {
+                    P.cycles[jq] = clock64() - t_start;
+                    atomicAdd(&g_dbg[7], (unsigned long long)(clock64() - t_valid));
+                }
                 const unsigned long long at = P.keep_invalid ? (unsigned long long)jq : atomicAdd(P.n_out, 1ull);
                 P.out[at] = o;
             }
@@ -1089,6 +1182,8 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     if (timing) {
         NRT_CUDA(cudaMallocAsync(&P.cycles, (size_t)(n_mine > 0 ? n_mine : 1) * 8, st));
         NRT_CUDA(cudaMemsetAsync(P.cycles, 0, (size_t)(n_mine > 0 ? n_mine : 1) * 8, st));
+        const unsigned long long zero[12] = {};
+        NRT_CUDA(cudaMemcpyToSymbolAsync(g_dbg, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st));
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine, 32 * NW, smem);
@@ -1132,8 +1227,8 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
                 (double)tot, (long long)blocks);
         unsigned long long dbg[12];
         cudaMemcpyFromSymbol(dbg, g_dbg, sizeof(dbg));
-        fprintf(stderr, "[nrt]   block cycles: regather %.3g jacobian %.3g solve %.3g linesearch %.3g\n",
-                (double)dbg[8], (double)dbg[9], (double)dbg[10], (double)dbg[11]);
+        fprintf(stderr, "[nrt]   block cycles: prologue %.3g regather %.3g jacobian %.3g solve %.3g linesearch %.3g validity %.3g\n",
+                (double)dbg[6], (double)dbg[8], (double)dbg[9], (double)dbg[10], (double)dbg[11], (double)dbg[7]);
         fprintf(stderr, "[nrt]   mls list %llu direct %llu, ls rounds %llu, gathers %llu\n", dbg[0], dbg[1],
                 dbg[2], dbg[3]);
         fprintf(stderr, "[nrt]   avg cycles: mls list %.0f direct %.0f\n", (double)dbg[4] / (dbg[0] + 1),
