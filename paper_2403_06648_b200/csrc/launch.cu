@@ -1286,11 +1286,26 @@ static nrt_status run_bounces(const TP& P, Wave& W, int iters, int dev, bool cou
         NRT_CUDA(cudaFuncSetAttribute(k_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shade_smem));
     cudaEvent_t ev[3 * kMaxIter + 3];
     for (int i = 0; i < 3 * iters; ++i) cudaEventCreate(&ev[i]);
+    unsigned long long last[3] = {0, 0, 0};
+    if (counters && P.counters && getenv("NRT_BOUNCE_STATS")) {
+        cudaMemcpyAsync(last, P.counters, sizeof(last), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+    }
     for (int b = 0; b < iters; ++b) {
         cudaEventRecord(ev[3 * b], st);
         if (counters) NRT_K_TRACE<true><<<tb, 128, 0, st>>>(P, W, b);
         else NRT_K_TRACE<false><<<tb, 128, 0, st>>>(P, W, b);
         ::nrt::count_launch();
+        if (counters && P.counters && getenv("NRT_BOUNCE_STATS")) {  // diagnostics: per-bounce work
+            unsigned long long c[3], na = 0;
+            cudaMemcpyAsync(c, P.counters, sizeof(c), cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(&na, W.n_alive + b, sizeof(na), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            fprintf(stderr, "[nrt] bounce %d: %llu segments, %.1f tests, %.1f cells, %.1f non-empty per segment\n", b, na,
+                    (double)(c[0] - last[0]) / (na ? na : 1), (double)(c[1] - last[1]) / (na ? na : 1),
+                    (double)(c[2] - last[2]) / (na ? na : 1));
+            for (int q = 0; q < 3; ++q) last[q] = c[q];
+        }
         cudaEventRecord(ev[3 * b + 1], st);
         k_shade<<<sb, 128, shade_smem, st>>>(P, W, b);
         ::nrt::count_launch();
