@@ -149,6 +149,12 @@ typedef struct {
     double theta_ex_deg; /* sheet angle for shadow rays, default 25 */
     int32_t rank, world; /* path shard: j == rank (mod world) */
     int32_t keep_invalid; /* 1 = keep failed paths in the output (with their status) */
+    int32_t select;       /* 0 = every path; 1 = only paths without a diffraction; 2 = only
+                             paths with one (R17 keys of the two kinds are disjoint, so the two
+                             refined sets are independent — refine the primary-ray paths while
+                             the fans are still being traced, then merge) */
+    int32_t blocks_per_sm; /* 0 = as many resident path blocks per SM as fit; k > 0 caps it
+                             (leaves room for kernels running concurrently on other streams) */
     void* stream;
 } nrt_refine_desc;
 void nrt_refine_desc_default(nrt_refine_desc* d);

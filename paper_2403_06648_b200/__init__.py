@@ -66,6 +66,7 @@ class nrt_refine_desc(C.Structure):
                 ("max_iter", C.c_int32), ("alpha", C.c_double), ("beta", C.c_double),
                 ("delta", C.c_double), ("tau", C.c_double), ("theta_ex_deg", C.c_double),
                 ("rank", C.c_int32), ("world", C.c_int32), ("keep_invalid", C.c_int32),
+                ("select", C.c_int32), ("blocks_per_sm", C.c_int32),
                 ("stream", C.c_void_p)]
 
 
@@ -274,12 +275,20 @@ class Paths:
         _check(lib().nrt_paths_export(self.h, C.c_void_p(a.ctypes.data), a.nbytes, MEM_HOST))
         return a
 
-    def export_events(self):
-        """Stage-1 events (nrt_event_rec) of a launch handle, host numpy."""
+    def export_events(self, device=None):
+        """Stage-1 events (nrt_event_rec) of a launch handle: host numpy, or a torch uint8
+        tensor on `device` (device-to-device copy)."""
         n = C.c_int64()
         st = lib().nrt_paths_export_events(self.h, None, 0, C.byref(n), MEM_HOST)
         if st not in (0, 4):
             _check(st)
+        if device is not None:
+            import torch
+            t = torch.zeros(n.value * EVENT_REC.itemsize, dtype=torch.uint8, device=device)
+            if n.value:
+                _check(lib().nrt_paths_export_events(self.h, C.c_void_p(t.data_ptr()), t.numel(),
+                                                     C.byref(n), MEM_DEVICE))
+            return t
         a = np.zeros(n.value, EVENT_REC)
         if n.value:
             _check(lib().nrt_paths_export_events(self.h, C.c_void_p(a.ctypes.data), a.nbytes,

@@ -548,6 +548,8 @@ void nrt_refine_desc_default(nrt_refine_desc* d) {
     d->rank = 0;
     d->world = 1;
     d->keep_invalid = 0;
+    d->select = 0;
+    d->blocks_per_sm = 0;
     d->stream = nullptr;
 }
 
@@ -571,6 +573,8 @@ nrt_status nrt_refine_ex(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d
         return set_error(NRT_E_INVALID, "bad refine parameters");
     if (d.world < 1 || d.rank < 0 || d.rank >= d.world)
         return set_error(NRT_E_INVALID, "need 0 <= rank < world");
+    if (d.select < 0 || d.select > 2) return set_error(NRT_E_INVALID, "select must be 0, 1 or 2");
+    if (d.blocks_per_sm < 0) return set_error(NRT_E_INVALID, "blocks_per_sm must be >= 0");
     NRT_CUDA(cudaSetDevice(s->device));
     ensure_pool(s->device);
     nrt_paths P = new nrt_paths_s();

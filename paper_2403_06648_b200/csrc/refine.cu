@@ -674,6 +674,13 @@ __global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
         }
         __syncthreads();
         const int m = D.dim;
+        // no state of the block's previous path survives (residual and MLS point/normal of a
+        // path whose first residual is undefined are reported as zero)
+        for (int e = tid; e < 3 * NRT_MAX_INT; e += blockDim.x) {
+            (&S.pb[0][0])[e] = 0.0;
+            (&S.nb[0][0])[e] = 0.0;
+            S.r[e] = 0.0;
+        }
         if (tid == 0)
             for (int k = 0; k < D.n; ++k) {
                 if (D.kind[k] == 0) {
@@ -1105,12 +1112,69 @@ __global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
     }
 }
 
+// select flags (nrt_refine_desc.select): 1 keeps paths without a diffraction, 2 with one
+// (f may be null: sel = 0 keeps everything); nrefl_max = max reflections of a kept path
+__global__ void k_select_flags(const nrt_coarse_rec* in, int64_t n, int sel, unsigned char* f,
+                               int* nrefl_max) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const bool keep = sel == 0 || (in[i].n_diff > 0) == (sel == 2);
+    if (f) f[i] = keep;
+    if (keep) atomicMax(nrefl_max, (int)in[i].n_int - (int)in[i].n_diff);
+}
+
 }  // namespace
 
 nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
                   cudaStream_t st) {
-    const int64_t n = coarse->n;
+    int64_t n = coarse->n;
     out->n = 0;
+    const nrt_coarse_rec* in = (const nrt_coarse_rec*)coarse->d_rec;
+    nrt_coarse_rec* sel_buf = nullptr;
+    // reflection vertices per path bound the shared candidate slots; a launch handle knows its
+    // max_refl, an imported or filtered set is scanned
+    int nrefl = coarse->max_refl > 0 ? coarse->max_refl : -1;
+    if ((d->select != 0 || nrefl < 0) && n > 0) {  // order-preserving compaction of the selected kind
+        unsigned char* flags = nullptr;
+        int64_t* d_ns = nullptr;
+        int* d_nr = nullptr;
+        void* tmp = nullptr;
+        size_t tb = 0;
+        cub::DeviceSelect::Flagged(nullptr, tb, in, (unsigned char*)nullptr, (nrt_coarse_rec*)nullptr,
+                                   (int64_t*)nullptr, n, st);
+        if (d->select != 0) {
+            NRT_CUDA(cudaMallocAsync(&sel_buf, n * sizeof(nrt_coarse_rec), st));
+            NRT_CUDA(cudaMallocAsync(&flags, n, st));
+            NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+        }
+        NRT_CUDA(cudaMallocAsync(&d_ns, sizeof(int64_t) + sizeof(int), st));
+        d_nr = (int*)(d_ns + 1);
+        NRT_CUDA(cudaMemsetAsync(d_ns, 0, sizeof(int64_t) + sizeof(int), st));
+        k_select_flags<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, n, d->select, flags, d_nr);
+        ::nrt::count_launch();
+        if (d->select != 0) cub::DeviceSelect::Flagged(tmp, tb, in, flags, sel_buf, d_ns, n, st);
+        struct {
+            int64_t ns;
+            int nr;
+        } h{0, 0};
+        NRT_CUDA(cudaMemcpyAsync(&h, d_ns, sizeof(int64_t) + sizeof(int), cudaMemcpyDeviceToHost, st));
+        NRT_CUDA(cudaStreamSynchronize(st));
+        cudaFreeAsync(flags, st);
+        cudaFreeAsync(d_ns, st);
+        cudaFreeAsync(tmp, st);
+        if (d->select != 0) {
+            in = sel_buf;
+            n = h.ns;
+        }
+        nrefl = h.nr;
+    }
+    struct SelGuard {
+        nrt_coarse_rec* p;
+        cudaStream_t st;
+        ~SelGuard() {
+            if (p) cudaFreeAsync(p, st);
+        }
+    } sel_guard{sel_buf, st};
     RP P{};
     P.cell = s->cell;
     P.rec = s->rec;
@@ -1132,7 +1196,7 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     P.hy = s->hdims[1];
     P.hz = s->hdims[2];
     P.edges = s->edges;
-    P.in = (const nrt_coarse_rec*)coarse->d_rec;
+    P.in = in;
     P.n_in = n;
     P.rank = d->rank;
     P.world = d->world;
@@ -1154,12 +1218,7 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     P.max_iter = d->max_iter;
     P.keep_invalid = d->keep_invalid;
     // shared candidate slots: one per reflection vertex of the longest path (<= max_refl)
-    int nv = 0;
-    {
-        // the coarse set's max reflections = its launch max_refl (imports: assume NRT_MAX_INT)
-        nv = coarse->max_refl > 0 ? coarse->max_refl : NRT_MAX_INT;
-        if (nv > NRT_MAX_INT) nv = NRT_MAX_INT;
-    }
+    int nv = nrefl < 1 ? 1 : nrefl > NRT_MAX_INT ? NRT_MAX_INT : nrefl;
     P.nv_max = nv;
     const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) + (size_t)nv * kCapS * 6 * sizeof(float);
     NRT_CUDA(cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1188,6 +1247,7 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine, 32 * NW, smem);
     if (per_sm < 1) per_sm = 1;
+    if (d->blocks_per_sm > 0 && d->blocks_per_sm < per_sm) per_sm = d->blocks_per_sm;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
     int64_t blocks = (int64_t)sms * per_sm;

@@ -109,3 +109,18 @@ def test_refine_sharding_union(N):
     for r, p in enumerate(parts):
         merged[r::3] = p
     assert merged.tobytes() == full.tobytes()
+
+
+def test_select_partitions(N):
+    """select=1/2 split the coarse set by diffraction (disjoint R17/R28 keys): their refined
+    records are exactly the full run's; blocks_per_sm only changes the schedule."""
+    case = G.case("C2s", sigma=0.005, n=12_000, n_rays=8000, max_refl=2, max_diff=1)
+    sc = N.build_case_scene(case)
+    coarse = N.launch_case(sc, case)
+    full = refine_gpu(N, case, sc, coarse)
+    p1 = refine_gpu(N, case, sc, coarse, select=1)
+    p2 = refine_gpu(N, case, sc, coarse, select=2, blocks_per_sm=1)
+    assert len(p1) + len(p2) == len(full) and len(p2) > 0 and len(p1) > 0
+    diff = coarse.export()["n_diff"] > 0
+    assert p1.tobytes() == full[~diff].tobytes()
+    assert p2.tobytes() == full[diff].tobytes()
