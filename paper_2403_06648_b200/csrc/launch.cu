@@ -70,6 +70,7 @@ struct Wave {
     unsigned* alive[2];       // ping-pong live lists
     unsigned* okey[2];        // ordering keys (primary batches)
     unsigned* oval;           // ordering values (slot ids)
+    unsigned* skey;           // SHADE: ordering keys of the next live list (null: no reorder)
     void* otmp;               // radix-sort temporary storage
     size_t otmp_bytes;
     unsigned long long* n_alive;  // [kMaxIter + 1]
@@ -93,6 +94,7 @@ struct TP {  // trace parameters (by value into the kernels)
     int max_refl, max_diff;
     float tau, cos_ex, cRw, b_e, edge_bin, c_R, dphi_deg;
     float slack;  // absolute slack of the division-free disk prefilter (m)
+    float ok_inv;  // 1 / (coarse ordering cell): 64 coarse cells span the grid's longest axis
     // receiver home grid (many RX): cells of rxg_v, RX sorted by cell as (x, y, z, j bits)
     const uint2* rxg_cell;
     const float4* rxg_rx;
@@ -854,6 +856,34 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace_coop(TP P, Wave W
     flush_counts(P, bounces, cnt, CNT);
 }
 
+// coherence key of a segment (origin h, direction d): Morton code of its coarse cell (6 bits
+// per axis), then the octahedral direction (7 + 7 bits).  Only the processing order of the
+// next bounce depends on it, never a result.
+__device__ __forceinline__ unsigned spread3(unsigned x) {  // 6 bits -> every third bit
+    x &= 63u;
+    x = (x | (x << 8)) & 0x0000F00Fu;
+    x = (x | (x << 4)) & 0x000C30C3u;
+    x = (x | (x << 2)) & 0x00249249u;
+    return x;
+}
+__device__ __forceinline__ unsigned order_key(const TP& P, float3 h, float3 d) {
+    const unsigned cx = (unsigned)min(63, max(0, (int)((h.x - P.ox) * P.ok_inv)));
+    const unsigned cy = (unsigned)min(63, max(0, (int)((h.y - P.oy) * P.ok_inv)));
+    const unsigned cz = (unsigned)min(63, max(0, (int)((h.z - P.oz) * P.ok_inv)));
+    const unsigned m = spread3(cx) | (spread3(cy) << 1) | (spread3(cz) << 2);
+    const float sa = fabsf(d.x) + fabsf(d.y) + fabsf(d.z);
+    float px = d.x / sa, py = d.y / sa;
+    if (d.z < 0.0f) {
+        const float qx = (1.0f - fabsf(py)) * (px < 0.0f ? -1.0f : 1.0f);
+        const float qy = (1.0f - fabsf(px)) * (py < 0.0f ? -1.0f : 1.0f);
+        px = qx;
+        py = qy;
+    }
+    const unsigned u = (unsigned)min(127, max(0, (int)((px + 1.0f) * 64.0f)));
+    const unsigned v = (unsigned)min(127, max(0, (int)((py + 1.0f) * 64.0f)));
+    return (m << 14) | (u << 7) | v;
+}
+
 // SHADE: captures, edge events, reflection; compacts the live list for bounce b+1.
 // Receivers (few) and edge cull spheres are staged in shared memory and looped over with a
 // warp-uniform trip count (one broadcast read per receiver/edge for the whole warp).
@@ -926,7 +956,9 @@ __global__ void __launch_bounds__(128) k_shade(TP P, Wave W, int b) {
             c.L = L + th;
             c.Ls = Ls + th;
             c.seg = c.seg + 1;
-            next[agg_inc(&W.n_alive[b + 1])] = ray;
+            const unsigned long long slot = agg_inc(&W.n_alive[b + 1]);
+            next[slot] = ray;
+            if (W.skey) W.skey[slot] = order_key(P, hp, make_float3(x.x / l, x.y / l, x.z / l));
         }
     }
 }
@@ -1062,6 +1094,10 @@ TP make_tp(nrt_scene s, const LaunchArgs& a) {
     P.oz = s->org[2];
     P.v = s->v;
     P.inv_v = s->inv_v;
+    {
+        const int md = std::max(s->dims[0], std::max(s->dims[1], s->dims[2]));
+        P.ok_inv = 1.0f / (s->v * (float)((md + 63) / 64));
+    }
     P.pad = s->pad;
     P.slack = fmaxf(s->slack, 4e-6f * fmaxf(fabsf(a.tx[0]), fmaxf(fabsf(a.tx[1]), fabsf(a.tx[2]))));
     P.nx = s->dims[0];
@@ -1224,8 +1260,19 @@ struct Counters {
 
 static std::atomic<unsigned long long> g_hint_raw{0}, g_hint_ev{0}, g_hint_fan{0};
 static const uint64_t kBatch = 1ull << 24;  // rays in flight per wavefront batch
+static const unsigned long long kSortMin = 1ull << 15;  // reorder live lists at least this long
 
 // wavefront buffers for up to `cap` rays (stream-ordered; freed by free_wave)
+// Reorder each bounce's live list by (coarse cell, direction) only when the scene's records
+// are well beyond L2 (measured: C5, 0.9 GB of records, trace -7 %; C2, 243 MB, no gain and
+// +0.45 ms of sorts).  NRT_REORDER=0/1 forces it.
+static bool reorder_on(nrt_scene s) {
+    if (const char* e = getenv("NRT_REORDER")) return atoi(e) != 0;
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s->device);
+    return (double)s->nref * 32.0 > 4.0 * (double)l2;
+}
+
 static nrt_status alloc_wave(Wave& W, uint64_t cap, int dev, cudaStream_t st) {
     if (cap < 1) cap = 1;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
@@ -1245,6 +1292,7 @@ static nrt_status alloc_wave(Wave& W, uint64_t cap, int dev, cudaStream_t st) {
         W.oval = (unsigned*)(q + 2 * b_a);
         W.otmp = q + 3 * b_a;
         W.otmp_bytes = b_t;
+        W.skey = nullptr;  // per-bounce coherence reorder: see reorder_on()
     }
     W.slab = p;
     W.o = (float4*)p;
@@ -1309,6 +1357,22 @@ static nrt_status run_bounces(const TP& P, Wave& W, int iters, int dev, bool cou
         cudaEventRecord(ev[3 * b + 1], st);
         k_shade<<<sb, 128, shade_smem, st>>>(P, W, b);
         ::nrt::count_launch();
+        if (W.skey && b + 1 < iters) {
+            // reorder the next live list by (coarse cell, direction): neighbouring lanes and
+            // blocks then walk the same cells and share their records in L1/L2
+            unsigned long long na = 0;
+            NRT_CUDA(cudaMemcpyAsync(&na, W.n_alive + b + 1, sizeof(na), cudaMemcpyDeviceToHost, st));
+            NRT_CUDA(cudaStreamSynchronize(st));
+            if (na >= kSortMin) {
+                size_t tb = W.otmp_bytes;
+                unsigned* nxt = W.alive[(b + 1) & 1];
+                NRT_CUDA(cub::DeviceRadixSort::SortPairs(W.otmp, tb, W.skey, W.okey[1], nxt, W.oval, (int)na,
+                                                         0, 32, st));
+                ::nrt::count_launch();
+                W.alive[(b + 1) & 1] = W.oval;
+                W.oval = nxt;
+            }
+        }
         cudaEventRecord(ev[3 * b + 2], st);
     }
     NRT_CUDA(cudaGetLastError());
@@ -1348,6 +1412,7 @@ nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw
     Wave W{};
     WaveGuard wg{&W, st};
     NRT_TRY(alloc_wave(W, n_shard < kBatch ? n_shard : kBatch, s->device, st));
+    if (reorder_on(s)) W.skey = W.okey[0];
     if (getenv("NRT_PHASES")) {
         cudaStreamSynchronize(st);
         cudaMemPool_t pool;
@@ -1476,6 +1541,7 @@ nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev
     Wave W{};
     WaveGuard wg{&W, st};
     if (total > 0) NRT_TRY(alloc_wave(W, total, s->device, st));
+    if (total > 0 && reorder_on(s)) W.skey = W.okey[0];
     W.n_alive = dc->n_alive;
     W.ctr = dc->ctr;
     for (int attempt = 0; attempt < 3 && total > 0; ++attempt) {
