@@ -331,7 +331,8 @@ def main():
     pb = 32 * prim_only["tests"] + 8 * prim_only["cells"]
     achieved = pb / (ms_trace / 1000.0) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "kernel": "k_trace (primary bounces)",
+            "frac": achieved / hbm, "traffic": measured_traffic(case.name),
+            "kernel": "k_trace (primary bounces)",
             "peak_source": src,
             "bytes_per_launch": pb, "bytes_per_bounce": pb / max(1, prim_only["bounces"]),
             "ms_per_launch": ms_trace}
@@ -391,6 +392,16 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def measured_traffic(workload):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed ncu
+    capture (profiles/r01_traffic.json, scripts/gpu_traffic.sh), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+        return float(t[workload]["dram_bytes_per_launch"])
+    except Exception:
+        return None
 
 
 def prim_counts(N, R, case):
