@@ -150,6 +150,40 @@ def test_c2_full_size_records_retraced_by_oracle(N, O, c2):
     assert keys == sorted(keys) and len(set(keys)) == len(keys)
 
 
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_full_size_sampled_hit_sequences_other_configs(N, O, name):
+    """BASELINE configs[2..4] at full size (1e6 surfels with PCA normals / 1e7 surfels of the
+    reconstructed-room recipe, 1e7 / 1e7 / 1e8-ray lattices): sampled rays' hit sequences
+    equal the brute-force argmin segment by segment."""
+    case = G.case(name)
+    sc = N.build_case_scene(case)
+    ids = np.sort(np.random.default_rng(5).choice(case.n_rays, 12, replace=False)).astype(np.uint64)
+    gpu = N.nrt_debug_trace_rays(sc, case.tx, case.n_rays, case.max_refl, ids, tau=case.tau,
+                                 theta_ex_deg=case.theta_ex_deg, c_R=case.c_R)
+    _, hits, _ = O.trace_rays(case, ids)
+    assert np.array_equal(gpu, hits)
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_full_size_records_retraced_other_configs(N, O, name):
+    """Full C4 (85 RX, diffraction on) and C5 (879 RX, 1e8 rays) launches: sampled primary
+    records are reproduced exactly by the oracle re-tracing their rays; keys unique+sorted."""
+    case = G.case(name)
+    sc = N.build_case_scene(case)
+    p = N.launch_case(sc, case)
+    got = p.export()
+    prim = got[got["ray_id"] < (1 << 63)]
+    assert len(prim) > 100
+    sample = prim[np.random.default_rng(2).permutation(len(prim))[:12]]
+    raw, _, _ = O.trace_rays(case, sample["ray_id"])
+    rb = {r.tobytes() for r in raw}
+    for r in sample:
+        assert r.tobytes() in rb
+    keys = [(int(r["rx"]), int(r["n_int"]), int(r["kinds"]), tuple(int(x) for x in r["label"]))
+            for r in got]
+    assert keys == sorted(keys) and len(set(keys)) == len(keys)
+
+
 # ------------------------------------------------------------------ sharding ------------
 def test_world_sharding_merge_equals_single(N, O):
     """R30: shards i == rank (mod world) merged by nrt_paths_merge == the world-1 set."""

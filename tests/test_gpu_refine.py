@@ -99,6 +99,23 @@ def test_c2_full_size_sampled_refined_parity(N, O):
     compare(got[idx], ref, 0.1, "C2 sample")
 
 
+def test_c4_full_size_sampled_refined_parity(N, O):
+    """Full C4 (1e7 surfels, fitted normals, 85 RX, diffraction): the oracle re-refines a
+    sample of the GPU's coarse paths one by one."""
+    case = G.case("C4")
+    sc = N.build_case_scene(case)
+    coarse = N.launch_case(sc, case)
+    cr = coarse.export()
+    allg = refine_gpu(N, case, sc, coarse)
+    rng = np.random.default_rng(4)
+    ok = np.nonzero(allg["status"] == 0)[0]
+    idx = np.sort(np.concatenate([rng.choice(ok, 6, replace=False),
+                                  rng.choice(len(cr), 2, replace=False)]))
+    got = allg[idx]
+    ref = O.refine(case, cr[idx])
+    compare(got, ref, 0.25, "C4 sample")
+
+
 def test_refine_sharding_union(N):
     case = G.case("C2s", sigma=0.0, n=20_000, n_rays=8000, max_diff=0)
     sc = N.build_case_scene(case)
