@@ -177,6 +177,18 @@ int or_path_residual(const or_scene* S, const or_refine_params* R, const or_coar
 int or_mls(const or_scene* S, const or_refine_params* R, int32_t label, const double nseed[3],
            const double x[3], double pbar[3], double nbar[3], double* f);
 
+/* refined-path post-processing (post.c; NEXT-3, readings R33-R36) */
+typedef struct {
+    double lambda_m;       /* wavelength of the first Fresnel zone (Eq. 13) */
+    double angle_deg;      /* ray-angle threshold of the duplicate test */
+    double r_s;            /* exact-label search radius = 2 r_s */
+    float tx[3];
+    const float* rx;       /* RX table indexed by the record's rx */
+} or_post_params;
+int64_t or_postprocess(const or_scene* S, const or_post_params* Q, const or_refined* in, int64_t n,
+                       or_refined* out);
+int or_fresnel_dup(const or_post_params* Q, double cos_max, const or_refined* a, const or_refined* b);
+
 #ifdef __cplusplus
 }
 #endif

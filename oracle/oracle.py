@@ -13,7 +13,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SRCS = ["coarse.c", "refine.c"]
+_SRCS = ["coarse.c", "refine.c", "post.c"]
 
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
           "-Wall", "-Wno-unused-function"]
@@ -461,3 +461,49 @@ def path_residual(case, rec, z=None, scene: OracleScene | None = None, **over):
     if m < 0:
         return None, None
     return r[:m].copy(), zs[:m].copy()
+
+
+class _PostParams(C.Structure):
+    _fields_ = [("lambda_m", C.c_double), ("angle_deg", C.c_double), ("r_s", C.c_double),
+                ("tx", C.c_float * 3), ("rx", C.c_void_p)]
+
+
+LAMBDA_60GHZ = 299792458.0 / 60e9   # Table I carrier frequency
+
+
+def _post_params(case, lambda_m=LAMBDA_60GHZ, angle_deg=10.0, r_s=None):
+    rxa = _f32(case.rx, (-1, 3))
+    q = _PostParams()
+    q.lambda_m = float(lambda_m)
+    q.angle_deg = float(angle_deg)
+    q.r_s = float(case.r_s if r_s is None else r_s)
+    q.tx[:] = [float(x) for x in np.asarray(case.tx, np.float32)]
+    q.rx = rxa.ctypes.data
+    return q, rxa
+
+
+def postprocess(case, refined, scene: OracleScene | None = None, **over):
+    """NEXT-3 post-processing of refined records (status-OK ones): exact labels, shortest per
+    key, delay order, greedy first-Fresnel-zone dedupe -> records in delay order."""
+    L = lib()
+    if not hasattr(L, "_post_setup"):
+        L.or_postprocess.argtypes = [C.POINTER(_Scene), C.POINTER(_PostParams), C.c_void_p,
+                                     C.c_int64, C.c_void_p]
+        L.or_postprocess.restype = C.c_int64
+        L.or_fresnel_dup.argtypes = [C.POINTER(_PostParams), C.c_double, C.c_void_p, C.c_void_p]
+        L._post_setup = True
+    sc = scene or OracleScene(case.scene)
+    q, rxa = _post_params(case, **over)
+    rin = np.ascontiguousarray(refined, dtype=REFINED_DTYPE)
+    out = np.zeros(max(1, rin.shape[0]), REFINED_DTYPE)
+    m = L.or_postprocess(C.byref(sc.c), C.byref(q), rin.ctypes.data, rin.shape[0], out.ctypes.data)
+    return out[:m].copy()
+
+
+def fresnel_dup(case, a, b, cos_max, **over):
+    """The duplicate predicate of R36 for two refined records (pin helper)."""
+    postprocess(case, np.zeros(0, REFINED_DTYPE), OracleScene(case.scene))
+    q, rxa = _post_params(case, **over)
+    ra = np.ascontiguousarray(np.asarray(a, REFINED_DTYPE).reshape(1))
+    rb = np.ascontiguousarray(np.asarray(b, REFINED_DTYPE).reshape(1))
+    return bool(lib().or_fresnel_dup(C.byref(q), float(cos_max), ra.ctypes.data, rb.ctypes.data))
