@@ -232,6 +232,29 @@ typedef struct {
     float ms_total;          /* device time of the whole call */
 } nrt_paths_info;
 
+/* ---------------------------------------------------------------------------------------
+ * Post-processing of refined paths (PAPER §II-E; DESIGN.md
+ * R33-R36): (1) every reflection vertex takes the label of the nearest surfel within 2 r_s
+ * ("the label of the closest point to the intersection point"; lowest id on ties; none
+ * -> unchanged); (2) the shortest path per (rx, interaction chain, labels) is kept;
+ * (3) paths are ordered by delay (ties in key order); (4) walking that order, a path
+ * is dropped when every interaction point lies inside the first Fresnel zone
+ * psi_k = sqrt(lambda s1 s2 / (s1 + s2)) (Eq. 13) of an earlier kept path with the same rx and
+ * chain and every pair of k-th rays is closer than angle_deg.  Input: a refined set
+ * (invalid records are ignored); output: a new refined set in delay order.  The input
+ * handle is not modified.  Errors: NRT_E_INVALID (null, lambda_m <= 0, angle_deg outside
+ * (0, 180), r_s < 0), NRT_E_STATE (not a refined set), NRT_E_NOMEM, NRT_E_CUDA.
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+    double lambda_m;  /* wavelength; default 299792458 / 60e9 m (60 GHz carrier, Table I) */
+    double angle_deg; /* ray-angle threshold of the duplicate test; default 10 */
+    double r_s;       /* exact-label search radius is 2 r_s; default 0.003 (Table II) */
+    void* stream;
+} nrt_post_desc;
+void nrt_post_desc_default(nrt_post_desc* d);
+nrt_status nrt_postprocess(nrt_scene s, nrt_paths refined, const nrt_post_desc* desc,
+                           nrt_paths* out);
+
 nrt_status nrt_paths_count(nrt_paths p, int64_t* n);
 nrt_status nrt_paths_record_size(nrt_paths p, int64_t* bytes);
 nrt_status nrt_paths_info_get(nrt_paths p, nrt_paths_info* info);

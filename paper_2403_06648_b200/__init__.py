@@ -61,6 +61,11 @@ class nrt_launch_desc(C.Structure):
                 ("counters", C.c_int32), ("mem", C.c_int), ("stream", C.c_void_p)]
 
 
+class nrt_post_desc(C.Structure):
+    _fields_ = [("lambda_m", C.c_double), ("angle_deg", C.c_double), ("r_s", C.c_double),
+                ("stream", C.c_void_p)]
+
+
 class nrt_refine_desc(C.Structure):
     _fields_ = [("xi", C.c_double), ("r_s", C.c_double), ("tol_m", C.c_double),
                 ("max_iter", C.c_int32), ("alpha", C.c_double), ("beta", C.c_double),
@@ -113,6 +118,8 @@ _SIGS = {
     "nrt_refine_desc_default": ([_P(nrt_refine_desc)], None),
     "nrt_refine": ([_VP, _VP, _P(_VP)], C.c_int),
     "nrt_refine_ex": ([_VP, _VP, _P(nrt_refine_desc), _P(_VP)], C.c_int),
+    "nrt_post_desc_default": ([_P(nrt_post_desc)], None),
+    "nrt_postprocess": ([_VP, _VP, _P(nrt_post_desc), _P(_VP)], C.c_int),
     "nrt_paths_count": ([_VP, _P(C.c_int64)], C.c_int),
     "nrt_paths_record_size": ([_VP, _P(C.c_int64)], C.c_int),
     "nrt_paths_info_get": ([_VP, _P(nrt_paths_info)], C.c_int),
@@ -414,6 +421,20 @@ def nrt_refine_ex(scene: Scene, coarse: Paths, **desc) -> Paths:
     d = refine_desc(stream=desc.pop("stream", None), **desc)
     h = C.c_void_p()
     _check(lib().nrt_refine_ex(scene.h, coarse.h, C.byref(d), C.byref(h)))
+    return Paths(h.value)
+
+
+def nrt_postprocess(scene: Scene, refined: Paths, **desc) -> Paths:
+    """NEXT-3 post-processing (exact labels, shortest per key, delay order, first-Fresnel-zone
+    dedupe) of a refined set -> a new refined set in delay order."""
+    d = nrt_post_desc()
+    lib().nrt_post_desc_default(C.byref(d))
+    for k, v in desc.items():
+        setattr(d, k, _stream_ptr(v) if k == "stream" else v)
+    if "stream" not in desc:
+        d.stream = _stream_ptr(None)
+    h = C.c_void_p()
+    _check(lib().nrt_postprocess(scene.h, refined.h, C.byref(d), C.byref(h)))
     return Paths(h.value)
 
 

@@ -262,6 +262,7 @@ void nrt_scene_free(nrt_scene s) {
     cudaFreeAsync(s->label, nullptr);
     cudaFreeAsync(s->hcell, nullptr);
     cudaFreeAsync(s->hrec, nullptr);
+    cudaFreeAsync(s->hid, nullptr);
     cudaFreeAsync(s->edges, nullptr);
     delete s;
 }
@@ -557,6 +558,43 @@ nrt_status nrt_refine(nrt_scene s, nrt_paths coarse, nrt_paths* out) {
     nrt_refine_desc d;
     nrt_refine_desc_default(&d);
     return nrt_refine_ex(s, coarse, &d, out);
+}
+
+void nrt_post_desc_default(nrt_post_desc* d) {
+    if (!d) return;
+    d->lambda_m = 299792458.0 / 60e9;
+    d->angle_deg = 10.0;
+    d->r_s = 0.003;
+    d->stream = nullptr;
+}
+
+nrt_status nrt_postprocess(nrt_scene s, nrt_paths refined, const nrt_post_desc* desc, nrt_paths* out) {
+    clear_error();
+    if (!s || !refined || !out) return set_error(NRT_E_INVALID, "null argument");
+    *out = nullptr;
+    if (refined->kind != NRT_PATHS_REFINED) return set_error(NRT_E_STATE, "post-processing needs a refined set");
+    nrt_post_desc d;
+    if (desc) d = *desc;
+    else nrt_post_desc_default(&d);
+    if (!(d.lambda_m > 0 && d.angle_deg > 0 && d.angle_deg < 180 && d.r_s >= 0))
+        return set_error(NRT_E_INVALID, "bad post-processing parameters");
+    NRT_CUDA(cudaSetDevice(s->device));
+    ensure_pool(s->device);
+    nrt_paths P = new nrt_paths_s();
+    P->kind = NRT_PATHS_REFINED;
+    P->device = s->device;
+    memcpy(P->tx, refined->tx, 12);
+    P->rx = refined->rx;
+    P->info.kind = NRT_PATHS_REFINED;
+    nrt_status rc = postprocess(s, refined, &d, P, (cudaStream_t)d.stream);
+    if (rc != NRT_OK) {
+        nrt_paths_free(P);
+        return rc;
+    }
+    P->info.n = P->n;
+    P->info.n_raw = refined->n;
+    *out = P;
+    return NRT_OK;
 }
 
 nrt_status nrt_refine_ex(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* desc,

@@ -142,6 +142,7 @@ struct nrt_scene_s {
     int hdims[3] = {0, 0, 0};
     uint2* hcell = nullptr;
     float4* hrec = nullptr;
+    unsigned* hid = nullptr;   // [n] surfel id of each home record
     int32_t* label = nullptr;  // [n]
     nrt::DevEdge* edges = nullptr;
     int n_edges = 0;
@@ -176,6 +177,8 @@ nrt_status dedupe_events(const nrt_event_rec* in, int64_t n, nrt_event_rec* out,
                          cudaStream_t st);
 nrt_status dedupe_refined(const nrt_refined_rec* in, int64_t n, nrt_refined_rec* out,
                           int64_t* n_out, cudaStream_t st);
+// post.cu
+nrt_status postprocess(nrt_scene s, nrt_paths in, const nrt_post_desc* d, nrt_paths out, cudaStream_t st);
 // launch.cu
 struct RxGrid {  // receiver home grid (device arrays; null when the RX set is small)
     uint2* cell = nullptr;

@@ -471,8 +471,8 @@ static nrt_status build_impl(const nrt_scene_desc* D, nrt_scene S, cudaStream_t 
         NRT_CUDA(cudaGetLastError());
         cudaFreeAsync(hk0, st);
         cudaFreeAsync(hk1, st);
-        cudaFreeAsync(hv0, st);
-        cudaFreeAsync(hv1, st);
+        S->hid = hvb.Current();  // kept: surfel ids of the home records (post-processing)
+        cudaFreeAsync(hvb.Current() == hv0 ? hv1 : hv0, st);
     }
     // labels array (int) for the history
     {
