@@ -328,6 +328,7 @@ def main():
     # counters cover primary + fans together; split by kernel time share is not exact, so the
     # primary kernel's bytes come from a primary-only instrumented launch below
     prim_only = prim_counts(N, R, case)
+    post = post_timing(N, R, case) if refine_on else None
     pb = 32 * prim_only["tests"] + 8 * prim_only["cells"]
     achieved = pb / (ms_trace / 1000.0) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -382,6 +383,8 @@ def main():
         "step_ms": [round(x, 3) for x in step_ms],
         "phase_ms_build_launch_refine": [o["phase_ms"] for o in outs],
         "roofline": roof,
+        # NEXT-3 post-processing (not a §8(a) row: timed separately, outside the step)
+        "postprocess": post,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "e2e": e2e,
@@ -392,6 +395,30 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def post_timing(N, R, case, reps=3):
+    """Device time of nrt_postprocess on this workload's refined set (median of reps)."""
+    import torch
+    sc = N.nrt_scene_build_ex(R.pts, R.nrm, case.voxel, radii=R.rad, labels=R.lab,
+                              edges=case.scene.edges, stream=R.stream)
+    coarse = N.nrt_launch_ex(sc, R.tx, R.rx, R.n_rays, case.max_refl, case.max_diff,
+                             rank=R.rank, world=R.world, stream=R.stream, **R.desc) \
+        if R.world == 1 else None
+    if coarse is None:
+        return None
+    ref = N.nrt_refine_ex(sc, coarse, stream=R.stream, **R.rdesc)
+    ms, n_out = [], 0
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(R.stream)
+        p = N.nrt_postprocess(sc, ref, r_s=case.r_s, stream=R.stream)
+        b.record(R.stream)
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+        n_out = p.count()
+        p.free()
+    return {"ms": statistics.median(ms), "paths_in": ref.count(), "paths_out": n_out}
 
 
 def measured_traffic(workload):
