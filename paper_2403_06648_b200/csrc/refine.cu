@@ -140,7 +140,7 @@ __device__ __forceinline__ float* cand_ptr(float* cand, int s) { return cand + (
 
 typedef cub::BlockScan<int, 32 * NW> BlockScanT;
 
-__device__ unsigned long long g_dbg[12];  // diagnostics (NRT_REFINE_TIMING): MLS list/direct, LS rounds, gathers
+__device__ unsigned long long g_dbg[16];  // diagnostics (NRT_REFINE_TIMING): MLS list/direct, LS rounds, gathers
 
 // home-grid cell range of the axis-aligned box [c - R, c + R] (clamped)
 struct Box {
@@ -332,6 +332,10 @@ __device__ bool mls(const RP& P, const Path& D, int k, const double x[3], const 
     }
     W = wsum(W);
     if (P.cycles && lane == 0) atomicAdd(&g_dbg[use_list ? 4 : 5], (unsigned long long)(clock64() - t_mls0));
+    if (P.cycles && lane == 0 && !use_list && !(W > 0.0)) {
+        atomicAdd(&g_dbg[12], 1ull);
+        atomicAdd(&g_dbg[13], (unsigned long long)(clock64() - t_mls0));
+    }
     Px = wsum(Px);
     Py = wsum(Py);
     Pz = wsum(Pz);
@@ -1241,7 +1245,7 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     if (timing) {
         NRT_CUDA(cudaMallocAsync(&P.cycles, (size_t)(n_mine > 0 ? n_mine : 1) * 8, st));
         NRT_CUDA(cudaMemsetAsync(P.cycles, 0, (size_t)(n_mine > 0 ? n_mine : 1) * 8, st));
-        const unsigned long long zero[12] = {};
+        const unsigned long long zero[16] = {};
         NRT_CUDA(cudaMemcpyToSymbolAsync(g_dbg, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st));
     }
     int per_sm = 0;
@@ -1285,7 +1289,7 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
         for (int64_t i = 0; i < n_mine; ++i) tot += cyc[i];
         fprintf(stderr, "[nrt] refine: %lld paths, sum %.3g cycles, blocks %lld\n", (long long)n_mine,
                 (double)tot, (long long)blocks);
-        unsigned long long dbg[12];
+        unsigned long long dbg[16];
         cudaMemcpyFromSymbol(dbg, g_dbg, sizeof(dbg));
         fprintf(stderr, "[nrt]   block cycles: prologue %.3g regather %.3g jacobian %.3g solve %.3g linesearch %.3g validity %.3g\n",
                 (double)dbg[6], (double)dbg[8], (double)dbg[9], (double)dbg[10], (double)dbg[11], (double)dbg[7]);
@@ -1293,6 +1297,8 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
                 dbg[2], dbg[3]);
         fprintf(stderr, "[nrt]   avg cycles: mls list %.0f direct %.0f\n", (double)dbg[4] / (dbg[0] + 1),
                 (double)dbg[5] / (dbg[1] + 1));
+        fprintf(stderr, "[nrt]   direct MLS with an empty neighbourhood: %llu (%.3g cycles)\n", dbg[12],
+                (double)dbg[13]);
         for (int64_t i = 0; i < n_mine && i < 12; ++i)
             fprintf(stderr, "[nrt]   path %lld: %.3g cycles, n_int %d, iters %d, status %d\n",
                     (long long)ix[i], (double)cyc[ix[i]], rr[ix[i]].n_int, rr[ix[i]].iters,
