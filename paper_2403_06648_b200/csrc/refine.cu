@@ -620,10 +620,12 @@ __device__ bool supported(const RP& P, int32_t label, const double x[3], int lan
     return __any_sync(0xffffffffu, s);
 }
 
-#ifndef NRT_REFINE_MINB
-#define NRT_REFINE_MINB 3
-#endif
-__global__ void __launch_bounds__(32 * NW, NRT_REFINE_MINB) k_refine(RP P) {
+// Two register budgets of the same kernel: MINB = 3 resident blocks per SM (80 registers) is
+// the throughput regime (many paths: C4/C5), MINB = 2 (128 registers, no spills) the latency
+// regime (few paths, a tail of long GN runs: C2).  Measured: C2 refine -4.6 % with 2,
+// C4 +12 % with 2.  refine() picks by the number of paths.
+template <int MINB>
+__global__ void __launch_bounds__(32 * NW, MINB) k_refine(RP P) {
     extern __shared__ __align__(16) unsigned char dyn[];
     Smem& S = *reinterpret_cast<Smem*>(dyn);
     float* cand = reinterpret_cast<float*>(dyn + ((sizeof(Smem) + 15) & ~size_t(15)));
@@ -1225,9 +1227,15 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     int nv = nrefl < 1 ? 1 : nrefl > NRT_MAX_INT ? NRT_MAX_INT : nrefl;
     P.nv_max = nv;
     const size_t smem = ((sizeof(Smem) + 15) & ~size_t(15)) + (size_t)nv * kCapS * 6 * sizeof(float);
-    NRT_CUDA(cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    NRT_CUDA(cudaFuncSetAttribute(k_refine, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     const int64_t n_mine = n > d->rank ? (n - d->rank + d->world - 1) / d->world : 0;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+    // latency regime: fewer paths than ~8 rounds of the throughput grid
+    const bool latency = getenv("NRT_REFINE_MINB") ? atoi(getenv("NRT_REFINE_MINB")) == 2
+                                                   : n_mine < (int64_t)sms * 3 * 8;
+    void (*kern)(RP) = latency ? k_refine<2> : k_refine<3>;
+    NRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     float* d_rx = nullptr;
     const size_t nrx = coarse->rx.size();
     NRT_CUDA(cudaMallocAsync(&d_rx, (nrx ? nrx : 3) * sizeof(float), st));
@@ -1249,11 +1257,9 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
         NRT_CUDA(cudaMemcpyToSymbolAsync(g_dbg, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st));
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine, 32 * NW, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NW, smem);
     if (per_sm < 1) per_sm = 1;
     if (d->blocks_per_sm > 0 && d->blocks_per_sm < per_sm) per_sm = d->blocks_per_sm;
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
     int64_t blocks = (int64_t)sms * per_sm;
     if (blocks > n_mine) blocks = n_mine;
     if (blocks < 1) blocks = 1;
@@ -1262,7 +1268,7 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
     if (n_mine > 0) {
-        k_refine<<<(unsigned)blocks, 32 * NW, smem, st>>>(P);
+        kern<<<(unsigned)blocks, 32 * NW, smem, st>>>(P);
         ::nrt::count_launch();
     }
     cudaEventRecord(e1, st);
