@@ -282,13 +282,16 @@ def main():
     refine_on = os.environ.get("NRT_BENCH_REFINE", "1") == "1"
     R = Runner(N, case, world, rank, stream, refine_on)
 
-    for _ in range(args.warmup):
+    # the L2-flush buffer exists before the warm-up, so that the memory pools are in their
+    # steady state when the timed steps start
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    for k in range(args.warmup):
+        flush.fill_(float(k))
         R.step()
     torch.cuda.synchronize()
     cnt = R.step(counters=1)  # instrumented (untimed): algorithmic byte counts
     torch.cuda.synchronize()
 
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     outs = []
