@@ -148,8 +148,9 @@ __device__ __forceinline__ int compact3(uint64_t x) {
     return (int)x;
 }
 
+template <class K>  // Morton keys: 32 bits when 3 x bits-per-axis <= 32, else 64
 __global__ void k_emit(Grid g, const float4* sp, const float4* sn, int64_t n,
-                       const unsigned int* off, uint64_t* keys, unsigned int* vals) {
+                       const unsigned int* off, K* keys, unsigned int* vals) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int lo[3], hi[3];
@@ -158,13 +159,14 @@ __global__ void k_emit(Grid g, const float4* sp, const float4* sn, int64_t n,
     for (int z = lo[2]; z <= hi[2]; ++z)
         for (int y = lo[1]; y <= hi[1]; ++y)
             for (int x = lo[0]; x <= hi[0]; ++x) {
-                keys[k] = morton3(x, y, z);
+                keys[k] = (K)morton3(x, y, z);
                 vals[k] = (unsigned)i;
                 ++k;
             }
 }
 
-__global__ void k_records(Grid g, const uint64_t* keys, const unsigned int* ids, int64_t nref,
+template <class K>
+__global__ void k_records(Grid g, const K* keys, const unsigned int* ids, int64_t nref,
                           const float4* sp, const float4* sn, float4* rec, uint2* cell) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nref) return;
@@ -172,7 +174,7 @@ __global__ void k_records(Grid g, const uint64_t* keys, const unsigned int* ids,
     float4 p = sp[id], nv = sn[id];
     rec[2 * k] = make_float4(p.x, p.y, p.z, p.w);  // record carries r; the test squares it as the definition does
     rec[2 * k + 1] = make_float4(nv.x, nv.y, nv.z, __uint_as_float(id));
-    uint64_t key = keys[k];
+    const uint64_t key = (uint64_t)keys[k];
     bool first = (k == 0) || keys[k - 1] != key;
     bool last = (k == nref - 1) || keys[k + 1] != key;
     if (first || last) {
@@ -252,6 +254,43 @@ nrt_status dmalloc(T** p, size_t count, cudaStream_t st) {
 }
 
 }  // namespace
+
+// (cell key, surfel id) pairs -> radix sort -> records + cell table.  Keys are 32-bit when the
+// Morton code fits (3 x bits <= 32: grids up to 1024 cells per axis), halving the key traffic
+// of the sort; the order (and hence every record) is the same either way.
+template <class K>
+static nrt_status sort_records(const Grid& g, nrt_scene S, int64_t n, const unsigned* off, int64_t nref,
+                               int64_t ncell, int bits, cudaStream_t st) {
+    const unsigned nb = (unsigned)((n + 255) / 256);
+    K *k0 = nullptr, *k1 = nullptr;
+    unsigned int *v0 = nullptr, *v1 = nullptr;
+    NRT_TRY(dmalloc(&k0, nref, st));
+    NRT_TRY(dmalloc(&k1, nref, st));
+    NRT_TRY(dmalloc(&v0, nref, st));
+    NRT_TRY(dmalloc(&v1, nref, st));
+    k_emit<K><<<nb, 256, 0, st>>>(g, S->sp, S->sn, n, off, k0, v0); ::nrt::count_launch();
+    NRT_CUDA(cudaGetLastError());
+    cub::DoubleBuffer<K> kb(k0, k1);
+    cub::DoubleBuffer<unsigned int> vb(v0, v1);
+    size_t tb = 0;
+    void* tmp = nullptr;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, (int)nref, 0, 3 * bits, st);
+    NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+    cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, (int)nref, 0, 3 * bits, st);
+    cudaFreeAsync(tmp, st);
+    NRT_TRY(dmalloc(&S->rec, 2 * nref, st));
+    NRT_TRY(dmalloc(&S->cell, ncell, st));
+    NRT_CUDA(cudaMemsetAsync(S->cell, 0, ncell * sizeof(uint2), st));
+    k_records<K><<<(unsigned)((nref + 255) / 256), 256, 0, st>>>(g, kb.Current(), vb.Current(), nref,
+                                                                S->sp, S->sn, S->rec, S->cell);
+    ::nrt::count_launch();
+    NRT_CUDA(cudaGetLastError());
+    cudaFreeAsync(k0, st);
+    cudaFreeAsync(k1, st);
+    cudaFreeAsync(v0, st);
+    cudaFreeAsync(v1, st);
+    return NRT_OK;
+}
 
 static nrt_status build_impl(const nrt_scene_desc* D, nrt_scene S, cudaStream_t st) {
     const int64_t n = D->n;
@@ -391,36 +430,14 @@ static nrt_status build_impl(const nrt_scene_desc* D, nrt_scene S, cudaStream_t 
     const int64_t nref = nref32;
     S->nref = nref;
     // ---- pairs, sort
-    uint64_t *k0 = nullptr, *k1 = nullptr;
-    unsigned int *v0 = nullptr, *v1 = nullptr;
-    NRT_TRY(dmalloc(&k0, nref, st));
-    NRT_TRY(dmalloc(&k1, nref, st));
-    NRT_TRY(dmalloc(&v0, nref, st));
-    NRT_TRY(dmalloc(&v1, nref, st));
-    k_emit<<<nb, 256, 0, st>>>(g, S->sp, S->sn, n, off, k0, v0); ::nrt::count_launch();
-    NRT_CUDA(cudaGetLastError());
-    int maxd = dims[0] > dims[1] ? dims[0] : dims[1];
-    maxd = maxd > dims[2] ? maxd : dims[2];
-    int bits = 1;
-    while ((1 << bits) < maxd) ++bits;
-    cub::DoubleBuffer<uint64_t> kb(k0, k1);
-    cub::DoubleBuffer<unsigned int> vb(v0, v1);
-    tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, (int)nref, 0, 3 * bits, st);
-    NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
-    cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, (int)nref, 0, 3 * bits, st);
-    cudaFreeAsync(tmp, st);
-    // ---- records + cell table
-    NRT_TRY(dmalloc(&S->rec, 2 * nref, st));
-    NRT_TRY(dmalloc(&S->cell, ncell, st));
-    NRT_CUDA(cudaMemsetAsync(S->cell, 0, ncell * sizeof(uint2), st));
-    k_records<<<(unsigned)((nref + 255) / 256), 256, 0, st>>>(g, kb.Current(), vb.Current(), nref,
-                                                             S->sp, S->sn, S->rec, S->cell); ::nrt::count_launch();
-    NRT_CUDA(cudaGetLastError());
-    cudaFreeAsync(k0, st);
-    cudaFreeAsync(k1, st);
-    cudaFreeAsync(v0, st);
-    cudaFreeAsync(v1, st);
+    {
+        int maxd = dims[0] > dims[1] ? dims[0] : dims[1];
+        maxd = maxd > dims[2] ? maxd : dims[2];
+        int bits = 1;
+        while ((1 << bits) < maxd) ++bits;
+        NRT_TRY(3 * bits <= 32 ? sort_records<uint32_t>(g, S, n, off, nref, ncell, bits, st)
+                               : sort_records<uint64_t>(g, S, n, off, nref, ncell, bits, st));
+    }
     cudaFreeAsync(cnt, st);
     cudaFreeAsync(off, st);
     // ---- empty-space skip field (the paper's "march distance", P:154 / P:281): Chebyshev
