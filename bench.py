@@ -204,7 +204,13 @@ def cpu_baseline(case, seconds=15.0):
         res = pool.map(_oracle_chunk, [(case, sample[k::P]) for k in range(P)])
     wall = time.perf_counter() - t0
     bounces = sum(r for r in res)
+    # the single-threaded oracle on one core (SURVEY §8(d) asks for both rates)
+    one = sample[:: max(1, len(sample) // max(1, int(3.0 / per_ray)))][: max(1, int(3.0 / per_ray))]
+    t1 = time.perf_counter()
+    nb1 = _oracle_chunk((case, one))
+    one_core = nb1 / max(1e-9, time.perf_counter() - t1)
     return {"value": bounces / wall, "unit": UNIT, "cores": P, "kind": "oracle",
+            "value_1core": one_core,
             "sample": f"{len(sample)} primary rays of {case.name} (evenly spaced lattice ids, "
                       f"brute force over {case.scene.n} surfels, no fans), {wall:.1f} s wall on "
                       f"{P} processes"}
