@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnrt.so")
-SOURCES = ["api.cu", "scene.cu", "launch.cu", "dedupe.cu", "refine.cu", "post.cu"]
+SOURCES = ["api.cu", "scene.cu", "launch.cu", "dedupe.cu", "refine.cu", "refine_nw12.cu", "post.cu"]
 COMMON = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -23,7 +23,7 @@ COMMON = [
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
     "-Xptxas", "-v",
 ]
-FMAD = {"refine.cu": "-fmad=true"}  # default -fmad=false (R3: no FMA contraction on the parity path)
+FMAD = {"refine.cu": "-fmad=true", "refine_nw12.cu": "-fmad=true"}  # default -fmad=false (R3: no FMA contraction on the parity path)
 if os.environ.get("NRT_REFINE_FMAD") == "0":  # A/B switch
     FMAD = {}
 NVCC_FLAGS = COMMON + ["-fmad=false", "--shared"]  # (kept for reference: the single-command form)
@@ -34,7 +34,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     `defines` (e.g. ["NRT_TRACE_MINB=8"]) are tuning variants for experiments."""
     lib = out or LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "internal.cuh"), os.path.join(ROOT, "include", "nrt.h"),
+    deps = srcs + [os.path.join(CSRC, "internal.cuh"), os.path.join(CSRC, "refine.cu"), os.path.join(ROOT, "include", "nrt.h"),
                    os.path.abspath(__file__)]
     if not force and os.path.exists(lib):
         mt = os.path.getmtime(lib)

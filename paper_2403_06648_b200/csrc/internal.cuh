@@ -218,4 +218,6 @@ float cRw_of(float c_R, int64_t n_rays);
 // refine.cu
 nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
                   cudaStream_t st);
+nrt_status refine_nw12(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
+                       cudaStream_t st);  // refine_nw12.cu: 12 warps/path
 }  // namespace nrt

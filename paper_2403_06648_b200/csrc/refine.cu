@@ -624,6 +624,9 @@ __device__ bool supported(const RP& P, int32_t label, const double x[3], int lan
 // the throughput regime (many paths: C4/C5), MINB = 2 (128 registers, no spills) the latency
 // regime (few paths, a tail of long GN runs: C2).  Measured: C2 refine -4.6 % with 2,
 // C4 +12 % with 2.  refine() picks by the number of paths.
+#ifndef NRT_LAT_MINB
+#define NRT_LAT_MINB 2  // resident blocks per SM in the latency regime
+#endif
 template <int MINB>
 __global__ void __launch_bounds__(32 * NW, MINB) k_refine(RP P) {
     extern __shared__ __align__(16) unsigned char dyn[];
@@ -1131,8 +1134,21 @@ __global__ void k_select_flags(const nrt_coarse_rec* in, int64_t n, int sel, uns
 
 }  // namespace
 
-nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
-                  cudaStream_t st) {
+#ifndef NRT_REFINE_ENTRY
+#define NRT_REFINE_ENTRY refine
+#endif
+nrt_status NRT_REFINE_ENTRY(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
+                            cudaStream_t st) {
+#if NRT_REFINE_WARPS == 8
+    {  // latency regime (few paths, set by a tail of long GN runs): the 12-warp build of this
+       // file (refine_nw12.cu) — per-path results do not depend on the warp count
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+        const int64_t mine = coarse->n / (d->world > 0 ? d->world : 1);
+        const char* e = getenv("NRT_REFINE_NW12");
+        if (e ? atoi(e) != 0 : mine < (int64_t)sms * 3 * 8) return refine_nw12(s, coarse, d, out, st);
+    }
+#endif
     int64_t n = coarse->n;
     out->n = 0;
     const nrt_coarse_rec* in = (const nrt_coarse_rec*)coarse->d_rec;
@@ -1231,9 +1247,18 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
     // latency regime: fewer paths than ~8 rounds of the throughput grid
+#if NRT_REFINE_WARPS == 8
     const bool latency = getenv("NRT_REFINE_MINB") ? atoi(getenv("NRT_REFINE_MINB")) == 2
                                                    : n_mine < (int64_t)sms * 3 * 8;
-    void (*kern)(RP) = latency ? k_refine<2> : k_refine<3>;
+#else
+    const bool latency = true;  // the wide build serves the latency regime only
+#endif
+#if NRT_REFINE_WARPS == 8
+    void (*kern)(RP) = latency ? k_refine<NRT_LAT_MINB> : k_refine<3>;
+#else
+    void (*kern)(RP) = k_refine<NRT_LAT_MINB>;
+    (void)latency;
+#endif
     NRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     NRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     float* d_rx = nullptr;
