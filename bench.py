@@ -223,6 +223,17 @@ def _oracle_chunk(args):
     return nb
 
 
+def run_config(case, world):
+    """The `config` object of both arms' JSON lines (same workload description)."""
+    return {"workload": f"{case.name}: {case.scene.name}, 1 TX/{len(case.rx)} RX, "
+                        f"{case.n_rays} rays per GPU, max_refl {case.max_refl}, "
+                        f"max_diff {case.max_diff}; step = scene build + launch + refine",
+            "voxel_m": case.voxel, "n_rays_total": case.n_rays * world,
+            "l2": "512 MiB write between steps (outside the timed events)",
+            "parallelism": f"dp{world}: rays i == rank mod {world}, paths j == rank mod "
+                           f"{world}, NCCL all-gather of events/coarse/refined records"}
+
+
 def run_reference(args, case):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -249,7 +260,8 @@ def run_reference(args, case):
             "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": case.name, "sample": f"{rays_per_step} primary rays per step"},
+            "config": dict(run_config(case, world),
+                           sample=f"oracle: {rays_per_step} primary rays of the lattice per step"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "oracle",
                              "sample": f"{rays_per_step} primary rays per step of {case.name}, "
                                        f"brute force over {case.scene.n} surfels"},
@@ -371,13 +383,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{case.name}: {case.scene.name}, 1 TX/{len(case.rx)} RX, "
-                               f"{case.n_rays} rays per GPU, max_refl {case.max_refl}, "
-                               f"max_diff {case.max_diff}; step = scene build + launch + refine",
-                   "voxel_m": case.voxel, "n_rays_total": case.n_rays * world,
-                   "l2": "512 MiB write between steps (outside the timed events)",
-                   "parallelism": f"dp{world}: rays i == rank mod {world}, paths j == rank mod "
-                                  f"{world}, NCCL all-gather of events/coarse/refined records"},
+        "config": run_config(case, world),
         # refined paths/s: coarse paths refined (the refinement's input rate, as the paper's
         # Table IV refine times count) per second of the whole step, and of the refine kernel
         "refined_paths_per_s": (outs[-1]["coarse"] * args.steps / (total_ms / 1000.0))
