@@ -116,6 +116,22 @@ def test_c4_full_size_sampled_refined_parity(N, O):
     compare(got, ref, 0.25, "C4 sample")
 
 
+def test_c5_full_size_sampled_refined_parity(N, O):
+    """Full C5 (1e7 surfels, 879 RX, 1e8-ray lattice; refinement of its coarse set in the
+    throughput regime): the oracle re-refines sampled paths one by one."""
+    case = G.case("C5")
+    sc = N.build_case_scene(case)
+    coarse = N.launch_case(sc, case)
+    cr = coarse.export()
+    allg = refine_gpu(N, case, sc, coarse)
+    rng = np.random.default_rng(6)
+    ok = np.nonzero(allg["status"] == 0)[0]
+    idx = np.sort(np.concatenate([rng.choice(ok, 5, replace=False),
+                                  rng.choice(len(cr), 2, replace=False)]))
+    ref = O.refine(case, cr[idx])
+    compare(allg[idx], ref, 0.3, "C5 sample")
+
+
 def test_refine_sharding_union(N):
     case = G.case("C2s", sigma=0.0, n=20_000, n_rays=8000, max_diff=0)
     sc = N.build_case_scene(case)
