@@ -124,9 +124,11 @@ void or_reflect(const float d[3], const float n[3], float out[3]) {
     out[2] = x[2] / l;
 }
 
-/* C.1 step 2(a): global lexicographic argmin over all surfels of (t, id) (R9). */
+/* C.1 step 2(a): global lexicographic argmin over all surfels of (t, id) (R9).  Tier 0 is
+ * this loop; with S->grid set the tier-1 grid (grid.c) computes the same minimum. */
 int64_t or_nearest(const or_scene* S, const float o[3], const float d[3], const float* lam,
                    int n_lam, int64_t prev, float tau, float cos_ex, float* t_hit) {
+    if (S->grid) return or_grid_nearest(S, S->grid, o, d, lam, n_lam, prev, tau, cos_ex, t_hit);
     int64_t best = -1;
     float bt = INFINITY;
     for (int64_t i = 0; i < S->n; ++i) {

@@ -30,6 +30,8 @@ typedef struct {
     int32_t label;      /* unique edge label */
 } or_edge;
 
+typedef struct or_grid or_grid;  /* tier-1 uniform grid (grid.c); NULL = brute force */
+
 typedef struct {
     const float* p;        /* n x 3 positions */
     const float* nrm;      /* n x 3 normals (as given) */
@@ -38,6 +40,7 @@ typedef struct {
     int64_t n;
     const or_edge* edges;
     int32_t n_edges;
+    const or_grid* grid;   /* optional tier-1 grid: same argmin, faster */
 } or_scene;
 
 typedef struct {
@@ -105,6 +108,15 @@ void or_reflect(const float d[3], const float n[3], float out[3]);
 int64_t or_nearest(const or_scene* S, const float o[3], const float d[3], const float* lam,
                    int n_lam, int64_t prev, float tau, float cos_ex, float* t_hit);
 
+/* tier 1 (grid.c): independent uniform grid of cell size `voxel`, origin shifted by `shift`
+ * (may be NULL); or_nearest uses it when S->grid is set.  Pinned to tier 0 bit for bit. */
+or_grid* or_grid_build(const or_scene* S, double voxel, const double shift[3]);
+void or_grid_free(or_grid* G);
+void or_grid_info(const or_grid* G, int64_t dims[3], int64_t* n_refs, double* pad);
+int64_t or_grid_nearest(const or_scene* S, const or_grid* G, const float o[3], const float d[3],
+                        const float* lam, int n_lam, int64_t prev, float tau, float cos_ex,
+                        float* t_hit);
+
 /* R13 closest approach of ray (o,d) to edge E; 0 if parallel */
 int or_edge_closest(const float o[3], const float d[3], const or_edge* E, float* te, float* s,
                     float* dist2);
@@ -170,6 +182,9 @@ typedef struct {
 /* refine every coarse record (out[q] for in[q], no dedupe; status per path) */
 int or_refine(const or_scene* S, const or_refine_params* R, const or_coarse* in, int64_t n,
               or_refined* out);
+/* 1 (default): or_refine finds MLS neighbourhoods through a cell index (same ids, same
+ * order, bitwise the same sums); 0: the plain label-list loop (pin tests compare both) */
+void or_refine_set_grid(int on);
 /* residual of record c at its seed (z_in NULL) or at z_in; returns dim or -1 (pin helper) */
 int or_path_residual(const or_scene* S, const or_refine_params* R, const or_coarse* c,
                      const double* z_in, double* r_out, double* z_out);

@@ -13,7 +13,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SRCS = ["coarse.c", "refine.c", "post.c"]
+_SRCS = ["coarse.c", "grid.c", "refine.c", "post.c"]
 
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
           "-Wall", "-Wno-unused-function"]
@@ -55,7 +55,8 @@ class _Edge(C.Structure):
 
 class _Scene(C.Structure):
     _fields_ = [("p", C.c_void_p), ("nrm", C.c_void_p), ("r", C.c_void_p), ("label", C.c_void_p),
-                ("n", C.c_int64), ("edges", C.c_void_p), ("n_edges", C.c_int32)]
+                ("n", C.c_int64), ("edges", C.c_void_p), ("n_edges", C.c_int32),
+                ("grid", C.c_void_p)]
 
 
 class _Params(C.Structure):
@@ -106,6 +107,11 @@ def lib():
                                       C.POINTER(C.c_float), C.POINTER(C.c_float),
                                       C.POINTER(C.c_float)]
         L.or_fan_dirs.argtypes = [C.POINTER(_Edge), C.c_void_p, C.c_float, C.c_void_p, C.c_int]
+        L.or_grid_build.argtypes = [C.POINTER(_Scene), C.c_double, C.c_void_p]
+        L.or_grid_build.restype = C.c_void_p
+        L.or_grid_free.argtypes = [C.c_void_p]
+        L.or_grid_info.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -118,9 +124,11 @@ def _f32(a, shape=None):
 
 
 class OracleScene:
-    """Keeps the numpy arrays alive and the C view of them."""
+    """Keeps the numpy arrays alive and the C view of them.  grid_voxel (m) attaches the
+    tier-1 uniform grid (grid.c: the same argmin as the brute force, pinned to it bit for bit);
+    shift (3,) moves the grid origin (invariance pins)."""
 
-    def __init__(self, scene):
+    def __init__(self, scene, grid_voxel=None, shift=None):
         self.p = _f32(scene.points, (-1, 3))
         self.nrm = _f32(scene.normals, (-1, 3))
         self.r = _f32(scene.radii, (-1,))
@@ -139,7 +147,25 @@ class OracleScene:
             e.label = int(E.label[j])
         self.c = _Scene(self.p.ctypes.data, self.nrm.ctypes.data, self.r.ctypes.data,
                         self.label.ctypes.data, self.p.shape[0],
-                        C.cast(self.edges, C.c_void_p), self.n_edges)
+                        C.cast(self.edges, C.c_void_p), self.n_edges, None)
+        self.grid = None
+        if grid_voxel is not None:
+            sh = np.ascontiguousarray(np.zeros(3) if shift is None else shift, np.float64)
+            self.grid = lib().or_grid_build(C.byref(self.c), float(grid_voxel), sh.ctypes.data)
+            self.c.grid = self.grid
+
+    def grid_info(self):
+        dims = np.zeros(3, np.int64)
+        n, pad = C.c_int64(), C.c_double()
+        lib().or_grid_info(self.grid, dims.ctypes.data, C.byref(n), C.byref(pad))
+        return {"dims": dims.tolist(), "n_refs": n.value, "pad": pad.value}
+
+    def __del__(self):
+        try:
+            if self.grid:
+                lib().or_grid_free(self.grid)
+        except Exception:
+            pass
 
 
 def _params(case, rx=None, max_diff=None):
@@ -228,7 +254,7 @@ _FORK = {}
 def _primary_worker(args):
     rank, world = args
     case, max_diff = _FORK["case"], _FORK["max_diff"]
-    sc = OracleScene(case.scene)
+    sc = _FORK.get("scene") or OracleScene(case.scene)
     p, rxa = _params(case, max_diff=max_diff)
     p.rank, p.world = rank, world
     rc, ec = 1 << 16, 1 << 16
@@ -246,7 +272,7 @@ def _primary_worker(args):
 def _fan_worker(args):
     part, parts = args
     case, max_diff, ev = _FORK["case"], _FORK["max_diff"], _FORK["events"]
-    sc = OracleScene(case.scene)
+    sc = _FORK.get("scene") or OracleScene(case.scene)
     p, rxa = _params(case, max_diff=max_diff)
     rc = 1 << 16
     while True:
@@ -259,19 +285,41 @@ def _fan_worker(args):
         rc = nr.value
 
 
+def trace_primary(case, rank=0, world=1, scene: OracleScene | None = None):
+    """or_trace_primary of lattice rays i == rank (mod world): raw records, raw events,
+    bounces (no fans, no dedupe)."""
+    sc = scene or OracleScene(case.scene)
+    p, rxa = _params(case)
+    p.rank, p.world = int(rank), int(world)
+    rc, ec = 1 << 12, 1 << 12
+    while True:
+        raw = np.zeros(rc, COARSE_DTYPE)
+        ev = np.zeros(ec, EVENT_DTYPE)
+        nr, ne, nb = C.c_int64(), C.c_int64(), C.c_uint64()
+        lib().or_trace_primary(C.byref(sc.c), C.byref(p), raw.ctypes.data, rc, C.byref(nr),
+                               ev.ctypes.data, ec, C.byref(ne), C.byref(nb))
+        if nr.value <= rc and ne.value <= ec:
+            return raw[:nr.value].copy(), ev[:ne.value].copy(), int(nb.value)
+        rc, ec = max(rc, nr.value), max(ec, ne.value)
+
+
 def event_dedupe(ev):
     a = np.ascontiguousarray(ev.copy())
     m = lib().or_event_dedupe(a.ctypes.data, a.shape[0])
     return a[:m].copy()
 
 
-def launch_phased(case, procs=1, max_diff=None, return_events=False):
+def launch_phased(case, procs=1, max_diff=None, return_events=False, grid_voxel=None,
+                  scene=None):
     """The same coarse operation run in phases over `procs` forked single-threaded
     processes (ray shards, then event shards); the merged set is identical (per-ray
-    results are independent; the event set is global).  Returns (records, n_raw, bounces)."""
+    results are independent; the event set is global).  Returns (records, n_raw, bounces).
+    grid_voxel: trace with the tier-1 grid (built once here, shared by the forked workers)."""
     import multiprocessing as mp
     lib()
     _FORK["case"], _FORK["max_diff"] = case, max_diff
+    _FORK["scene"] = scene if scene is not None else (
+        OracleScene(case.scene, grid_voxel=grid_voxel) if grid_voxel is not None else None)
     ctx = mp.get_context("fork")
     if procs > 1:
         with ctx.Pool(procs) as pool:
@@ -291,6 +339,7 @@ def launch_phased(case, procs=1, max_diff=None, return_events=False):
         raw = np.concatenate([raw] + [x[0] for x in fparts])
         nb += sum(x[1] for x in fparts)
     recs = dedupe(raw, case.kappa)
+    _FORK.pop("scene", None)
     if return_events:
         return recs, raw.shape[0], nb, ev
     return recs, raw.shape[0], nb
@@ -407,12 +456,40 @@ def refine(case, coarse, scene: OracleScene | None = None, **over):
                                 C.c_void_p]
         L.or_mls.argtypes = [C.POINTER(_Scene), C.POINTER(_RefParams), C.c_int32, C.c_void_p,
                              C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
+        L.or_refine_set_grid.argtypes = [C.c_int]
         L._ref_setup = True
+    grid = over.pop("grid", True)
     sc = scene or OracleScene(case.scene)
     p, rxa = _ref_params(case, **over)
     cin = np.ascontiguousarray(coarse, dtype=COARSE_DTYPE)
     out = np.zeros(cin.shape[0], REFINED_DTYPE)
+    L.or_refine_set_grid(1 if grid else 0)
     L.or_refine(C.byref(sc.c), C.byref(p), cin.ctypes.data, cin.shape[0], out.ctypes.data)
+    L.or_refine_set_grid(1)
+    return out
+
+
+def _refine_worker(args):
+    case, recs, over = args
+    return refine(case, recs, _FORK.get("rscene"), **over)
+
+
+def refine_par(case, coarse, procs=1, **over):
+    """refine() over forked single-threaded processes (paths are independent; out[q] is
+    bitwise the serial result for in[q])."""
+    import multiprocessing as mp
+    lib()
+    cin = np.ascontiguousarray(coarse, dtype=COARSE_DTYPE)
+    if procs <= 1 or len(cin) < 2:
+        return refine(case, cin, **over)
+    _FORK["rscene"] = OracleScene(case.scene)
+    chunks = [cin[k::procs] for k in range(procs)]
+    with mp.get_context("fork").Pool(procs) as pool:
+        parts = pool.map(_refine_worker, [(case, c, over) for c in chunks if len(c)])
+    _FORK.pop("rscene", None)
+    out = np.zeros(len(cin), REFINED_DTYPE)
+    for k, p in enumerate(parts):
+        out[k::procs] = p
     return out
 
 

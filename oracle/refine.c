@@ -43,7 +43,83 @@ typedef struct {
     int64_t* lab_start; /* [4097] */
     int64_t* lab_ids;   /* [n] */
     double sigma, rad2, tx[3], rx[3];
+    /* optional neighbourhood index (or_refine on large clouds): cells of edge 4 sigma, ids
+     * ascending per cell.  It only finds the candidates; the MLS sums run over exactly the
+     * label-list ids within 4 sigma, in the same ascending order (bitwise the same sums). */
+    int64_t* nb_start;  /* [ncell + 1] or NULL */
+    int64_t* nb_ids;
+    double nb_org[3], nb_cell;
+    int64_t nb_dims[3];
+    int64_t* scratch;   /* candidate ids of one query */
+    int64_t scratch_cap;
 } rctx_t;
+
+static int or_refine_use_grid = 1; /* pin tests switch it off to compare with the plain loop */
+void or_refine_set_grid(int on) { or_refine_use_grid = on; }
+
+static int cmp_i64(const void* a, const void* b) {
+    int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+    return x < y ? -1 : x > y;
+}
+
+/* the ids q of `label` with |p_q - x|^2 <= rad2, ascending (grid query); returns the count */
+static int64_t nb_query(rctx_t* C, int32_t label, const double x[3]) {
+    const or_scene* S = C->S;
+    int64_t c[3], m = 0;
+    for (int a = 0; a < 3; ++a) c[a] = (int64_t)floor((x[a] - C->nb_org[a]) / C->nb_cell);
+    for (int64_t z = c[2] - 1; z <= c[2] + 1; ++z)
+        for (int64_t y = c[1] - 1; y <= c[1] + 1; ++y)
+            for (int64_t xx = c[0] - 1; xx <= c[0] + 1; ++xx) {
+                if (xx < 0 || y < 0 || z < 0 || xx >= C->nb_dims[0] || y >= C->nb_dims[1] ||
+                    z >= C->nb_dims[2])
+                    continue;
+                int64_t cell = xx + C->nb_dims[0] * (y + C->nb_dims[1] * z);
+                for (int64_t k = C->nb_start[cell]; k < C->nb_start[cell + 1]; ++k) {
+                    int64_t i = C->nb_ids[k];
+                    if (S->label[i] != label) continue;
+                    double dd[3] = {S->p[3 * i] - x[0], S->p[3 * i + 1] - x[1], S->p[3 * i + 2] - x[2]};
+                    if ((dd[0] * dd[0] + dd[1] * dd[1]) + dd[2] * dd[2] > C->rad2) continue;
+                    if (m == C->scratch_cap) {
+                        C->scratch_cap = C->scratch_cap ? 2 * C->scratch_cap : 1024;
+                        C->scratch = (int64_t*)realloc(C->scratch, sizeof(int64_t) * (size_t)C->scratch_cap);
+                    }
+                    C->scratch[m++] = i;
+                }
+            }
+    qsort(C->scratch, (size_t)m, sizeof(int64_t), cmp_i64);
+    return m;
+}
+
+static void nb_build(rctx_t* C) {
+    const or_scene* S = C->S;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = 0; i < S->n; ++i)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = fmin(lo[a], S->p[3 * i + a]);
+            hi[a] = fmax(hi[a], S->p[3 * i + a]);
+        }
+    C->nb_cell = 4.0 * C->sigma;
+    for (int a = 0; a < 3; ++a) {
+        C->nb_org[a] = lo[a] - C->nb_cell;
+        C->nb_dims[a] = (int64_t)ceil((hi[a] - C->nb_org[a]) / C->nb_cell) + 2;
+    }
+    int64_t nc = C->nb_dims[0] * C->nb_dims[1] * C->nb_dims[2];
+    C->nb_start = (int64_t*)calloc((size_t)nc + 1, sizeof(int64_t));
+    C->nb_ids = (int64_t*)malloc(sizeof(int64_t) * (size_t)(S->n > 0 ? S->n : 1));
+    int64_t* cellof = (int64_t*)malloc(sizeof(int64_t) * (size_t)(S->n > 0 ? S->n : 1));
+    for (int64_t i = 0; i < S->n; ++i) {
+        int64_t c[3];
+        for (int a = 0; a < 3; ++a) c[a] = (int64_t)floor((S->p[3 * i + a] - C->nb_org[a]) / C->nb_cell);
+        cellof[i] = c[0] + C->nb_dims[0] * (c[1] + C->nb_dims[1] * c[2]);
+        C->nb_start[cellof[i] + 1]++;
+    }
+    for (int64_t c = 0; c < nc; ++c) C->nb_start[c + 1] += C->nb_start[c];
+    int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (size_t)nc);
+    memcpy(fill, C->nb_start, sizeof(int64_t) * (size_t)nc);
+    for (int64_t i = 0; i < S->n; ++i) C->nb_ids[fill[cellof[i]]++] = i;
+    free(fill);
+    free(cellof);
+}
 
 static double dot(const double a[3], const double b[3]) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
 static double norm(const double a[3]) { return sqrt(dot(a, a)); }
@@ -58,8 +134,14 @@ static int mls(const rctx_t* C, int32_t label, const double nseed[3], const doub
                double pbar[3], double nbar[3]) {
     const or_scene* S = C->S;
     double W = 0, P[3] = {0, 0, 0}, Nn[3] = {0, 0, 0};
-    for (int64_t q = C->lab_start[label]; q < C->lab_start[label + 1]; ++q) {
-        int64_t i = C->lab_ids[q];
+    const int64_t* ids = C->lab_ids + C->lab_start[label];
+    int64_t cnt = C->lab_start[label + 1] - C->lab_start[label];
+    if (C->nb_start) {
+        cnt = nb_query((rctx_t*)C, label, x);
+        ids = C->scratch;
+    }
+    for (int64_t q = 0; q < cnt; ++q) {
+        int64_t i = ids[q];
         double p[3] = {S->p[3 * i], S->p[3 * i + 1], S->p[3 * i + 2]};
         double dd[3] = {p[0] - x[0], p[1] - x[1], p[2] - x[2]};
         double d2 = dot(dd, dd);
@@ -474,12 +556,16 @@ int or_refine(const or_scene* S, const or_refine_params* R, const or_coarse* in,
         C.lab_ids[C.lab_start[l] + fill[l]++] = i;
     }
     free(fill);
+    if (or_refine_use_grid && n > 0 && S->n > 0) nb_build(&C);
     for (int64_t q = 0; q < n; ++q) {
         for (int a = 0; a < 3; ++a) C.rx[a] = R->rx[3 * (int64_t)in[q].rx + a];
         refine_one(&C, &in[q], &out[q]);
     }
     free(C.lab_start);
     free(C.lab_ids);
+    free(C.nb_start);
+    free(C.nb_ids);
+    free(C.scratch);
     return 0;
 }
 

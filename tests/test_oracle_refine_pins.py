@@ -245,3 +245,56 @@ def test_reciprocity_box_room(O):
         if n:
             assert np.abs(r["v"][:n] - s["v"][:n][::-1]).max() < 1e-9
         assert abs(r["delay"] - s["delay"]) < 1e-15
+
+
+# ---------------------------------------------------------------- R27 angles ------------
+def _angles(r):
+    return (float(r["aod_az"]), float(r["aod_el"]), float(r["aoa_az"]), float(r["aoa_el"]))
+
+
+def _close_deg(a, b, tol=1e-4):
+    """angle tuples equal within tol degrees; azimuths compared on the circle (+-180 alike)"""
+    d = np.abs(np.asarray(a, float) - np.asarray(b, float))
+    d = np.minimum(d, 360.0 - d)
+    return bool(np.all(d <= tol))
+
+
+def test_angles_closed_form_reflection(O):
+    """R27: azimuth = atan2(y, x) about +z, elevation = asin(z); AoD along the
+    first segment, AoA from the RX toward the last vertex; incidence = angle to the normal.
+    Floor z = 0, TX (0,0,1), RX (2,0,1): vertex (1,0,0), AoD (0, -45), AoA (180, -45), 45 deg;
+    the same turned by 90 deg about z: AoD (90, -45), AoA (-90, -45)."""
+    sc = plane_scene([(0.0, 1.0)], extent=((-1.0, 3.0), (-1.0, 3.0)), h=0.02, r=0.02)
+    for tx, rx, v, expect in (((0, 0, 1), (2, 0, 1), (1, 0, 0), (0.0, -45.0, 180.0, -45.0)),
+                              ((0, 0, 1), (0, 2, 1), (0, 1, 0), (90.0, -45.0, -90.0, -45.0)),
+                              ((0, 0, 1), (1, 1, 2), (1 / 3, 1 / 3, 0),
+                               (45.0, -math.degrees(math.atan2(1, math.sqrt(2) / 3)), -135.0,
+                                -math.degrees(math.atan2(2, 2 * math.sqrt(2) / 3))))):
+        case = make_case(sc, tx, rx)
+        seed = (v[0] + 0.02, v[1] - 0.01, 0.0)
+        c = coarse_rec(O, [seed], [0], [nearest_id(sc, seed, 0)])
+        r = O.refine(case, c)[0]
+        assert O.STATUS[int(r["status"])] == "OK"
+        assert np.allclose(r["v"][0], v, atol=1e-9)
+        assert _close_deg(_angles(r), expect), (_angles(r), expect)
+        inc = math.degrees(math.acos(tx[2] / math.dist(tx, v)))
+        assert abs(float(r["inc"][0]) - inc) < 1e-4
+
+
+def test_angles_los_and_diffraction(O):
+    """LOS: AoD points TX -> RX, AoA RX -> TX.  Diffraction on the z-axis edge, TX (1,0,0), RX
+    (0,1,2): vertex (0,0,1); the incidence angle is the Keller cone angle to the edge, 45 deg;
+    AoD az 180, el 45; AoA from RX (0,1,2) toward (0,0,1): az -90, el -45."""
+    g = GOLD["edge_example"]
+    case = edge_case(O, g["tx"], g["rx"], g["a"], g["b"])
+    los = np.zeros(1, O.COARSE_DTYPE)
+    r = O.refine(case, los)[0]
+    d = np.array(g["rx"], float) - g["tx"]
+    az = math.degrees(math.atan2(d[1], d[0]))
+    el = math.degrees(math.asin(d[2] / np.linalg.norm(d)))
+    assert _close_deg(_angles(r), (az, el, math.degrees(math.atan2(-d[1], -d[0])), -el))
+    c = coarse_rec(O, [(0.0, 0.0, 0.7)], [100], [0], kinds=1)
+    r = O.refine(case, c)[0]
+    assert O.STATUS[int(r["status"])] == "OK"
+    assert _close_deg(_angles(r), (180.0, 45.0, -90.0, -45.0))
+    assert abs(float(r["inc"][0]) - 45.0) < 1e-4
