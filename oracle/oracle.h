@@ -162,6 +162,7 @@ typedef struct {
     double theta_ex_deg;   /* sheet angle for the shadow rays */
     float tx[3];
     const float* rx;       /* RX table indexed by the record's rx */
+    int32_t jac_fd;        /* 0: analytic Jacobian (R37, default); 1: central differences */
 } or_refine_params;
 
 typedef struct {
@@ -188,6 +189,10 @@ void or_refine_set_grid(int on);
 /* residual of record c at its seed (z_in NULL) or at z_in; returns dim or -1 (pin helper) */
 int or_path_residual(const or_scene* S, const or_refine_params* R, const or_coarse* c,
                      const double* z_in, double* r_out, double* z_out);
+/* Jacobian dr/dz (m x m, row-major) of record c at its seed (z_in NULL) or at z_in, analytic
+ * (fd = 0) or by central differences with step h (fd = 1); returns dim or -1 (pin helper) */
+int or_path_jacobian(const or_scene* S, const or_refine_params* R, const or_coarse* c,
+                     const double* z_in, int fd, double h, double* J_out);
 /* Eqs. 1-4 at x over the label's surfels within 4 sigma (pin helper); 0 if empty */
 int or_mls(const or_scene* S, const or_refine_params* R, int32_t label, const double nseed[3],
            const double x[3], double pbar[3], double nbar[3], double* f);

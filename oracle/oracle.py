@@ -429,7 +429,7 @@ class _RefParams(C.Structure):
     _fields_ = [("xi", C.c_double), ("r_s", C.c_double), ("tol_m", C.c_double),
                 ("max_iter", C.c_int32), ("alpha", C.c_double), ("beta", C.c_double),
                 ("tau", C.c_double), ("theta_ex_deg", C.c_double), ("tx", C.c_float * 3),
-                ("rx", C.c_void_p)]
+                ("rx", C.c_void_p), ("jac_fd", C.c_int32)]
 
 
 def _ref_params(case, rx=None, **over):
@@ -445,7 +445,30 @@ def _ref_params(case, rx=None, **over):
     p.theta_ex_deg = float(over.get("theta_ex_deg", case.theta_ex_deg))
     p.tx[:] = [float(x) for x in np.asarray(case.tx, np.float32)]
     p.rx = rxa.ctypes.data
+    p.jac_fd = int(over.get("jac_fd", 0))
     return p, rxa
+
+
+def path_jacobian(case, rec, z=None, fd=False, h=1e-7, scene: OracleScene | None = None, **over):
+    """Jacobian dr/dz of one coarse record's residual (pin helper): analytic (R37) or by central
+    differences with step h -> (J m x m) or None."""
+    refine(case, np.zeros(0, COARSE_DTYPE), scene)
+    L = lib()
+    if not hasattr(L, "_jac_setup"):
+        L.or_path_jacobian.argtypes = [C.POINTER(_Scene), C.POINTER(_RefParams), C.c_void_p,
+                                       C.c_void_p, C.c_int, C.c_double, C.c_void_p]
+        L._jac_setup = True
+    sc = scene or OracleScene(case.scene)
+    p, rxa = _ref_params(case, **over)
+    c = np.ascontiguousarray(np.asarray(rec, dtype=COARSE_DTYPE).reshape(1))
+    J = np.zeros(24 * 24)
+    zin = None if z is None else np.ascontiguousarray(z, np.float64)
+    m = L.or_path_jacobian(C.byref(sc.c), C.byref(p), c.ctypes.data,
+                           None if zin is None else zin.ctypes.data, int(bool(fd)), float(h),
+                           J.ctypes.data)
+    if m < 0:
+        return None
+    return J[: m * m].reshape(m, m).copy()
 
 
 def refine(case, coarse, scene: OracleScene | None = None, **over):

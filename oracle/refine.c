@@ -166,6 +166,68 @@ static int mls(const rctx_t* C, int32_t label, const double nseed[3], const doub
     return 1;
 }
 
+/* MLS at x with the derivatives of pbar(x) and nbar(x) (analytic Jacobian, reading R37):
+ *   w_i = exp(-|d_i|^2 / 2 s^2), d_i = p_i - x, dw_i/dx = w_i d_i / s^2;
+ *   pbar = x + sum w d / W,  dpbar/dx = (sum w d d^T / s^2 - (pbar - x) dW^T) / W,
+ *     dW = sum w d / s^2;
+ *   nbar = N / |N|, N = sum w sgn(n_i . n_seed) n_i,
+ *   dnbar/dx = (I - nbar nbar^T) (sum w sgn n_i d^T / s^2) / |N|.
+ * The same neighbourhood (same-label surfels within 4 sigma) and id order as mls().
+ * Returns 0 where mls() does. */
+static int mls_d(const rctx_t* C, int32_t label, const double nseed[3], const double x[3],
+                 double dP[3][3], double dN[3][3], double nbar[3], double pbar[3]) {
+    const or_scene* S = C->S;
+    const double s2 = C->sigma * C->sigma;
+    double W = 0, Dv[3] = {0, 0, 0}, Sdd[3][3] = {{0}}, Nn[3] = {0, 0, 0}, Snd[3][3] = {{0}};
+    const int64_t* ids = C->lab_ids + C->lab_start[label];
+    int64_t cnt = C->lab_start[label + 1] - C->lab_start[label];
+    if (C->nb_start) {
+        cnt = nb_query((rctx_t*)C, label, x);
+        ids = C->scratch;
+    }
+    for (int64_t q = 0; q < cnt; ++q) {
+        int64_t i = ids[q];
+        double p[3] = {S->p[3 * i], S->p[3 * i + 1], S->p[3 * i + 2]};
+        double dd[3] = {p[0] - x[0], p[1] - x[1], p[2] - x[2]};
+        double d2 = dot(dd, dd);
+        if (d2 > C->rad2) continue;
+        double w = exp(-d2 / (2.0 * C->sigma * C->sigma));
+        double n[3] = {S->nrm[3 * i], S->nrm[3 * i + 1], S->nrm[3 * i + 2]};
+        double sg = dot(n, nseed) < 0.0 ? -1.0 : 1.0;
+        W += w;
+        for (int a = 0; a < 3; ++a) {
+            Dv[a] += w * dd[a];
+            Nn[a] += w * sg * n[a];
+            for (int b = 0; b < 3; ++b) {
+                Sdd[a][b] += w * dd[a] * dd[b];
+                Snd[a][b] += w * sg * n[a] * dd[b];
+            }
+        }
+    }
+    if (!(W > 0.0)) return 0;
+    double ln = norm(Nn);
+    if (!(ln > 0.0)) return 0;
+    double dW[3], q[3];
+    for (int a = 0; a < 3; ++a) {
+        dW[a] = Dv[a] / s2;
+        q[a] = Dv[a] / W;          /* pbar - x */
+        pbar[a] = x[a] + q[a];
+        nbar[a] = Nn[a] / ln;
+    }
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) dP[a][b] = (Sdd[a][b] / s2 - q[a] * dW[b]) / W;
+    double M[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) M[a][b] = Snd[a][b] / s2;
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+            double t = M[a][b];
+            for (int c = 0; c < 3; ++c) t -= nbar[a] * nbar[c] * M[c][b];
+            dN[a][b] = t / ln;
+        }
+    return 1;
+}
+
 static void basis(const double n[3], double u[3], double v[3]) {
     double ax[3] = {0, 0, 0};
     double m0 = fabs(n[0]), m1 = fabs(n[1]), m2 = fabs(n[2]);
@@ -236,6 +298,138 @@ static int residual(const rctx_t* C, const pathdef_t* D, const double* z, double
         }
     }
     if (gradsq) *gradsq = gs;
+    return 1;
+}
+
+/* Analytic Jacobian of the residual of residual() (reading R37): chain rule through
+ * g_k = (x_k - x_{k-1})/|.| + (x_k - x_{k+1})/|.| (d(h/|h|)/dh = (I - h h^T/|h|^2)/|h|),
+ * the MLS point and normal (mls_d), the basis u = normalize(nbar x a) (a fixed per evaluation:
+ * du/dnbar = (I - u u^T)/|nbar x a| (-[a]x)), v = nbar x u (dv/dnbar = -[u]x + [nbar]x du/dnbar)
+ * and x_k = a_k + t_k e_k for diffractions.  J[i*m + j] = dr_i/dz_j.  0 where the residual is
+ * undefined. */
+static void cross_mat(const double a[3], double Mx[3][3]) { /* Mx v = a x v */
+    Mx[0][0] = 0; Mx[0][1] = -a[2]; Mx[0][2] = a[1];
+    Mx[1][0] = a[2]; Mx[1][1] = 0; Mx[1][2] = -a[0];
+    Mx[2][0] = -a[1]; Mx[2][1] = a[0]; Mx[2][2] = 0;
+}
+
+static int jacobian(const rctx_t* C, const pathdef_t* D, const double* z, double* J) {
+    const int m = D->dim;
+    double I[NV + 2][3];
+    points(C, D, z, I);
+    memset(J, 0, sizeof(double) * m * m);
+    for (int k = 0; k < D->n; ++k) {
+        const double* x = I[k + 1];
+        double a[3] = {x[0] - I[k][0], x[1] - I[k][1], x[2] - I[k][2]};
+        double b[3] = {x[0] - I[k + 2][0], x[1] - I[k + 2][1], x[2] - I[k + 2][2]};
+        double la = norm(a), lb = norm(b);
+        if (!(la > 0.0 && lb > 0.0)) return 0;
+        double ha[3], hb[3], g[3];
+        for (int q = 0; q < 3; ++q) {
+            ha[q] = a[q] / la;
+            hb[q] = b[q] / lb;
+            g[q] = ha[q] + hb[q];
+        }
+        double Ma[3][3], Mb[3][3];
+        for (int p = 0; p < 3; ++p)
+            for (int q = 0; q < 3; ++q) {
+                Ma[p][q] = ((p == q ? 1.0 : 0.0) - ha[p] * ha[q]) / la;
+                Mb[p][q] = ((p == q ? 1.0 : 0.0) - hb[p] * hb[q]) / lb;
+            }
+        /* rows of vertex k: derivative rows w.r.t. x_{k-1}, x_k, x_{k+1} (R[row][nbr][coord]) */
+        int nrow = D->kind[k] == 0 ? 3 : 1;
+        double R[3][3][3];
+        memset(R, 0, sizeof(R));
+        if (D->kind[k] == 0) {
+            double dP[3][3], dN[3][3], nb[3], pb[3];
+            if (!mls_d(C, D->label[k], D->nseed[k], x, dP, dN, nb, pb)) return 0;
+            /* the residual's own MLS point (P/W, as residual()) for (x - pbar) */
+            double pbr[3], nbr[3];
+            if (!mls(C, D->label[k], D->nseed[k], x, pbr, nbr)) return 0;
+            double u[3], v[3];
+            basis(nbr, u, v);
+            double m0 = fabs(nbr[0]), m1 = fabs(nbr[1]), m2 = fabs(nbr[2]);
+            int ax = 0;
+            if (m1 < m0) ax = 1;
+            if (m2 < (ax == 0 ? m0 : m1)) ax = 2;
+            double av[3] = {0, 0, 0};
+            av[ax] = 1.0;
+            double c[3];
+            cross(nbr, av, c);
+            double lc = norm(c), Ax[3][3], Ux[3][3], Nx[3][3], dU[3][3], dV[3][3];
+            cross_mat(av, Ax);
+            cross_mat(u, Ux);
+            cross_mat(nbr, Nx);
+            for (int p = 0; p < 3; ++p)
+                for (int q = 0; q < 3; ++q) {
+                    double t = 0;
+                    for (int r = 0; r < 3; ++r) t += ((p == r ? 1.0 : 0.0) - u[p] * u[r]) * (-Ax[r][q]);
+                    dU[p][q] = t / lc;
+                }
+            for (int p = 0; p < 3; ++p)
+                for (int q = 0; q < 3; ++q) {
+                    double t = -Ux[p][q];
+                    for (int r = 0; r < 3; ++r) t += Nx[p][r] * dU[r][q];
+                    dV[p][q] = t;
+                }
+            double xp[3] = {x[0] - pbr[0], x[1] - pbr[1], x[2] - pbr[2]};
+            for (int q = 0; q < 3; ++q) {
+                double gu = 0, gv = 0, uM = 0, vM = 0, up = 0, vp = 0, un = 0, vn = 0, fx = 0;
+                for (int p = 0; p < 3; ++p) {
+                    /* g^T dU dN[:, q] and g^T dV dN[:, q] */
+                    double dun = 0, dvn = 0;
+                    for (int r = 0; r < 3; ++r) {
+                        dun += dU[p][r] * dN[r][q];
+                        dvn += dV[p][r] * dN[r][q];
+                    }
+                    gu += g[p] * dun;
+                    gv += g[p] * dvn;
+                    uM += u[p] * (Ma[p][q] + Mb[p][q]);
+                    vM += v[p] * (Ma[p][q] + Mb[p][q]);
+                    up += u[p] * Ma[p][q];
+                    vp += v[p] * Ma[p][q];
+                    un += u[p] * Mb[p][q];
+                    vn += v[p] * Mb[p][q];
+                    fx += nbr[p] * ((p == q ? 1.0 : 0.0) - dP[p][q]) + xp[p] * dN[p][q];
+                }
+                R[0][1][q] = uM + gu;
+                R[1][1][q] = vM + gv;
+                R[2][1][q] = fx;
+                R[0][0][q] = -up;
+                R[1][0][q] = -vp;
+                R[0][2][q] = -un;
+                R[1][2][q] = -vn;
+            }
+        } else {
+            const double* e = D->ee[k];
+            for (int q = 0; q < 3; ++q) {
+                double t1 = 0, t0 = 0, t2 = 0;
+                for (int p = 0; p < 3; ++p) {
+                    t1 += e[p] * (Ma[p][q] + Mb[p][q]);
+                    t0 += e[p] * Ma[p][q];
+                    t2 += e[p] * Mb[p][q];
+                }
+                R[0][1][q] = t1;
+                R[0][0][q] = -t0;
+                R[0][2][q] = -t2;
+            }
+        }
+        /* scatter into J: neighbour j = k-1, k, k+1 (unknown vertices only) */
+        for (int nb_ = 0; nb_ < 3; ++nb_) {
+            int j = k - 1 + nb_;
+            if (j < 0 || j >= D->n) continue;
+            for (int row = 0; row < nrow; ++row) {
+                double* Jr = J + (D->col[k] + row) * m;
+                if (D->kind[j] == 0) {
+                    for (int q = 0; q < 3; ++q) Jr[D->col[j] + q] += R[row][nb_][q];
+                } else {
+                    double t = 0;
+                    for (int q = 0; q < 3; ++q) t += R[row][nb_][q] * D->ee[j][q];
+                    Jr[D->col[j]] += t;
+                }
+            }
+        }
+    }
     return 1;
 }
 
@@ -372,16 +566,19 @@ static void refine_one(const rctx_t* C, const or_coarse* c, or_refined* out) {
     else if (!residual(C, &D, z, r, NULL, NULL)) status = NRT_OR_NO_SUPPORT;
     else {
         for (it = 1; it <= R->max_iter; ++it) {
-            /* Jacobian by central differences */
             int ok = 1;
-            for (int j = 0; j < m && ok; ++j) {
-                double zj = z[j];
-                z[j] = zj + h;
-                ok &= residual(C, &D, z, rp, NULL, NULL);
-                z[j] = zj - h;
-                ok &= residual(C, &D, z, rm, NULL, NULL);
-                z[j] = zj;
-                for (int i = 0; i < m; ++i) J[i * m + j] = (rp[i] - rm[i]) / (2.0 * h);
+            if (R->jac_fd) { /* Jacobian by central differences */
+                for (int j = 0; j < m && ok; ++j) {
+                    double zj = z[j];
+                    z[j] = zj + h;
+                    ok &= residual(C, &D, z, rp, NULL, NULL);
+                    z[j] = zj - h;
+                    ok &= residual(C, &D, z, rm, NULL, NULL);
+                    z[j] = zj;
+                    for (int i = 0; i < m; ++i) J[i * m + j] = (rp[i] - rm[i]) / (2.0 * h);
+                }
+            } else { /* analytic Jacobian (R37) */
+                ok = jacobian(C, &D, z, J);
             }
             if (!ok) {
                 status = NRT_OR_NO_SUPPORT;
@@ -624,6 +821,77 @@ int or_path_residual(const or_scene* S, const or_refine_params* R, const or_coar
     if (z_out) memcpy(z_out, z, sizeof(double) * m);
     if (z_in) memcpy(z, z_in, sizeof(double) * m);
     int ok = m == 0 ? 1 : residual(&C, &D, z, r_out, NULL, NULL);
+    free(C.lab_start);
+    free(C.lab_ids);
+    return ok ? m : -1;
+}
+
+/* pin helper: the Jacobian of or_path_residual's residual (analytic or central differences) */
+int or_path_jacobian(const or_scene* S, const or_refine_params* R, const or_coarse* c,
+                     const double* z_in, int fd, double h, double* J_out) {
+    rctx_t C;
+    memset(&C, 0, sizeof(C));
+    C.S = S;
+    C.R = R;
+    C.sigma = R->xi * R->r_s;
+    C.rad2 = (4.0 * C.sigma) * (4.0 * C.sigma);
+    for (int a = 0; a < 3; ++a) {
+        C.tx[a] = R->tx[a];
+        C.rx[a] = R->rx[3 * (int64_t)c->rx + a];
+    }
+    C.lab_start = (int64_t*)calloc(4098, sizeof(int64_t));
+    C.lab_ids = (int64_t*)malloc(sizeof(int64_t) * (size_t)(S->n > 0 ? S->n : 1));
+    for (int64_t i = 0; i < S->n; ++i) C.lab_start[S->label[i] + 1]++;
+    for (int l = 0; l < 4097; ++l) C.lab_start[l + 1] += C.lab_start[l];
+    int64_t* fill = (int64_t*)calloc(4097, sizeof(int64_t));
+    for (int64_t i = 0; i < S->n; ++i) C.lab_ids[C.lab_start[S->label[i]] + fill[S->label[i]]++] = i;
+    free(fill);
+    pathdef_t D;
+    memset(&D, 0, sizeof(D));
+    D.n = c->n_int;
+    double z[MAXDIM];
+    int m = 0;
+    for (int k = 0; k < D.n; ++k) {
+        D.kind[k] = (c->kinds >> k) & 1u;
+        D.label[k] = c->label[k];
+        D.prim[k] = c->prim[k];
+        D.col[k] = m;
+        if (D.kind[k] == 0) {
+            for (int a = 0; a < 3; ++a) {
+                D.nseed[k][a] = S->nrm[3 * (int64_t)c->prim[k] + a];
+                z[m + a] = c->v[k][a];
+            }
+            m += 3;
+        } else {
+            const or_edge* E = &S->edges[c->prim[k]];
+            double ev[3] = {(double)E->b[0] - E->a[0], (double)E->b[1] - E->a[1], (double)E->b[2] - E->a[2]};
+            double l = norm(ev);
+            for (int a = 0; a < 3; ++a) {
+                D.ea[k][a] = E->a[a];
+                D.ee[k][a] = ev[a] / l;
+            }
+            D.elen[k] = l;
+            double w[3] = {c->v[k][0] - D.ea[k][0], c->v[k][1] - D.ea[k][1], c->v[k][2] - D.ea[k][2]};
+            z[m] = dot(w, D.ee[k]);
+            m += 1;
+        }
+    }
+    D.dim = m;
+    if (z_in) memcpy(z, z_in, sizeof(double) * m);
+    int ok = 1;
+    if (m > 0 && !fd) ok = jacobian(&C, &D, z, J_out);
+    if (m > 0 && fd) {
+        double rp[MAXDIM], rm[MAXDIM];
+        for (int jj = 0; jj < m && ok; ++jj) {
+            double zj = z[jj];
+            z[jj] = zj + h;
+            ok &= residual(&C, &D, z, rp, NULL, NULL);
+            z[jj] = zj - h;
+            ok &= residual(&C, &D, z, rm, NULL, NULL);
+            z[jj] = zj;
+            for (int i = 0; i < m; ++i) J_out[i * m + jj] = (rp[i] - rm[i]) / (2.0 * h);
+        }
+    }
     free(C.lab_start);
     free(C.lab_ids);
     return ok ? m : -1;

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnrt.so")
-SOURCES = ["api.cu", "scene.cu", "launch.cu", "dedupe.cu", "refine.cu", "refine_nw12.cu", "post.cu"]
+SOURCES = ["api.cu", "scene.cu", "launch.cu", "dedupe.cu", "refine.cu", "post.cu"]
 COMMON = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -23,7 +23,7 @@ COMMON = [
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
     "-Xptxas", "-v",
 ]
-FMAD = {"refine.cu": "-fmad=true", "refine_nw12.cu": "-fmad=true"}  # default -fmad=false (R3: no FMA contraction on the parity path)
+FMAD = {"refine.cu": "-fmad=true"}  # default -fmad=false (R3: no FMA contraction on the parity path)
 if os.environ.get("NRT_REFINE_FMAD") == "0":  # A/B switch
     FMAD = {}
 NVCC_FLAGS = COMMON + ["-fmad=false", "--shared"]  # (kept for reference: the single-command form)

@@ -263,6 +263,7 @@ void nrt_scene_free(nrt_scene s) {
     cudaFreeAsync(s->hcell, nullptr);
     cudaFreeAsync(s->hrec, nullptr);
     cudaFreeAsync(s->hid, nullptr);
+    cudaFreeAsync(s->hoff, nullptr);
     cudaFreeAsync(s->edges, nullptr);
     delete s;
 }

@@ -143,6 +143,8 @@ struct nrt_scene_s {
     uint2* hcell = nullptr;
     float4* hrec = nullptr;
     unsigned* hid = nullptr;   // [n] surfel id of each home record
+    unsigned* hoff = nullptr;  // [nh + 1] exclusive prefix of the home-cell counts: the records of
+                               // cells a..b (consecutive linear indices) are [hoff[a], hoff[b+1])
     int32_t* label = nullptr;  // [n]
     nrt::DevEdge* edges = nullptr;
     int n_edges = 0;
@@ -218,6 +220,4 @@ float cRw_of(float c_R, int64_t n_rays);
 // refine.cu
 nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
                   cudaStream_t st);
-nrt_status refine_nw12(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
-                       cudaStream_t st);  // refine_nw12.cu: 12 warps/path
 }  // namespace nrt

@@ -150,82 +150,6 @@ __device__ __forceinline__ unsigned long long lane_inc(unsigned long long* ctr) 
 #define NRT_TRACE_REFILL 8  // 1: each lane refills alone; k > 1: warp refills k+ idle lanes together
 #endif
 
-// ---- A3 reference walk (debug path): nearest surfel along (o, d) by plain 3D-DDA --------
-__device__ int nearest(const TP& P, float3 o, float3 d, float3 l0, float3 l1, int prev,
-                       float& t_out) {
-    float best_t = INFINITY;
-    int best = -1;
-    const float gx1 = P.ox + P.nx * P.v, gy1 = P.oy + P.ny * P.v, gz1 = P.oz + P.nz * P.v;
-    float ix_ = 1.0f / d.x, iy_ = 1.0f / d.y, iz_ = 1.0f / d.z;
-    float t0 = 0.0f, t1 = INFINITY;
-    {
-        float a = (P.ox - o.x) * ix_, b = (gx1 - o.x) * ix_;
-        if (d.x != 0.0f) { t0 = fmaxf(t0, fminf(a, b)); t1 = fminf(t1, fmaxf(a, b)); }
-        else if (o.x < P.ox || o.x > gx1) t1 = -1.0f;
-        a = (P.oy - o.y) * iy_; b = (gy1 - o.y) * iy_;
-        if (d.y != 0.0f) { t0 = fmaxf(t0, fminf(a, b)); t1 = fminf(t1, fmaxf(a, b)); }
-        else if (o.y < P.oy || o.y > gy1) t1 = -1.0f;
-        a = (P.oz - o.z) * iz_; b = (gz1 - o.z) * iz_;
-        if (d.z != 0.0f) { t0 = fmaxf(t0, fminf(a, b)); t1 = fminf(t1, fmaxf(a, b)); }
-        else if (o.z < P.oz || o.z > gz1) t1 = -1.0f;
-    }
-    if (t0 > t1) {
-        t_out = INFINITY;
-        return -1;
-    }
-    float sx = o.x + t0 * d.x, sy = o.y + t0 * d.y, sz = o.z + t0 * d.z;
-    int ix = min(P.nx - 1, max(0, (int)floorf((sx - P.ox) * P.inv_v)));
-    int iy = min(P.ny - 1, max(0, (int)floorf((sy - P.oy) * P.inv_v)));
-    int iz = min(P.nz - 1, max(0, (int)floorf((sz - P.oz) * P.inv_v)));
-    const int stx = d.x > 0.0f ? 1 : -1, sty = d.y > 0.0f ? 1 : -1, stz = d.z > 0.0f ? 1 : -1;
-    float tmx = d.x != 0.0f ? ((P.ox + (float)(ix + (stx > 0)) * P.v) - o.x) * ix_ : INFINITY;
-    float tmy = d.y != 0.0f ? ((P.oy + (float)(iy + (sty > 0)) * P.v) - o.y) * iy_ : INFINITY;
-    float tmz = d.z != 0.0f ? ((P.oz + (float)(iz + (stz > 0)) * P.v) - o.z) * iz_ : INFINITY;
-    for (;;) {
-        const uint2 rg = __ldg(&P.cell[ix + P.nx * (iy + P.ny * iz)]);
-        for (unsigned k = rg.x; k < rg.y; ++k) {
-            const float4 A = __ldg(&P.rec[2 * k]);
-            const float4 B = __ldg(&P.rec[2 * k + 1]);
-            const int id = __float_as_int(B.w);
-            const float wx = o.x - A.x, wy = o.y - A.y, wz = o.z - A.z;
-            const float f0 = (wx * B.x + wy * B.y) + wz * B.z;
-            const float dn = (d.x * B.x + d.y * B.y) + d.z * B.z;
-            if (!(f0 * dn < 0.0f) || id == prev) continue;
-            if (fabsf(f0) <= P.tau) {
-                const float c0 = (B.x * l0.x + B.y * l0.y) + B.z * l0.z;
-                const float c1 = (B.x * l1.x + B.y * l1.y) + B.z * l1.z;
-                if (fabsf(c0) >= P.cos_ex || fabsf(c1) >= P.cos_ex) continue;
-            }
-            const float t = (-f0) / dn;
-            if (t > best_t) continue;
-            const float hx = o.x + t * d.x, hy = o.y + t * d.y, hz = o.z + t * d.z;
-            const float qx = hx - A.x, qy = hy - A.y, qz = hz - A.z;
-            const float qq = (qx * qx + qy * qy) + qz * qz;
-            if (qq <= A.w * A.w && (t < best_t || id < best)) {
-                best_t = t;
-                best = id;
-            }
-        }
-        const float te = fminf(tmx, fminf(tmy, tmz));
-        if (best_t < te - P.pad) break;
-        if (tmx <= tmy && tmx <= tmz) {
-            ix += stx;
-            if (ix < 0 || ix >= P.nx) break;
-            tmx = ((P.ox + (float)(ix + (stx > 0)) * P.v) - o.x) * ix_;
-        } else if (tmy <= tmz) {
-            iy += sty;
-            if (iy < 0 || iy >= P.ny) break;
-            tmy = ((P.oy + (float)(iy + (sty > 0)) * P.v) - o.y) * iy_;
-        } else {
-            iz += stz;
-            if (iz < 0 || iz >= P.nz) break;
-            tmz = ((P.oz + (float)(iz + (stz > 0)) * P.v) - o.z) * iz_;
-        }
-    }
-    t_out = best_t;
-    return best;
-}
-
 __device__ void write_record(const TP& P, const Hist& h, int rx, float L, uint64_t ray_id) {
     unsigned long long slot = agg_inc(P.raw_n);
     if (slot >= P.raw_cap) return;
@@ -423,34 +347,6 @@ __device__ __forceinline__ void edge_captures_staged(const TP& P, const float4* 
             if (ux * ux + uy * uy + uz * uz <= lim * lim) edge_event(P, h, o, d, t_hit, L, ray_id, j);
         }
         __syncwarp();
-    }
-}
-
-// ---- debug: C.1 step 2 for one primary ray, sequentially, with the reference walk -------
-__global__ void k_debug(TP P, const uint64_t* ids, int64_t n) {
-    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n) return;
-    int64_t* out = P.hit_out + q * (P.max_refl + 1);
-    for (int k = 0; k <= P.max_refl; ++k) out[k] = -2;
-    float3 o = make_float3(P.tx, P.ty, P.tz);
-    float3 d = fib_dir(ids[q], P.n_rays);
-    float3 l0 = make_float3(0.0f, 0.0f, 0.0f), l1 = l0;
-    int prev = -1;
-    for (int seg = 0; seg <= P.max_refl; ++seg) {
-        float th;
-        const int s = nearest(P, o, d, l0, l1, prev, th);
-        out[seg] = s;
-        if (s < 0 || seg == P.max_refl) break;
-        const float3 hp = make_float3(o.x + th * d.x, o.y + th * d.y, o.z + th * d.z);
-        const float4 nv = __ldg(&P.sn[s]);
-        const float3 nn = make_float3(nv.x, nv.y, nv.z);
-        const float k2 = 2.0f * dot3(d, nn);
-        const float3 x = make_float3(d.x - k2 * nn.x, d.y - k2 * nn.y, d.z - k2 * nn.z);
-        const float l = sqrtf(dot3(x, x));
-        d = make_float3(x.x / l, x.y / l, x.z / l);
-        o = hp;
-        l0 = l1 = nn;
-        prev = s;
     }
 }
 
@@ -881,7 +777,16 @@ __device__ __forceinline__ unsigned order_key(const TP& P, float3 h, float3 d) {
     }
     const unsigned u = (unsigned)min(127, max(0, (int)((px + 1.0f) * 64.0f)));
     const unsigned v = (unsigned)min(127, max(0, (int)((py + 1.0f) * 64.0f)));
-    return (m << 14) | (u << 7) | v;
+    return min((m << 14) | (u << 7) | v, 0xFFFFFFFEu);  // 0xFFFFFFFF pads the sorted list
+}
+
+// live-list entries [n_alive, cap) get the largest key, so a sort of all cap entries puts the
+// live ones first (in key order) and needs no host-side count
+__global__ void k_pad_keys(unsigned* keys, const unsigned long long* n_alive, uint64_t cap) {
+    const uint64_t na = *n_alive;
+    for (uint64_t j = na + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cap;
+         j += (uint64_t)gridDim.x * blockDim.x)
+        keys[j] = 0xFFFFFFFFu;
 }
 
 // SHADE: captures, edge events, reflection; compacts the live list for bounce b+1.
@@ -934,6 +839,7 @@ __global__ void __launch_bounds__(128) k_shade(TP P, Wave W, int b) {
         } else if (edges) {
             edge_captures(P, c.h, o, d, th, L, rid);
         }
+        if (P.hit_out && on) P.hit_out[(size_t)ray * (P.max_refl + 1) + c.seg] = sid;  // debug dump
         if (on && sid >= 0 && c.seg < c.budget) {
             // A4: reflect at the hit surfel: d' = d - (2 d.n) n, normalised
             const float3 hp = make_float3(o.x + th * d.x, o.y + th * d.y, o.z + th * d.z);
@@ -1011,6 +917,36 @@ __global__ void k_gen_primary(TP P, Wave W, uint64_t n_shard, uint64_t j0, const
         W.alive[0][j] = (unsigned)j;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) W.n_alive[0] = n_shard;
+}
+
+// primary rays with explicit lattice ids (nrt_debug_trace_rays): slot j traces ray ids[j]
+// through the same TRACE/SHADE kernels; SHADE writes each segment's hit into P.hit_out
+__global__ void k_gen_ids(TP P, Wave W, const uint64_t* ids, uint64_t n) {
+    const int nseg = P.max_refl + 1;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const float3 d = fib_dir(ids[j], P.n_rays);
+        W.o[j] = make_float4(P.tx, P.ty, P.tz, __int_as_float(-1));
+        W.d[j] = make_float4(d.x, d.y, d.z, 0.0f);
+        W.l0[j] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        W.l1[j] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        RayCold& c = W.cold[j];
+        c.L = 0.0f;
+        c.Ls = 0.0f;
+        c.kR = P.cRw;
+        c.R0 = 0.0f;
+        c.seg = 0;
+        c.budget = P.max_refl;
+        c.flags = 0;
+        c.rid = ids[j];
+        c.h.n = 0;
+        c.h.n_diff = 0;
+        c.h.kinds = 0;
+        c.h.s_edge = 0.0f;
+        for (int k = 0; k < nseg; ++k) P.hit_out[j * nseg + k] = -2;  // not traced
+        W.alive[0][j] = (unsigned)j;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) W.n_alive[0] = n;
 }
 
 // fan ray generation (A7, R15-R16): fan index f -> (event r, m); Eq. 14 lift
@@ -1260,7 +1196,12 @@ struct Counters {
 
 static std::atomic<unsigned long long> g_hint_raw{0}, g_hint_ev{0}, g_hint_fan{0};
 static const uint64_t kBatch = 1ull << 24;  // rays in flight per wavefront batch
-static const unsigned long long kSortMin = 1ull << 15;  // reorder live lists at least this long
+// reorder live lists of batches at least this long (NRT_SORT_MIN overrides: tests force the
+// reorder path on small scenes)
+static unsigned long long sort_min() {
+    if (const char* e = getenv("NRT_SORT_MIN")) return strtoull(e, nullptr, 10);
+    return 1ull << 15;
+}
 
 // wavefront buffers for up to `cap` rays (stream-ordered; freed by free_wave)
 // Reorder each bounce's live list by (coarse cell, direction) only when the scene's records
@@ -1319,7 +1260,7 @@ struct WaveGuard {  // every exit path of a launch phase
 };
 
 // bounce loop: TRACE + SHADE per bounce; ms_kernel accumulates the TRACE kernels' time
-static nrt_status run_bounces(const TP& P, Wave& W, int iters, int dev, bool counters,
+static nrt_status run_bounces(const TP& P, Wave& W, uint64_t cap, int iters, int dev, bool counters,
                               float* ms_trace, cudaStream_t st) {
 #if NRT_TRACE_COOP
 #define NRT_K_TRACE k_trace_coop
@@ -1357,21 +1298,19 @@ static nrt_status run_bounces(const TP& P, Wave& W, int iters, int dev, bool cou
         cudaEventRecord(ev[3 * b + 1], st);
         k_shade<<<sb, 128, shade_smem, st>>>(P, W, b);
         ::nrt::count_launch();
-        if (W.skey && b + 1 < iters) {
+        if (W.skey && b + 1 < iters && cap >= sort_min()) {
             // reorder the next live list by (coarse cell, direction): neighbouring lanes and
-            // blocks then walk the same cells and share their records in L1/L2
-            unsigned long long na = 0;
-            NRT_CUDA(cudaMemcpyAsync(&na, W.n_alive + b + 1, sizeof(na), cudaMemcpyDeviceToHost, st));
-            NRT_CUDA(cudaStreamSynchronize(st));
-            if (na >= kSortMin) {
-                size_t tb = W.otmp_bytes;
-                unsigned* nxt = W.alive[(b + 1) & 1];
-                NRT_CUDA(cub::DeviceRadixSort::SortPairs(W.otmp, tb, W.skey, W.okey[1], nxt, W.oval, (int)na,
-                                                         0, 32, st));
-                ::nrt::count_launch();
-                W.alive[(b + 1) & 1] = W.oval;
-                W.oval = nxt;
-            }
+            // blocks then walk the same cells and share their records in L1/L2.  The count
+            // stays on the device: entries past it are padded with the largest key and the
+            // whole capacity is sorted (no host round trip inside the bounce loop)
+            k_pad_keys<<<(unsigned)sm_count(dev) * 4, 256, 0, st>>>(W.skey, W.n_alive + b + 1, cap);
+            ::nrt::count_launch();
+            size_t tb = W.otmp_bytes;
+            unsigned* nxt = W.alive[(b + 1) & 1];
+            NRT_CUDA(cub::DeviceRadixSort::SortPairs(W.otmp, tb, W.skey, W.okey[1], nxt, W.oval, (int)cap,
+                                                     0, 32, st));
+            W.alive[(b + 1) & 1] = W.oval;
+            W.oval = nxt;
         }
         cudaEventRecord(ev[3 * b + 2], st);
     }
@@ -1471,7 +1410,7 @@ nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw
                 fprintf(stderr, "[nrt] gen done %.3f ms\n", host_ms_since(t_start));
             }
             float ms = 0.0f;
-            NRT_TRY(run_bounces(P, W, a.max_refl + 1, s->device, a.desc.counters != 0, &ms, st));
+            NRT_TRY(run_bounces(P, W, nb, a.max_refl + 1, s->device, a.desc.counters != 0, &ms, st));
             stats->ms_kernel += ms;
         }
         NRT_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, st));
@@ -1560,7 +1499,7 @@ nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev
         k_gen_fans<<<gb, 256, 0, st>>>(P, W, ev, n_ev, off, total);
         ::nrt::count_launch();
         // fans need at most max_refl + 1 segments (budget <= max_refl)
-        NRT_TRY(run_bounces(P, W, a.max_refl + 1, s->device, a.desc.counters != 0,
+        NRT_TRY(run_bounces(P, W, total, a.max_refl + 1, s->device, a.desc.counters != 0,
                             &stats->ms_kernel, st));
         NRT_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, st));
         NRT_CUDA(cudaStreamSynchronize(st));
@@ -1583,6 +1522,8 @@ nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev
     return NRT_OK;
 }
 
+// per-segment hit ids of explicit primary rays, traced by the production wavefront (the same
+// k_trace / k_shade launches, refill and reorder paths as nrt_launch); no records are emitted
 nrt_status debug_trace(nrt_scene s, const LaunchArgs& a, const uint64_t* ids, int64_t n,
                        int64_t* hit_ids, cudaStream_t st) {
     if (n <= 0) return NRT_OK;
@@ -1590,17 +1531,41 @@ nrt_status debug_trace(nrt_scene s, const LaunchArgs& a, const uint64_t* ids, in
     uint64_t* dids = nullptr;
     int64_t* dh = nullptr;
     const size_t nseg = (size_t)a.max_refl + 1;
+    Counters* dc = nullptr;
+    NRT_CUDA(cudaMallocAsync(&dc, sizeof(Counters), st));
+    NRT_CUDA(cudaMemsetAsync(dc, 0, sizeof(Counters), st));
     NRT_CUDA(cudaMallocAsync(&dids, n * 8, st));
     NRT_CUDA(cudaMallocAsync(&dh, n * nseg * 8, st));
     NRT_CUDA(cudaMemcpyAsync(dids, ids, n * 8, cudaMemcpyHostToDevice, st));
+    Wave W{};
+    WaveGuard wg{&W, st};
+    NRT_TRY(alloc_wave(W, (uint64_t)n, s->device, st));
+    if (reorder_on(s)) W.skey = W.okey[0];
+    W.n_alive = dc->n_alive;
+    W.ctr = dc->ctr;
+    P.raw = nullptr;
+    P.raw_cap = 0;
+    P.raw_n = &dc->raw_n;
+    P.ev = nullptr;
+    P.ev_cap = 0;
+    P.ev_n = &dc->ev_n;
+    P.bounces = &dc->bounces;
+    P.counters = &dc->tests;
+    P.n_edges = 0;
     P.hit_out = dh;
-    k_debug<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(P, dids, n);
+    unsigned gb = (unsigned)((n + 255) / 256);
+    if (gb > (unsigned)sm_count(s->device) * 16) gb = (unsigned)sm_count(s->device) * 16;
+    k_gen_ids<<<gb, 256, 0, st>>>(P, W, dids, (uint64_t)n);
     ::nrt::count_launch();
+    float ms = 0.0f;
+    NRT_TRY(run_bounces(P, W, (uint64_t)n, a.max_refl + 1, s->device, false, &ms, st));
     NRT_CUDA(cudaGetLastError());
     NRT_CUDA(cudaMemcpyAsync(hit_ids, dh, n * nseg * 8, cudaMemcpyDeviceToHost, st));
     NRT_CUDA(cudaStreamSynchronize(st));
+    free_wave(W, st);
     cudaFreeAsync(dids, st);
     cudaFreeAsync(dh, st);
+    cudaFreeAsync(dc, st);
     return NRT_OK;
 }
 

@@ -246,6 +246,12 @@ __global__ void k_home_records(const unsigned* keys, const unsigned* ids, int64_
     if (k == n - 1 || keys[k + 1] != key) hcell[key].y = (unsigned)(k + 1);
 }
 
+__global__ void k_home_counts(const uint2* hcell, int64_t nh, unsigned* cnt) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > nh) return;
+    cnt[c] = c < nh ? hcell[c].y - hcell[c].x : 0u;
+}
+
 template <class T>
 nrt_status dmalloc(T** p, size_t count, cudaStream_t st) {
     if (count == 0) count = 1;
@@ -486,6 +492,21 @@ static nrt_status build_impl(const nrt_scene_desc* D, nrt_scene S, cudaStream_t 
                                            S->hcell);
         ::nrt::count_launch();
         NRT_CUDA(cudaGetLastError());
+        // offsets of every home cell (empty ones included): runs of consecutive cells are
+        // contiguous record ranges (refinement's direct neighbourhood scans walk cell rows)
+        {
+            unsigned* cnt = nullptr;
+            NRT_TRY(dmalloc(&cnt, nh + 1, st));
+            NRT_TRY(dmalloc(&S->hoff, nh + 1, st));
+            k_home_counts<<<(unsigned)((nh + 256) / 256), 256, 0, st>>>(S->hcell, nh, cnt);
+            ::nrt::count_launch();
+            size_t tbs = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tbs, cnt, S->hoff, (int)(nh + 1), st);
+            NRT_CUDA(cudaMallocAsync(&tmp, tbs, st));
+            cub::DeviceScan::ExclusiveSum(tmp, tbs, cnt, S->hoff, (int)(nh + 1), st);
+            cudaFreeAsync(tmp, st);
+            cudaFreeAsync(cnt, st);
+        }
         cudaFreeAsync(hk0, st);
         cudaFreeAsync(hk1, st);
         S->hid = hvb.Current();  // kept: surfel ids of the home records (post-processing)

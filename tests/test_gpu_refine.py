@@ -16,6 +16,7 @@ pytestmark = pytest.mark.gpu
 NPROC = max(1, min(32, os.cpu_count() or 1))
 TOL_V = 1e-5      # m
 TOL_DELAY = 1e-12  # s
+TOL_ANG = 1e-4     # degrees (R27 angles are float32)
 
 
 @pytest.fixture(scope="module")
@@ -36,15 +37,37 @@ def compare(got, ref, max_flip_frac=0.0, what=""):
     assert len(got) == len(ref), what
     for f in ("rx", "n_int", "kinds", "label", "prim", "ray_id"):
         assert np.array_equal(got[f], ref[f]), (what, f)
-    flips = np.nonzero(got["status"] != ref["status"])[0]
+    # A knife-edge flip is a path whose status differs, or which both sides refine to a valid
+    # path but at different roots (|dv| > TOL_V): on noisy MLS surfaces the root is local to the
+    # seed and a stalled Gauss-Newton trajectory is chaotic at the rounding level (SURVEY §8(c)
+    # C.1 "a few knife-edge validity flips are possible. They are reported, not hidden").
+    ok2 = (got["status"] == 0) & (ref["status"] == 0)
+    dvp = np.abs(got["v"] - ref["v"]).reshape(len(got), -1).max(axis=1) if len(got) else np.zeros(0)
+    root_flip = ok2 & (dvp > TOL_V)
+    flips = np.nonzero((got["status"] != ref["status"]) | root_flip)[0]
     assert len(flips) <= max_flip_frac * len(got), (what, len(flips), got["status"][flips[:5]],
                                                     ref["status"][flips[:5]])
-    both = (got["status"] == 0) & (ref["status"] == 0)
+    both = ok2 & ~root_flip
     assert both.sum() > 0 or len(got) == 0
+    # the paths both sides refine to the same root agree far inside the tolerance
+    if both.sum() >= 10:
+        assert np.median(dvp[both]) <= 1e-11, (what, np.median(dvp[both]))
     dv = np.abs(got["v"][both] - ref["v"][both]).max() if both.any() else 0.0
     dd = np.abs(got["delay"][both] - ref["delay"][both]).max() if both.any() else 0.0
     assert dv <= TOL_V, (what, dv)
     assert dd <= TOL_DELAY, (what, dd)
+    # R27 angles (float32 degrees from the FP64 vertices; azimuths compared on the circle)
+    da = 0.0
+    if both.any():
+        for f in ("aod_az", "aod_el", "aoa_az", "aoa_el", "inc"):
+            d = np.abs(got[f][both].astype(np.float64) - ref[f][both])
+            d = np.minimum(d, 360.0 - d)
+            da = max(da, float(d.max()))
+    assert da <= TOL_ANG, (what, da)
+    print(f"[refine parity] {what}: {len(got)} paths, {len(flips)} knife-edge flips "
+          f"({100.0 * len(flips) / max(1, len(got)):.2f} %; {int(root_flip.sum())} of them at "
+          f"another root), {int(both.sum())} OK on both, "
+          f"max |dv| {dv:.2e} m, |d delay| {dd:.2e} s, |d angle| {da:.2e} deg")
     return len(flips), dv, dd
 
 
@@ -85,51 +108,53 @@ def test_sr_small_diffraction_refined_parity(N, O):
     assert ((got["status"] == 0) & (got["n_diff"] == 1)).sum() > 0
 
 
-def test_c2_full_size_sampled_refined_parity(N, O):
-    """Full C2 (1e6 surfels, sigma = 1 cm): GPU refines every coarse path; the oracle
-    re-refines a sample of them one by one."""
+def test_sr_small_refined_parity_full_size_rs(N, O):
+    """Small synthetic room refined at the full-size configurations' r_s = 0.01 m (sigma = 2 cm
+    neighbourhoods, C2/C3's regime) rather than the sparse-cloud 0.03 m."""
+    case = G.case("C2s", sigma=0.010, n=200_000, n_rays=20_000, max_diff=0)
+    case.r_s = 0.01
+    sc = N.build_case_scene(case)
+    coarse = N.launch_case(sc, case)
+    got = refine_gpu(N, case, sc, coarse)
+    ref = O.refine_par(case, coarse.export(), procs=NPROC)
+    compare(got, ref, 0.02, "SR 2e5 surfels r_s=0.01")
+    assert (got["status"] == 0).sum() >= 10
+
+
+def test_c2_full_set_refined_parity(N, O):
+    """Full C2 (1e6 surfels, sigma = 1 cm, the bench's secondary workload): the GPU refines every
+    coarse path, the oracle re-refines EVERY one of them; <= 0.5 % knife-edge status flips."""
     case = G.case("C2", sigma=0.010)
     sc = N.build_case_scene(case)
     coarse = N.launch_case(sc, case)
     got = refine_gpu(N, case, sc, coarse)
     cr = coarse.export()
-    rng = np.random.default_rng(3)
-    idx = np.sort(rng.choice(len(cr), min(24, len(cr)), replace=False))
-    ref = O.refine(case, cr[idx])
-    compare(got[idx], ref, 0.1, "C2 sample")
+    ref = O.refine_par(case, cr, procs=NPROC)
+    compare(got, ref, 0.005, "C2 whole set")
+    assert len(got) > 1000
 
 
-def test_c4_full_size_sampled_refined_parity(N, O):
-    """Full C4 (1e7 surfels, fitted normals, 85 RX, diffraction): the oracle re-refines a
-    sample of the GPU's coarse paths one by one."""
-    case = G.case("C4")
-    sc = N.build_case_scene(case)
+def _sample(allg, n_ok, n_any, seed):
+    rng = np.random.default_rng(seed)
+    ok = np.nonzero(allg["status"] == 0)[0]
+    rest = np.setdiff1d(np.arange(len(allg)), ok)
+    return np.sort(np.concatenate([rng.choice(ok, min(n_ok, len(ok)), replace=False),
+                                   rng.choice(rest, min(n_any, len(rest)), replace=False)]))
+
+
+@pytest.mark.parametrize("name,seed", [("C4", 4), ("C5", 6)])
+def test_full_size_sampled_refined_parity(N, O, name, seed):
+    """Full C4 (1e7 surfels, fitted normals, 85 RX, diffraction) and C5 (879 RX, 1e8-ray
+    lattice) — refinement in the throughput regime: the oracle re-refines 100 paths the GPU
+    found valid and 100 others; <= 1 % status flips."""
+    case = G.case(name)
+    sc = N.build_case_scene(case, device_arrays=True)
     coarse = N.launch_case(sc, case)
     cr = coarse.export()
     allg = refine_gpu(N, case, sc, coarse)
-    rng = np.random.default_rng(4)
-    ok = np.nonzero(allg["status"] == 0)[0]
-    idx = np.sort(np.concatenate([rng.choice(ok, 6, replace=False),
-                                  rng.choice(len(cr), 2, replace=False)]))
-    got = allg[idx]
-    ref = O.refine(case, cr[idx])
-    compare(got, ref, 0.25, "C4 sample")
-
-
-def test_c5_full_size_sampled_refined_parity(N, O):
-    """Full C5 (1e7 surfels, 879 RX, 1e8-ray lattice; refinement of its coarse set in the
-    throughput regime): the oracle re-refines sampled paths one by one."""
-    case = G.case("C5")
-    sc = N.build_case_scene(case)
-    coarse = N.launch_case(sc, case)
-    cr = coarse.export()
-    allg = refine_gpu(N, case, sc, coarse)
-    rng = np.random.default_rng(6)
-    ok = np.nonzero(allg["status"] == 0)[0]
-    idx = np.sort(np.concatenate([rng.choice(ok, 5, replace=False),
-                                  rng.choice(len(cr), 2, replace=False)]))
-    ref = O.refine(case, cr[idx])
-    compare(allg[idx], ref, 0.3, "C5 sample")
+    idx = _sample(allg, 100, 100, seed)
+    ref = O.refine_par(case, cr[idx], procs=NPROC)
+    compare(allg[idx], ref, 0.01, f"{name} sample")
 
 
 def test_refine_sharding_union(N):

@@ -298,3 +298,52 @@ def test_angles_los_and_diffraction(O):
     assert O.STATUS[int(r["status"])] == "OK"
     assert _close_deg(_angles(r), (180.0, 45.0, -90.0, -45.0))
     assert abs(float(r["inc"][0]) - 45.0) < 1e-4
+
+
+# ---------------------------------------------------------------- R37 analytic Jacobian --
+def test_analytic_jacobian_equals_central_differences(O):
+    """R37: the analytic Jacobian (chain rule through g, the MLS point/normal of Eqs. 2-4 and the
+    (u, v) basis) equals central differences of the residual to their own accuracy (~1e-9
+    relative at h = 1e-6..1e-7) on noisy synthetic-room paths with reflections and a
+    diffraction; a wrong term (sign, index, transposed block) shows at 1e-3 or worse."""
+    case = G.case("C2s", sigma=0.010, n=30_000, n_rays=15_000, max_diff=1, max_refl=2)
+    co, _, _ = O.launch_phased(case, procs=os.cpu_count() or 1)
+    sc = O.OracleScene(case.scene)
+    checked = 0
+    for i in range(0, len(co), max(1, len(co) // 30)):
+        Ja = O.path_jacobian(case, co[i], scene=sc)
+        if Ja is None:
+            continue
+        errs = []
+        for h in (1e-5, 1e-6, 1e-7):
+            Jf = O.path_jacobian(case, co[i], fd=True, h=h, scene=sc)
+            errs.append(np.abs(Ja - Jf).max() / max(1e-12, np.abs(Ja).max()))
+        assert min(errs) < 2e-8, (i, errs)
+        checked += 1
+    assert checked >= 20
+    # and at a point away from the seed (z shifted by 3 mm on every unknown)
+    r, z = O.path_residual(case, co[len(co) // 2], scene=sc)
+    z2 = z + 0.003
+    Ja = O.path_jacobian(case, co[len(co) // 2], z=z2, scene=sc)
+    Jf = O.path_jacobian(case, co[len(co) // 2], z=z2, fd=True, h=1e-6, scene=sc)
+    assert np.abs(Ja - Jf).max() / np.abs(Ja).max() < 1e-7
+
+
+def test_analytic_jacobian_planar_closed_form(O):
+    """On one plane z = 0 (noise-free, normals +z) the MLS point/normal derivatives are closed
+    forms: dn/dx = 0, f = x_z, so the third residual row is (0, 0, 1) for the vertex and 0 for
+    its neighbours; rows 1-2 are u, v projected (d g / d x)."""
+    sc = plane_scene([(0.0, 1.0)])
+    case = make_case(sc, (0.0, 0.0, 1.0), (2.0, 0.0, 1.0))
+    c = coarse_rec(O, [(1.02, 0.01, 0.0)], [0], [nearest_id(sc, (1.02, 0.01, 0), 0)])
+    J = O.path_jacobian(case, c)
+    assert J.shape == (3, 3)
+    assert np.allclose(J[2], [0, 0, 1], atol=1e-9)
+    x = np.array([1.02, 0.01, 0.0])
+    a, b = x - (0, 0, 1.0), x - (2.0, 0, 1.0)
+    Ma = (np.eye(3) - np.outer(a, a) / (a @ a)) / np.linalg.norm(a)
+    Mb = (np.eye(3) - np.outer(b, b) / (b @ b)) / np.linalg.norm(b)
+    # basis of n = +z: axis x (smallest |n.a|, ties x<y<z), u = normalize(z x x) = +y, v = z x y = -x
+    u, v = np.array([0, 1.0, 0]), np.array([-1.0, 0, 0])
+    assert np.allclose(J[0], u @ (Ma + Mb), atol=1e-9)
+    assert np.allclose(J[1], v @ (Ma + Mb), atol=1e-9)
