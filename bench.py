@@ -1,14 +1,15 @@
 #!/usr/bin/env python
 """bench.py — one JSON line for the driver (see DESIGN.md §7 "Measurement").
 
-Step = one pass of the whole hot path over the workload (BASELINE.json configs[1], "C2": SR
-room, 1e6 surfels, sigma = 10 mm, 1 TX / 1 RX, 1e6 rays, <= 3 reflections + 1 diffraction):
-  A1 scene build -> A2-A7 launch (primary rays, events, Keller fans) -> A8 dedupe
-  -> A9-A10 refinement (when built).
-Multi-GPU (torchrun): scene replicated, rays i == rank (mod N), NCCL all-gather of events and of
-coarse records, global merge on every rank, refinement sharded by path.
-
-`value` = ray-bounces per second of the whole job (device time, inputs resident in HBM).
+Workload (default): BASELINE.json configs[4], "C5" — the reconstructed-room cloud (1e7 surfels,
+fitted normals, 879 RX), a FIXED lattice of 1e8 Fibonacci rays from one TX, <= 4 reflections,
+sharded i == rank (mod N) over the N GPUs (strong scaling: every N traces the same global set).
+One step = one pass of the whole hot path over that workload:
+  A1 scene build -> A2-A8 launch (primary rays, events/fans when the config has edges, dedupe,
+  NCCL all-gather + global merge for N > 1) -> A9-A10 refinement (sharded by path, refined
+  records all-gathered and merged).
+`value` = ray-bounces per second of the whole job (device time, inputs resident in HBM, max over
+ranks).  `--config C2` gives the secondary line (1e6 surfels, 1e6 rays, diffraction).
 `--impl reference` times the CPU oracle (oracle/) on a bounded sample of the same workload.
 """
 from __future__ import annotations
@@ -29,6 +30,10 @@ sys.path.insert(0, ROOT)
 METRIC = "ray-bounces/sec and refined paths/sec at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "ray-bounces/s"
 L2_FLUSH_BYTES = 512 << 20
+# FP64 operations per neighbourhood term (k_refine rows): a value pass (Eqs. 2-4:
+# difference 3, squared distance 5, weight 1 + exp 22, sums W/P/N 13) and a derivative pass of
+# the analytic Jacobian (the same 31 + W, sum w d, sum w d d^T, sum w n, sum w n d^T = 43)
+FLOPS_VALUE, FLOPS_DERIV = 44, 74
 
 
 def peaks():
@@ -104,11 +109,33 @@ def dist_env():
     return world, rank, local
 
 
-class Runner:
-    """One hot-path step on this rank, device-resident inputs.  Weak scaling: the Fibonacci
-    lattice has n_rays x world directions, rank r traces i == r (mod world)."""
+def max_over_ranks(world, *vals):
+    """Element-wise max of host floats over the ranks (NCCL all-reduce)."""
+    if world == 1:
+        return list(vals)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(list(vals), dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
 
-    def __init__(self, N, case, world, rank, stream, refine_on):
+
+def sum_over_ranks(world, *vals):
+    if world == 1:
+        return list(vals)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(list(vals), dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(x) for x in t.tolist()]
+
+
+class Runner:
+    """One hot-path step on this rank, inputs resident in device memory.  Strong scaling: the
+    lattice has case.n_rays directions for every N, rank r traces i == r (mod N); weak: the
+    lattice grows to n_rays x N."""
+
+    def __init__(self, N, case, world, rank, stream, scaling):
         import torch
         self.N, self.case, self.world, self.rank, self.stream = N, case, world, rank, stream
         s = case.scene
@@ -118,16 +145,15 @@ class Runner:
         self.pts, self.nrm, self.rad, self.lab = t(s.points), t(s.normals), t(s.radii), t(s.labels)
         self.tx = t(case.tx)
         self.rx = t(case.rx.reshape(-1, 3))
-        self.n_rays = case.n_rays * world
-        self.refine_on = refine_on
+        self.n_rays = case.n_rays * (world if scaling == "weak" else 1)
         self.desc = dict(kappa=case.kappa, tau=case.tau, c_R=case.c_R, dphi_deg=case.dphi_deg,
                          theta_ex_deg=case.theta_ex_deg, edge_bin=case.edge_bin)
         self.rdesc = dict(xi=case.xi, r_s=case.r_s, tau=case.tau, theta_ex_deg=case.theta_ex_deg)
 
     def step(self, counters=0):
-        import torch
         from paper_2403_06648_b200 import dist as D
         N, c = self.N, self.case
+        import torch
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record(self.stream)
         sc = N.nrt_scene_build_ex(self.pts, self.nrm, c.voxel, radii=self.rad, labels=self.lab,
@@ -143,92 +169,111 @@ class Runner:
                 has_edges=len(c.scene.edges) > 0, device=self.dev, stream=self.stream,
                 counters=counters, **self.desc)
         ev[2].record(self.stream)
-        refined, rinfo = None, None
-        if self.refine_on:
-            refined, rinfo = D.refine_distributed(N, sc, coarse, c.tx, c.rx, self.rank, self.world,
-                                                  device=self.dev, stream=self.stream, **self.rdesc)
+        refined, rinfo = D.refine_distributed(N, sc, coarse, c.tx, c.rx, self.rank, self.world,
+                                              device=self.dev, stream=self.stream,
+                                              counters=counters, **self.rdesc)
         ev[3].record(self.stream)
         ev[3].synchronize()
         out = {
             "phase_ms": [round(ev[i].elapsed_time(ev[i + 1]), 3) for i in range(3)],
             "bounces": info["bounces"],
             "coarse": coarse.count(),
-            "refined": refined.count() if refined is not None else 0,
+            "refined": refined.count(),
             "ms_trace": info["ms_trace"],
             "ms_fans": info["ms_fans"],
-            "tests": info["surfel_tests"],
-            "cells": info["cells_visited"],
-            "nonempty": info["cells_nonempty"],
+            "ms_refine": rinfo["ms_refine"],
+            "refine_paths": rinfo["n_raw"],
+            "mls_value": rinfo["mls_value"],
+            "mls_deriv": rinfo["mls_deriv"],
             "n_events": info["n_events"],
             "n_fan_rays": info["n_fan_rays"],
-            "scene": sc.info(),
-            "refined_info": rinfo,
         }
         for h in (refined, coarse, sc):
-            if h is not None:
-                h.free()
+            h.free()
         return out
 
 
-def e2e_step(N, case, host, stream, refine_on):
-    """The public API with HOST buffers: H2D of the cloud inside the build, D2H of results."""
+def e2e_step(N, case, host, n_rays, world, rank, stream):
+    """The public API with HOST buffers (pinned): H2D of the cloud inside the build, the
+    distributed launch + refinement, D2H of the global refined set."""
+    from paper_2403_06648_b200 import dist as D
+    import torch
     sc = N.nrt_scene_build_ex(host["p"], host["n"], case.voxel, radii=host["r"],
                               labels=host["l"], edges=case.scene.edges, stream=stream)
-    coarse = N.launch_case(sc, case, stream=stream)
-    rec = coarse.export()
-    out_b = rec.nbytes
-    if refine_on:
-        ref = N.nrt_refine_ex(sc, coarse, xi=case.xi, r_s=case.r_s, tau=case.tau, stream=stream)
-        out_b += ref.export().nbytes
-    return coarse.info()["bounces"], out_b
+    desc = dict(kappa=case.kappa, tau=case.tau, c_R=case.c_R, dphi_deg=case.dphi_deg,
+                theta_ex_deg=case.theta_ex_deg, edge_bin=case.edge_bin)
+    if world == 1:
+        coarse = N.nrt_launch_ex(sc, case.tx, case.rx, n_rays, case.max_refl, case.max_diff,
+                                 stream=stream, **desc)
+    else:
+        coarse, _ = D.launch_distributed(N, sc, case.tx, case.rx, n_rays, case.max_refl,
+                                         case.max_diff, rank, world,
+                                         has_edges=len(case.scene.edges) > 0,
+                                         device=torch.device("cuda", torch.cuda.current_device()),
+                                         stream=stream, **desc)
+    b = coarse.info()["bounces"]
+    ref, _ = D.refine_distributed(N, sc, coarse, case.tx, case.rx, rank, world,
+                                  device=torch.device("cuda", torch.cuda.current_device()),
+                                  stream=stream, xi=case.xi, r_s=case.r_s, tau=case.tau,
+                                  theta_ex_deg=case.theta_ex_deg)
+    out = ref.export()  # D2H of the result
+    for h in (ref, coarse, sc):
+        h.free()
+    return b, out.nbytes
 
 
 # ------------------------------------------------------------------------------------------
-def cpu_baseline(case, seconds=15.0):
-    """The oracle as it stands, on this host's cores (processes over a ray sample)."""
-    import multiprocessing as mp
-    from oracle import oracle as O
-    O.lib()
-    P = os.cpu_count() or 1
-    # calibrate: rays per second per core on a handful of rays
-    ids = np.arange(0, case.n_rays, max(1, case.n_rays // 997), dtype=np.uint64)
-    t0 = time.perf_counter()
-    _, _, nb = O.trace_rays(case, ids[:2])
-    dt = max(1e-3, time.perf_counter() - t0)
-    per_ray = dt / 2
-    n_per = max(1, int(seconds / per_ray))
-    sample = np.linspace(0, case.n_rays - 1, n_per * P).astype(np.uint64)
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(P) as pool:
-        res = pool.map(_oracle_chunk, [(case, sample[k::P]) for k in range(P)])
-    wall = time.perf_counter() - t0
-    bounces = sum(r for r in res)
-    # the single-threaded oracle on one core (SURVEY §8(d) asks for both rates)
-    one = sample[:: max(1, len(sample) // max(1, int(3.0 / per_ray)))][: max(1, int(3.0 / per_ray))]
-    t1 = time.perf_counter()
-    nb1 = _oracle_chunk((case, one))
-    one_core = nb1 / max(1e-9, time.perf_counter() - t1)
-    return {"value": bounces / wall, "unit": UNIT, "cores": P, "kind": "oracle",
-            "value_1core": one_core,
-            "sample": f"{len(sample)} primary rays of {case.name} (evenly spaced lattice ids, "
-                      f"brute force over {case.scene.n} surfels, no fans), {wall:.1f} s wall on "
-                      f"{P} processes"}
+def oracle_voxel(case):
+    """The oracle's own tier-1 grid cell (independent of the GPU's voxel)."""
+    return 0.03 if case.name in ("C4", "C5") else 0.05
 
 
 def _oracle_chunk(args):
     case, ids = args
     from oracle import oracle as O
-    _, _, nb = O.trace_rays(case, ids)
+    _, _, nb = O.trace_rays(case, ids, scene=O._FORK.get("scene"))
     return nb
 
 
-def run_config(case, world):
-    """The `config` object of both arms' JSON lines (same workload description)."""
+def cpu_baseline(case, seconds=15.0):
+    """The oracle as it stands (tier-1 grid, oracle/grid.c) on this host's cores: forked
+    processes over an evenly spaced sample of the lattice's primary rays."""
+    import multiprocessing as mp
+    from oracle import oracle as O
+    O.lib()
+    P = os.cpu_count() or 1
+    O._FORK["scene"] = O.OracleScene(case.scene, grid_voxel=oracle_voxel(case))
+    ids = np.arange(0, case.n_rays, max(1, case.n_rays // 997), dtype=np.uint64)
+    t0 = time.perf_counter()
+    nb0 = _oracle_chunk((case, ids[:64]))
+    per_bounce = max(1e-9, (time.perf_counter() - t0) / max(1, nb0))
+    n_rays = max(P, int(seconds * P / (per_bounce * (case.max_refl + 1))))
+    sample = np.linspace(0, case.n_rays - 1, n_rays).astype(np.uint64)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(P) as pool:
+        res = pool.map(_oracle_chunk, [(case, sample[k::P]) for k in range(P)])
+    wall = time.perf_counter() - t0
+    bounces = sum(res)
+    one = sample[: max(1, len(sample) // (4 * P))]
+    t1 = time.perf_counter()
+    nb1 = _oracle_chunk((case, one))
+    one_core = nb1 / max(1e-9, time.perf_counter() - t1)
+    O._FORK.pop("scene", None)
+    return {"value": bounces / wall, "unit": UNIT, "cores": P, "kind": "oracle",
+            "value_1core": one_core,
+            "sample": f"{len(sample)} primary rays of {case.name}'s lattice (evenly spaced ids; "
+                      f"tier-1 grid oracle over {case.scene.n} surfels, {len(case.rx)} RX; "
+                      f"coarse tracing only), {wall:.1f} s wall on {P} processes"}
+
+
+def run_config(case, world, scaling):
+    n_total = case.n_rays * (world if scaling == "weak" else 1)
     return {"workload": f"{case.name}: {case.scene.name}, 1 TX/{len(case.rx)} RX, "
-                        f"{case.n_rays} rays per GPU, max_refl {case.max_refl}, "
-                        f"max_diff {case.max_diff}; step = scene build + launch + refine",
-            "voxel_m": case.voxel, "n_rays_total": case.n_rays * world,
+                        f"{n_total} rays in total ({scaling} scaling over {world} GPU(s)), "
+                        f"max_refl {case.max_refl}, max_diff {case.max_diff}; "
+                        f"step = scene build + launch + refine",
+            "voxel_m": case.voxel, "n_rays_total": n_total,
             "l2": "512 MiB write between steps (outside the timed events)",
             "parallelism": f"dp{world}: rays i == rank mod {world}, paths j == rank mod "
                            f"{world}, NCCL all-gather of events/coarse/refined records"}
@@ -242,7 +287,8 @@ def run_reference(args, case):
     O.lib()
     import multiprocessing as mp
     P = os.cpu_count() or 1
-    rays_per_step = 8 * P
+    O._FORK["scene"] = O.OracleScene(case.scene, grid_voxel=oracle_voxel(case))
+    rays_per_step = 512 * P
     times, bounces = [], []
     ctx = mp.get_context("fork")
     with ctx.Pool(P) as pool:
@@ -258,13 +304,14 @@ def run_reference(args, case):
     value = sum(bounces) / sum(times)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
-            "config": dict(run_config(case, world),
+            "config": dict(run_config(case, world, args.scaling),
                            sample=f"oracle: {rays_per_step} primary rays of the lattice per step"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "oracle",
-                             "sample": f"{rays_per_step} primary rays per step of {case.name}, "
-                                       f"brute force over {case.scene.n} surfels"},
+                             "sample": f"{rays_per_step} primary rays per step of {case.name} "
+                                       f"(tier-1 grid oracle over {case.scene.n} surfels, "
+                                       f"coarse tracing only)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -276,7 +323,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="nrt", choices=["nrt", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--sigma", type=float, default=0.010)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -297,8 +345,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
-    refine_on = os.environ.get("NRT_BENCH_REFINE", "1") == "1"
-    R = Runner(N, case, world, rank, stream, refine_on)
+    R = Runner(N, case, world, rank, stream, args.scaling)
 
     # the L2-flush buffer exists before the warm-up, so that the memory pools are in their
     # steady state when the timed steps start
@@ -307,7 +354,7 @@ def main():
         flush.fill_(float(k))
         R.step()
     torch.cuda.synchronize()
-    cnt = R.step(counters=1)  # instrumented (untimed): algorithmic byte counts
+    cnt = R.step(counters=1)  # instrumented (untimed): algorithmic byte and FLOP counts
     torch.cuda.synchronize()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -328,69 +375,71 @@ def main():
         torch.distributed.barrier()
     launches = (N.nrt_kernel_launches() - launches0) / args.steps
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
-    bounces = outs[-1]["bounces"]
-    refined = outs[-1]["refined"]
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([total_ms, float(bounces)], dtype=torch.float64, device="cuda")
-        tl = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(tl, t)
-        total_ms = max(float(x[0]) for x in tl)
-        bounces = sum(int(x[1]) for x in tl)
+    total_ms = max_over_ranks(world, sum(step_ms))[0]
+    bounces = int(sum_over_ranks(world, float(outs[-1]["bounces"]))[0])
     value = bounces * args.steps / (total_ms / 1000.0)
-
-    # ---- roofline of the dominant kernel (primary traversal k_primary)
-    hbm, src = peaks()
-    prim_bytes = 32 * cnt["tests"] + 8 * cnt["cells"]
     ms_trace = statistics.mean(o["ms_trace"] for o in outs)
     ms_fans = statistics.mean(o["ms_fans"] for o in outs)
-    ms_refine = statistics.mean((o["refined_info"] or {}).get("ms_refine", 0.0) for o in outs)
-    # counters cover primary + fans together; split by kernel time share is not exact, so the
-    # primary kernel's bytes come from a primary-only instrumented launch below
+    ms_refine = statistics.mean(o["ms_refine"] for o in outs)
+
+    # ---- rooflines: the traversal (HBM, BJ's "% of HBM roofline") and the refinement (FP64)
+    hbm, src = peaks()
     prim_only = prim_counts(N, R, case)
-    post = post_timing(N, R, case) if refine_on else None
     pb = 32 * prim_only["tests"] + 8 * prim_only["cells"]
     achieved = pb / (ms_trace / 1000.0) / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": measured_traffic(case.name),
-            "kernel": "k_trace (primary bounces)",
-            "peak_source": src,
-            "bytes_per_launch": pb, "bytes_per_bounce": pb / max(1, prim_only["bounces"]),
-            "ms_per_launch": ms_trace}
+    roof_trace = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                  "frac": achieved / hbm, "traffic": measured_traffic(case.name),
+                  "kernel": "k_trace (primary bounces)", "peak_source": src,
+                  "bytes_per_launch": pb, "bytes_per_bounce": pb / max(1, prim_only["bounces"]),
+                  "ms_per_launch": ms_trace}
+    fp64 = N.nrt_probe_fp64_tflops(local)
+    flops = FLOPS_VALUE * cnt["mls_value"] + FLOPS_DERIV * cnt["mls_deriv"]
+    ach_f = flops / (ms_refine / 1000.0) / 1e12 if ms_refine else 0.0
+    roof_refine = {"bound": "alu", "achieved": ach_f, "peak": fp64, "unit": "TFLOP/s",
+                   "frac": ach_f / fp64 if fp64 > 0 else None, "traffic": None,
+                   "kernel": "k_refine_w (FP64 Gauss-Newton, one warp per path)",
+                   "peak_source": "measured FP64 FMA probe (nrt_probe_fp64_tflops); nominal "
+                                  "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s",
+                   "flops_per_launch": flops, "ms_per_launch": ms_refine,
+                   "mls_terms": [cnt["mls_value"], cnt["mls_deriv"]]}
+    dominant_refine = ms_refine > ms_trace + ms_fans
+    roof = roof_refine if dominant_refine else roof_trace
+    post = post_timing(N, R, case) if world == 1 else None
 
-    # ---- e2e through the public API with host (pinned) buffers
+    # ---- e2e through the public API with host (pinned) buffers, every rank
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
         s = case.scene
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
         host = {"p": pin(s.points), "n": pin(s.normals), "r": pin(s.radii), "l": pin(s.labels)}
         h2d = sum(v.nbytes for v in host.values()) + case.rx.nbytes + case.tx.nbytes
-        e2e_step(N, case, host, stream, refine_on)
+        e2e_step(N, case, host, R.n_rays, world, rank, stream)
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
         tot_b, d2h = 0, 0
         for _ in range(args.steps):
-            b, ob = e2e_step(N, case, host, stream, refine_on)
+            b, ob = e2e_step(N, case, host, R.n_rays, world, rank, stream)
             tot_b += b
             d2h = ob
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
+        dt = max_over_ranks(world, time.perf_counter() - t0)[0]
+        tot_b = int(sum_over_ranks(world, float(tot_b))[0])
         e2e = {"value": tot_b / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000 * dt / args.steps}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": run_config(case, world),
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": run_config(case, world, args.scaling),
         # refined paths/s: coarse paths refined (the refinement's input rate, as the paper's
         # Table IV refine times count) per second of the whole step, and of the refine kernel
-        "refined_paths_per_s": (outs[-1]["coarse"] * args.steps / (total_ms / 1000.0))
-        if refine_on else None,
-        "refine_kernel_paths_per_s": (outs[-1]["coarse"] / (ms_refine / 1000.0))
-        if refine_on and ms_refine else None,
-        "coarse_paths": outs[-1]["coarse"], "refined_valid_paths": refined,
+        "refined_paths_per_s": outs[-1]["coarse"] * args.steps / (total_ms / 1000.0),
+        "refine_kernel_paths_per_s": (outs[-1]["refine_paths"] / (ms_refine / 1000.0))
+        if ms_refine else None,
+        "coarse_paths": outs[-1]["coarse"], "refined_valid_paths": outs[-1]["refined"],
         "breakdown_ms": {"trace": ms_trace, "fans": ms_fans, "refine": ms_refine,
                          "step": total_ms / args.steps},
         "n_events": outs[-1]["n_events"], "n_fan_rays": outs[-1]["n_fan_rays"],
@@ -398,6 +447,8 @@ def main():
         "step_ms": [round(x, 3) for x in step_ms],
         "phase_ms_build_launch_refine": [o["phase_ms"] for o in outs],
         "roofline": roof,
+        "roofline_trace": roof_trace,
+        "roofline_refine": roof_refine,
         # NEXT-3 post-processing (not a §8(a) row: timed separately, outside the step)
         "postprocess": post,
         "gpu_launches": int(launches),
@@ -418,10 +469,7 @@ def post_timing(N, R, case, reps=3):
     sc = N.nrt_scene_build_ex(R.pts, R.nrm, case.voxel, radii=R.rad, labels=R.lab,
                               edges=case.scene.edges, stream=R.stream)
     coarse = N.nrt_launch_ex(sc, R.tx, R.rx, R.n_rays, case.max_refl, case.max_diff,
-                             rank=R.rank, world=R.world, stream=R.stream, **R.desc) \
-        if R.world == 1 else None
-    if coarse is None:
-        return None
+                             stream=R.stream, **R.desc)
     ref = N.nrt_refine_ex(sc, coarse, stream=R.stream, **R.rdesc)
     ms, n_out = [], 0
     for _ in range(reps):
@@ -437,22 +485,26 @@ def post_timing(N, R, case, reps=3):
 
 
 def measured_traffic(workload):
-    """DRAM bytes (read + write) per launch of the dominant kernel from the committed ncu
-    capture (profiles/r01_traffic.json, scripts/gpu_traffic.sh), or None."""
-    try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
-        return float(t[workload]["dram_bytes_per_launch"])
-    except Exception:
-        return None
+    """DRAM bytes (read + write) per launch of the traversal kernel from the committed ncu
+    capture (profiles/r02_traffic.json, else r01), or None."""
+    for name in ("r02_traffic.json", "r01_traffic.json"):
+        try:
+            t = json.load(open(os.path.join(ROOT, "profiles", name)))
+            return float(t[workload]["dram_bytes_per_launch"])
+        except Exception:
+            continue
+    return None
 
 
 def prim_counts(N, R, case):
-    """Instrumented primary-only launch (stage 1: no fans) for the k_primary byte count."""
+    """Instrumented primary-only launch (stage 1: no fans) for the k_trace byte count."""
     sc = N.nrt_scene_build_ex(R.pts, R.nrm, case.voxel, radii=R.rad, labels=R.lab,
                               edges=case.scene.edges, stream=R.stream)
     p = N.nrt_launch_ex(sc, R.tx, R.rx, R.n_rays, case.max_refl, case.max_diff, counters=1,
                         stage=1, rank=R.rank, world=R.world, stream=R.stream, **R.desc)
     i = p.info()
+    p.free()
+    sc.free()
     return {"tests": i["surfel_tests"], "cells": i["cells_visited"], "bounces": i["bounces"]}
 
 

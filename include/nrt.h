@@ -156,6 +156,9 @@ typedef struct {
     int32_t blocks_per_sm; /* 0 = as many resident path blocks per SM as fit; k > 0 caps it
                              (leaves room for kernels running concurrently on other streams) */
     void* stream;
+    int32_t counters;     /* 1 = also count the MLS candidate evaluations (nrt_paths_info
+                             mls_value / mls_deriv: the algorithmic FP64 work); results are
+                             unchanged */
 } nrt_refine_desc;
 void nrt_refine_desc_default(nrt_refine_desc* d);
 nrt_status nrt_refine(nrt_scene s, nrt_paths coarse, nrt_paths* refined_out);
@@ -230,6 +233,9 @@ typedef struct {
     float ms_dedupe;         /* device time of event + record dedupe */
     float ms_refine;         /* device time of the refinement kernels */
     float ms_total;          /* device time of the whole call */
+    uint64_t mls_value;      /* refine with counters = 1: surfel terms of Eqs. 2-4 evaluated
+                                (neighbourhood members within 4 sigma, value passes) */
+    uint64_t mls_deriv;      /* idem, derivative passes of the analytic Jacobian (R37) */
 } nrt_paths_info;
 
 /* ---------------------------------------------------------------------------------------
@@ -285,6 +291,10 @@ uint64_t nrt_kernel_launches(void);
 /* Bytes of device memory the library keeps cached between launches (wavefront workspaces:
  * per-ray state of the rays in flight, up to ~300 B x 2^24 rays), and a call that returns
  * all idle cached blocks to the CUDA memory pool.  Must not race with a running launch. */
+/* Diagnostic: FP64 fused multiply-add throughput of this device, TFLOP/s (2 flops per FMA),
+ * measured by a synthetic kernel of independent FMA chains (~20 ms).  The roofline denominator
+ * of the FP64-bound refinement kernel (bench.py).  <= 0 on failure. */
+double nrt_probe_fp64_tflops(int device);
 uint64_t nrt_workspace_bytes(void);
 void nrt_workspace_trim(void);
 

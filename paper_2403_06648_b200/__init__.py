@@ -72,7 +72,7 @@ class nrt_refine_desc(C.Structure):
                 ("delta", C.c_double), ("tau", C.c_double), ("theta_ex_deg", C.c_double),
                 ("rank", C.c_int32), ("world", C.c_int32), ("keep_invalid", C.c_int32),
                 ("select", C.c_int32), ("blocks_per_sm", C.c_int32),
-                ("stream", C.c_void_p)]
+                ("stream", C.c_void_p), ("counters", C.c_int32)]
 
 
 class nrt_paths_info(C.Structure):
@@ -81,7 +81,8 @@ class nrt_paths_info(C.Structure):
                 ("surfel_tests", C.c_uint64), ("cells_visited", C.c_uint64),
                 ("cells_nonempty", C.c_uint64),
                 ("ms_trace", C.c_float), ("ms_fans", C.c_float), ("ms_dedupe", C.c_float),
-                ("ms_refine", C.c_float), ("ms_total", C.c_float)]
+                ("ms_refine", C.c_float), ("ms_total", C.c_float),
+                ("mls_value", C.c_uint64), ("mls_deriv", C.c_uint64)]
 
 
 COARSE_REC = np.dtype([
@@ -134,6 +135,7 @@ _SIGS = {
     "nrt_last_error": ([], C.c_char_p),
     "nrt_version": ([], C.c_char_p),
     "nrt_kernel_launches": ([], C.c_uint64),
+    "nrt_probe_fp64_tflops": ([C.c_int], C.c_double),
     "nrt_workspace_bytes": ([], C.c_uint64),
     "nrt_workspace_trim": ([], None),
 }
@@ -480,6 +482,10 @@ def nrt_version() -> str:
 
 def nrt_kernel_launches() -> int:
     return int(lib().nrt_kernel_launches())
+
+
+def nrt_probe_fp64_tflops(device=0) -> float:
+    return float(lib().nrt_probe_fp64_tflops(int(device)))
 
 
 def nrt_workspace_bytes() -> int:

@@ -209,6 +209,8 @@ const char* nrt_last_error(void) { return g_err; }
 const char* nrt_version(void) { return "nrt 0.1 (sm_100a)"; }
 uint64_t nrt_kernel_launches(void) { return g_launches.load(); }
 
+double nrt_probe_fp64_tflops(int device) { return ::nrt::probe_fp64_tflops(device); }
+
 uint64_t nrt_workspace_bytes(void) {
     std::lock_guard<std::mutex> lk(g_ws_mu);
     uint64_t t = 0;

@@ -218,6 +218,7 @@ nrt_status debug_trace(nrt_scene s, const LaunchArgs& a, const uint64_t* ids, in
 float cos_ex_of(float theta_deg);
 float cRw_of(float c_R, int64_t n_rays);
 // refine.cu
+double probe_fp64_tflops(int device);
 nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
                   cudaStream_t st);
 }  // namespace nrt

@@ -71,6 +71,7 @@ struct RP {
     int keep_invalid;
     unsigned long long* work;
     long long* cycles;  // optional per-path latency (NRT_REFINE_TIMING diagnostics)
+    unsigned long long* mls_cnt;  // optional [value, deriv] neighbourhood terms evaluated
 };
 
 struct Path {
@@ -289,6 +290,7 @@ __device__ __noinline__ bool mls_w(const RP& P, const Path& D, int k, const doub
     const bool use_list = !V.direct && sqrt(dxc * dxc + dyc * dyc + dzc * dzc) <= P.mw;
     if (P.cycles && lane == 0) atomicAdd(&g_dbg[use_list ? 0 : 1], 1ull);
     const long long t_mls0 = P.cycles ? clock64() : 0;
+    unsigned terms = 0;  // neighbourhood members within 4 sigma evaluated by this lane
     if (use_list) {
         const int n = V.n, cap = P.capw;
         const double x0 = x[0], x1 = x[1], x2 = x[2];
@@ -305,6 +307,7 @@ __device__ __noinline__ bool mls_w(const RP& P, const Path& D, int k, const doub
             const double wa0 = exp_neg(-dda * inv2s2), wb0 = exp_neg(-ddb * inv2s2);
             const double wa = dda <= r2 ? wa0 : 0.0;
             const double wb = (has2 && ddb <= r2) ? wb0 : 0.0;
+            terms += (dda <= r2) + (has2 && ddb <= r2);
             const double na0 = list[3 * cap + j], na1 = list[4 * cap + j], na2 = list[5 * cap + j];
             const double nb0 = has2 ? list[3 * cap + j2] : 0.0, nb1 = has2 ? list[4 * cap + j2] : 0.0,
                          nb2 = has2 ? list[5 * cap + j2] : 0.0;
@@ -351,6 +354,7 @@ __device__ __noinline__ bool mls_w(const RP& P, const Path& D, int k, const doub
                     const double n0 = nv.x, n1 = nv.y, n2 = nv.z;
                     const double sg = ((n0 * ns[0] + n1 * ns[1]) + n2 * ns[2]) < 0.0 ? -1.0 : 1.0;
                     const double w = exp_neg(-dd * inv2s2);
+                    ++terms;
                     W += w;
                     Px += w * p0;
                     Py += w * p1;
@@ -360,6 +364,11 @@ __device__ __noinline__ bool mls_w(const RP& P, const Path& D, int k, const doub
                     Nz += w * (sg * n2);
                 }
             }
+    }
+    if (P.mls_cnt) {
+        unsigned t = terms;
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) atomicAdd(&P.mls_cnt[0], (unsigned long long)t);
     }
     W = wsum(W);
     Px = wsum(Px);
@@ -397,7 +406,9 @@ __device__ __noinline__ bool mls_w_d(const RP& P, const Path& D, int k, const do
     const double r2 = (4.0 * P.sigma) * (4.0 * P.sigma);
     double W = 0, D0 = 0, D1 = 0, D2 = 0, S00 = 0, S01 = 0, S02 = 0, S11 = 0, S12 = 0, S22 = 0;
     double N0 = 0, N1 = 0, N2 = 0, T[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    unsigned terms = 0;
     auto acc = [&](double d0, double d1, double d2, double dd, double n0, double n1, double n2) {
+        ++terms;
         const double w = exp_neg(-dd * inv2s2);
         const double w0 = w * d0, w1 = w * d1, w2 = w * d2;
         W += w;
@@ -460,6 +471,11 @@ __device__ __noinline__ bool mls_w_d(const RP& P, const Path& D, int k, const do
                         acc(d0, d1, d2, dd, sg * n0, sg * n1, sg * n2);
                     }
                 }
+    }
+    if (P.mls_cnt) {
+        unsigned t = terms;
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) atomicAdd(&P.mls_cnt[1], (unsigned long long)t);
     }
     W = wsum(W);
     D0 = wsum(D0);
@@ -1737,7 +1753,45 @@ __global__ void k_select_flags(const nrt_coarse_rec* in, int64_t n, int sel, uns
     }
 }
 
+// FP64 FMA throughput probe: 8 independent chains per thread, no memory traffic
+__global__ void k_fp64_probe(double* out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = threadIdx.x * 1e-9 + j;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = fma(x[j], a, b);
+    double s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += x[j];
+    if (s == 12345.678) out[0] = s;  // keeps the chains alive
+}
+
 }  // namespace
+
+double probe_fp64_tflops(int device) {
+    if (cudaSetDevice(device) != cudaSuccess) return -1.0;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    double* out = nullptr;
+    if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return -1.0;
+    const int iters = 4096, threads = 256, blocks = sms * 8;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_fp64_probe<<<blocks, threads>>>(out, 64, 0.999999, 1e-7);  // warm-up
+    cudaEventRecord(e0);
+    k_fp64_probe<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (cudaGetLastError() != cudaSuccess || !(ms > 0)) return -1.0;
+    return 2.0 * 8.0 * iters * (double)threads * blocks / (ms * 1e-3) / 1e12;
+}
 
 nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out, cudaStream_t st) {
     int64_t n = coarse->n;
@@ -1870,11 +1924,12 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     nrt_refined_rec* o = nullptr;
     NRT_CUDA(cudaMallocAsync(&o, (size_t)(n_mine > 0 ? n_mine : 1) * sizeof(nrt_refined_rec), st));
     unsigned long long* ctr = nullptr;
-    NRT_CUDA(cudaMallocAsync(&ctr, 2 * sizeof(unsigned long long), st));
-    NRT_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), st));
+    NRT_CUDA(cudaMallocAsync(&ctr, 4 * sizeof(unsigned long long), st));
+    NRT_CUDA(cudaMemsetAsync(ctr, 0, 4 * sizeof(unsigned long long), st));
     P.out = o;
     P.n_out = ctr;
     P.work = ctr + 1;
+    P.mls_cnt = d->counters ? ctr + 2 : nullptr;
     const bool timing = getenv("NRT_REFINE_TIMING") != nullptr && d->keep_invalid;
     if (timing) {
         NRT_CUDA(cudaMallocAsync(&P.cycles, (size_t)(n_mine > 0 ? n_mine : 1) * 8, st));
@@ -1894,9 +1949,12 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     cudaEventRecord(e1, st);
     NRT_CUDA(cudaGetLastError());
     cudaFreeAsync(scratch, st);
-    unsigned long long n_ok = 0;
-    NRT_CUDA(cudaMemcpyAsync(&n_ok, ctr, sizeof(n_ok), cudaMemcpyDeviceToHost, st));
+    unsigned long long hctr[4] = {0, 0, 0, 0};
+    NRT_CUDA(cudaMemcpyAsync(hctr, ctr, sizeof(hctr), cudaMemcpyDeviceToHost, st));
     NRT_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long n_ok = hctr[0];
+    out->info.mls_value = hctr[2];
+    out->info.mls_deriv = hctr[3];
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);

@@ -23,9 +23,13 @@ def shard_count(n: int, rank: int, world: int) -> int:
 
 def allgather_bytes(t, group=None):
     """All-gather variable-length 1-D uint8 tensors: exchange the lengths, then one padded
-    all_gather_into_tensor (a single NCCL collective), concatenated in rank order."""
+    all_gather_into_tensor (a single NCCL collective), concatenated in rank order.  With the
+    gloo backend (CPU plumbing tests, several ranks on one GPU) device tensors are staged
+    through the host and the result returned on the input's device."""
     import torch
     import torch.distributed as dist
+    if t.device.type == "cuda" and dist.get_backend(group) == "gloo":
+        return allgather_bytes(t.cpu(), group).to(t.device)
     world = dist.get_world_size(group)
     n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
     ns = [torch.zeros_like(n) for _ in range(world)]
@@ -60,12 +64,11 @@ def records_tensor(paths, device):
 def launch_distributed(N, scene, tx, rx, n_rays, max_refl, max_diff, rank, world, *, has_edges,
                        group=None, device="cuda", stream=None, counters=0, **desc):
     """Coarse launch over `world` ranks -> (global coarse set on every rank, local launch info)."""
-    import torch
     has_diff = max_diff > 0 and has_edges
     local = N.nrt_launch_ex(scene, tx, rx, n_rays, max_refl, max_diff, rank=rank, world=world,
                             stage=1 if has_diff else 0, counters=counters, stream=stream, **desc)
     if has_diff:
-        ev = torch.from_numpy(local.export_events().view(np.uint8)).to(device)
+        ev = local.export_events(device=device)  # device-to-device copy of the stage-1 events
         evall = allgather_bytes(ev, group)
         N.nrt_launch_fans(scene, local, evall, rank=rank, world=world, stream=stream, **desc)
     info = local.info()

@@ -21,7 +21,7 @@ def N():
 def header_functions():
     src = open(os.path.join(ROOT, "include", "nrt.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(nrt_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(nrt_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol(N):
