@@ -58,6 +58,33 @@ void ensure_pool(int dev) {
     done.fetch_or(bit);
 }
 
+// Keep the stream-ordered pool's physical backing at 1.5x the high-water mark of its use: a pool
+// that must grow inside a step maps new pages there (measured on C5: scene builds of 0.1-1.5 s
+// instead of 6 ms in 4 of 10 steps); one reservation after the first large call removes that.
+void pool_keep_headroom(int dev, cudaStream_t st) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t reserved = 0, used = 0, high = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    uint64_t target = high + high / 2;
+    if (target > total_b / 2) target = total_b / 2;  // never more than half of the device
+    if (reserved >= target || target <= used) return;
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, (size_t)(target - used), st) == cudaSuccess) {
+        cudaFreeAsync(p, st);
+    } else {
+        cudaGetLastError();
+    }
+    // the reservation itself is not use: restore the high-water mark to the real one
+    cudaStreamSynchronize(st);
+    uint64_t zero = 0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
+}
+
 namespace {
 struct WsBlock {
     int dev;
@@ -464,6 +491,7 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
         return rc;
     }
     P->info.ms_total = total.stop();
+    pool_keep_headroom(s->device, st);
     *out = P;
     return NRT_OK;
 }
@@ -625,6 +653,7 @@ nrt_status nrt_refine_ex(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d
     P->rx = coarse->rx;
     P->info.kind = NRT_PATHS_REFINED;
     nrt_status rc = refine(s, coarse, &d, P, (cudaStream_t)d.stream);
+    if (rc == NRT_OK) pool_keep_headroom(s->device, (cudaStream_t)d.stream);
     if (rc != NRT_OK) {
         nrt_paths_free(P);
         return rc;

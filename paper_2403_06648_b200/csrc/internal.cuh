@@ -21,6 +21,7 @@ nrt_status set_error(nrt_status st, const char* fmt, ...);
 void clear_error();
 void count_launch();  // every kernel launch of the library increments a process-wide counter
 void ensure_pool(int dev);  // default mempool keeps freed memory cached
+void pool_keep_headroom(int dev, cudaStream_t st);  // pool backing >= 1.5x its high-water mark
 // Workspace cache for large per-launch buffers (wavefront state).  Growing the stream-ordered
 // pool by gigabytes maps fresh physical pages (~50 ms/GB measured), so the biggest buffers are
 // kept across launches: ws_get returns an idle cached block of >= bytes on dev (or a new one);

@@ -202,18 +202,27 @@ __device__ __forceinline__ double exp_neg(double x) {
     return __hiloint2double(__double2hiint(w) + ((k >> 5) << 20), __double2loint(w));
 }
 
-// candidate list of one reflection vertex in the warp kernel's global scratch: FP64 SoA,
+// list element type: the surfel inputs are float, so float storage is exact (the conversion to
+// double happens at use); NRT_LIST_F64=1 stores them pre-converted (twice the L2 footprint;
+// measured: no faster)
+#if defined(NRT_LIST_F64) && NRT_LIST_F64
+typedef double lst_t;
+#else
+typedef float lst_t;
+#endif
+
+// candidate list of one reflection vertex in the warp kernel's global scratch: SoA,
 // rows (p.x, p.y, p.z, s n.x, s n.y, s n.z) of capw entries, s = sgn(n . n_seed) folded in at
 // gather time (the Eq. 3 + R20 orientation is fixed per vertex), so an MLS evaluation does no
 // float->double conversion and no orientation test.
-__device__ __forceinline__ double* wlist(double* cand, int slot, int capw) {
+__device__ __forceinline__ lst_t* wlist(lst_t* cand, int slot, int capw) {
     return cand + (size_t)slot * 6 * capw;
 }
 
 // warp gather of the label's surfels within 4 sigma + mw of c (home cells in linear order,
 // records of a cell in order, compacted by a warp prefix sum over rounds of 32 cells)
 __device__ __noinline__ void gather_w(const RP& P, int32_t label, const double ns[3], const double c[3],
-                                      double* list, Vtx& V, int lane) {
+                                      lst_t* list, Vtx& V, int lane) {
     if (lane == 0) {
         V.c[0] = c[0];
         V.c[1] = c[1];
@@ -281,7 +290,7 @@ __device__ __noinline__ void gather_w(const RP& P, int32_t label, const double n
 // MLS (Eqs. 1-4) at x, one warp: from the vertex's FP64 list when x lies within mw of its
 // gather centre (the list then holds every label surfel within 4 sigma of x), else by a direct
 // scan of the home grid.  Two candidates per lane per round (independent exp chains).
-__device__ __noinline__ bool mls_w(const RP& P, const Path& D, int k, const double x[3], const double* list,
+__device__ __noinline__ bool mls_w(const RP& P, const Path& D, int k, const double x[3], const lst_t* list,
                                    const Vtx& V, double pb[3], double nb[3], int lane) {
     const double inv2s2 = 1.0 / (2.0 * P.sigma * P.sigma);
     const double r2 = (4.0 * P.sigma) * (4.0 * P.sigma);
@@ -399,7 +408,7 @@ __device__ __noinline__ bool mls_w(const RP& P, const Path& D, int k, const doub
 //   dpbar/dx = (sum w d d^T / s^2 - (pbar - x) dW^T) / W,  dW = sum w d / s^2,  pbar - x = sum w d / W;
 //   dnbar/dx = (I - nbar nbar^T)(sum w sn d^T / s^2) / |N|,  N = sum w sn  (sn: oriented normal).
 // 22 sums in one pass over the same neighbourhood as mls_w (list or direct rows).
-__device__ __noinline__ bool mls_w_d(const RP& P, const Path& D, int k, const double x[3], const double* list,
+__device__ __noinline__ bool mls_w_d(const RP& P, const Path& D, int k, const double x[3], const lst_t* list,
                                      const Vtx& V, double dP[3][3], double dN[3][3], int lane) {
     const double s2 = P.sigma * P.sigma;
     const double inv2s2 = 1.0 / (2.0 * s2);
@@ -587,7 +596,7 @@ __device__ __forceinline__ bool vertex_residual_w(const RP& P, const Path& D, co
 }
 
 // residual_all() of the warp kernel (MLS from the FP64 lists)
-__device__ __noinline__ void residual_all_w(const RP& P, const Path& D, const double* z, double* cand,
+__device__ __noinline__ void residual_all_w(const RP& P, const Path& D, const double* z, lst_t* cand,
                                             const Vtx* V, Trial& T, int lane) {
     bool ok = true;
     double pb[3], nb[3];
@@ -733,7 +742,7 @@ __device__ bool jac_vertex(const RP& P, const Path& D, const double* z, int k, c
 
 // the whole Jacobian at z by one warp: the derivative MLS of every reflection vertex (22 sums,
 // warp-wide), then lane k assembles the rows of vertex k.  dPN: scratch [NRT_MAX_INT][18].
-__device__ __noinline__ bool jacobian_w(const RP& P, const Path& D, const double* z, double* cand, const Vtx* V,
+__device__ __noinline__ bool jacobian_w(const RP& P, const Path& D, const double* z, lst_t* cand, const Vtx* V,
                                        const double (*pb)[3], const double (*nb)[3], double (*dPN)[18],
                                        double* J, int m, int lane) {
     for (int k = 0; k < D.n; ++k) {
@@ -771,7 +780,7 @@ __device__ __noinline__ bool jacobian_w(const RP& P, const Path& D, const double
 // squared residuals exceeds the bound (every term is non-negative, so the full sum would too; the
 // 1e-12 relative guard is far above the rounding of <= 24 terms).  A trial evaluated to the end
 // gets T.r, T.pb/nb and f summed in index order, exactly as residual_all_w.
-__device__ __noinline__ bool trial_w(const RP& P, const Path& D, const double* z, double* cand,
+__device__ __noinline__ bool trial_w(const RP& P, const Path& D, const double* z, lst_t* cand,
                                      const Vtx* V, Trial& T, const int* order, double bound, int lane) {
     double part = 0.0;
     for (int q = 0; q < D.n; ++q) {
@@ -1114,13 +1123,13 @@ struct WS {  // one warp's path state in shared memory (J and A follow all WS, s
     int order[NRT_MAX_INT];  // backtracking: vertex evaluation order (cheap / far first)
 };
 
-__global__ void __launch_bounds__(32 * kWPB, NRT_WMINB) k_refine_w(RP P, double* scratch, int mmax) {
+__global__ void __launch_bounds__(32 * kWPB, NRT_WMINB) k_refine_w(RP P, lst_t* scratch, int mmax) {
     extern __shared__ __align__(16) unsigned char dyn[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WS& S = reinterpret_cast<WS*>(dyn)[wid];
     double* J = reinterpret_cast<double*>(dyn + kWPB * sizeof(WS)) + (size_t)wid * 2 * mmax * mmax;
     double* A = J + (size_t)mmax * mmax;
-    double* cand = scratch + (size_t)(blockIdx.x * kWPB + wid) * P.nv_max * P.capw * 6;
+    lst_t* cand = scratch + (size_t)(blockIdx.x * kWPB + wid) * P.nv_max * P.capw * 6;
     init_exp2();
     __syncthreads();
     const int64_t n_mine = P.n_in > P.rank ? (P.n_in - P.rank + P.world - 1) / P.world : 0;
@@ -1387,7 +1396,7 @@ struct Smem {
 
 // the residual at z by the whole block: MLS of reflection vertex k on warp k mod NW, vertex
 // residuals on warp 0 (the values residual_all_w gives).  Ends synced.
-__device__ void residual_coop_w(const RP& P, const Path& D, const double* z, double* cand, const Vtx* V,
+__device__ void residual_coop_w(const RP& P, const Path& D, const double* z, lst_t* cand, const Vtx* V,
                                 Trial& T, int* okv_s, int wid, int lane) {
     for (int k = wid; k < D.n; k += NW) {
         int ok = 1;
@@ -1421,11 +1430,11 @@ __device__ void residual_coop_w(const RP& P, const Path& D, const double* z, dou
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(32 * NW, 1) k_refine_b(RP P, double* scratch) {
+__global__ void __launch_bounds__(32 * NW, 1) k_refine_b(RP P, lst_t* scratch) {
     extern __shared__ __align__(16) unsigned char dyn[];
     Smem& S = *reinterpret_cast<Smem*>(dyn);
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-    double* cand = scratch + (size_t)blockIdx.x * P.nv_max * P.capw * 6;
+    lst_t* cand = scratch + (size_t)blockIdx.x * P.nv_max * P.capw * 6;
     init_exp2();
     __syncthreads();
     const int64_t n_mine = P.n_in > P.rank ? (P.n_in - P.rank + P.world - 1) / P.world : 0;
@@ -1914,8 +1923,8 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     const int64_t per_block = warp_impl ? kWPB : 1;  // paths in flight per block
     if (blocks > (n_mine + per_block - 1) / per_block) blocks = (n_mine + per_block - 1) / per_block;
     if (blocks < 1) blocks = 1;
-    double* scratch = nullptr;  // candidate lists: per warp (warp kernel) or per block
-    NRT_CUDA(cudaMallocAsync(&scratch, (size_t)blocks * per_block * nv * P.capw * 6 * sizeof(double), st));
+    lst_t* scratch = nullptr;  // candidate lists: per warp (warp kernel) or per block
+    NRT_CUDA(cudaMallocAsync(&scratch, (size_t)blocks * per_block * nv * P.capw * 6 * sizeof(lst_t), st));
     float* d_rx = nullptr;
     const size_t nrx = coarse->rx.size();
     NRT_CUDA(cudaMallocAsync(&d_rx, (nrx ? nrx : 3) * sizeof(float), st));

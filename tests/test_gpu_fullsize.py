@@ -92,7 +92,7 @@ def _tier0_shard(O, case, rank, world):
     return O.dedupe(raw, KAPPA_ALL), ev, sum(x[2] for x in parts)
 
 
-@pytest.mark.parametrize("name,rays", [("C2", 4000), ("C3", 300), ("C4", 300), ("C5", 200)])
+@pytest.mark.parametrize("name,rays", [("C2", 4000), ("C3", 300), ("C4", 300), ("C5", 1000)])
 def test_sharded_subset_vs_brute_force(N, O, name, rays):
     """A shard of the full-size lattice through the production path (stage 1) equals tier 0:
     every raw record (kappa = 2^30), the locally deduped events and the bounce count."""
