@@ -396,7 +396,8 @@ def main():
     flops = FLOPS_VALUE * cnt["mls_value"] + FLOPS_DERIV * cnt["mls_deriv"]
     ach_f = flops / (ms_refine / 1000.0) / 1e12 if ms_refine else 0.0
     roof_refine = {"bound": "alu", "achieved": ach_f, "peak": fp64, "unit": "TFLOP/s",
-                   "frac": ach_f / fp64 if fp64 > 0 else None, "traffic": None,
+                   "frac": ach_f / fp64 if fp64 > 0 else None,
+                   "traffic": measured_traffic(case.name + "_refine"),
                    "kernel": "k_refine_w (FP64 Gauss-Newton, one warp per path)",
                    "peak_source": "measured FP64 FMA probe (nrt_probe_fp64_tflops); nominal "
                                   "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s",
@@ -484,13 +485,14 @@ def post_timing(N, R, case, reps=3):
     return {"ms": statistics.median(ms), "paths_in": ref.count(), "paths_out": n_out}
 
 
-def measured_traffic(workload):
-    """DRAM bytes (read + write) per launch of the traversal kernel from the committed ncu
-    capture (profiles/r02_traffic.json, else r01), or None."""
+def measured_traffic(key):
+    """DRAM bytes (read + write) per launch from the committed ncu launch list
+    (profiles/r02_traffic.json, else r01): key = config name for the traversal kernel,
+    config + "_refine" for the refinement kernel; None if not captured."""
     for name in ("r02_traffic.json", "r01_traffic.json"):
         try:
             t = json.load(open(os.path.join(ROOT, "profiles", name)))
-            return float(t[workload]["dram_bytes_per_launch"])
+            return float(t[key]["dram_bytes_per_launch"])
         except Exception:
             continue
     return None

@@ -1195,7 +1195,12 @@ struct Counters {
 };
 
 static std::atomic<unsigned long long> g_hint_raw{0}, g_hint_ev{0}, g_hint_fan{0};
-static const uint64_t kBatch = 1ull << 24;  // rays in flight per wavefront batch
+// rays in flight per wavefront batch (bounded wavefront state: ~300 B per ray in flight);
+// NRT_BATCH overrides (A/B)
+static uint64_t batch_rays() {
+    if (const char* e = getenv("NRT_BATCH")) return strtoull(e, nullptr, 10);
+    return 1ull << 24;
+}
 // reorder live lists of batches at least this long (NRT_SORT_MIN overrides: tests force the
 // reorder path on small scenes)
 static unsigned long long sort_min() {
@@ -1350,6 +1355,7 @@ nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw
     NRT_CUDA(cudaMallocAsync(&dc, sizeof(Counters), st));
     Wave W{};
     WaveGuard wg{&W, st};
+    const uint64_t kBatch = batch_rays();
     NRT_TRY(alloc_wave(W, n_shard < kBatch ? n_shard : kBatch, s->device, st));
     if (reorder_on(s)) W.skey = W.okey[0];
     if (getenv("NRT_PHASES")) {
