@@ -92,11 +92,13 @@ def _rect_grid(c, U, V, nu, nv):
             + B.reshape(-1, 1) * np.asarray(V, np.float64)[None, :])
 
 
-def box_room() -> Scene:
+def box_room(density: int = 1) -> Scene:
     """C1: box [0,4]x[0,3]x[0,2.5] m, inward normals, regular cell-centred grids.
 
     floor/ceiling 74x55, x-walls 55x46, y-walls 74x46 -> 20,008 surfels, r = 0.042 m,
-    labels 0..5 (x=0, x=4, y=0, y=3, z=0, z=2.5)."""
+    labels 0..5 (x=0, x=4, y=0, y=3, z=0, z=2.5).  density k multiplies the grid counts per
+    axis by k (and divides r by k): the dense variants the point-set SDF intersection (NEXT-1)
+    needs — its AABB primitives must hold several points each."""
     X, Y, Z = 4.0, 3.0, 2.5
     faces = [
         # (corner, U, V, nu, nv, normal, label)
@@ -109,15 +111,15 @@ def box_room() -> Scene:
     ]
     P, N, L = [], [], []
     for c, U, V, nu, nv, nrm, lab in faces:
-        p = _rect_grid(c, U, V, nu, nv)
+        p = _rect_grid(c, U, V, nu * density, nv * density)
         P.append(p)
         N.append(np.repeat(np.asarray(nrm, np.float64)[None, :], p.shape[0], 0))
         L.append(np.full(p.shape[0], lab, np.int32))
     P = np.concatenate(P).astype(np.float32)
     N = np.concatenate(N).astype(np.float32)
     L = np.concatenate(L)
-    R = np.full(P.shape[0], 0.042, np.float32)
-    return Scene(P, N, R, L, Edges.empty(), "box_room")
+    R = np.full(P.shape[0], 0.042 / density, np.float32)
+    return Scene(P, N, R, L, Edges.empty(), "box_room" if density == 1 else f"box_room(x{density})")
 
 
 # --------------------------------------------------------------------------

@@ -281,18 +281,22 @@ static void trace(const ctx_t* C, sink_t* K, hist_t h, const float o0[3], const 
     for (int k = 0; k < 3 * n_lam0; ++k) lam[k] = lam0[k];
     float L = L0, Ls = 0.0f;
     int64_t prev = -1;
+    const int sdf = P->sdf.cell > 0.0f && S->sdf;  /* NEXT-1: point-set SDF intersection */
     for (int seg = 0; seg <= refl_budget; ++seg) {
-        float th;
-        int64_t s = or_nearest(S, o, d, lam, n_lam, prev, P->tau, C->cos_ex, &th);
+        float th, nsdf[3] = {0.0f, 0.0f, 0.0f};
+        int64_t cell = -1;
+        int64_t s = sdf ? or_sdf_nearest(S, S->sdf, &P->sdf, o, d, lam, n_lam, prev, P->tau, C->cos_ex,
+                                         &th, &cell, nsdf)
+                        : or_nearest(S, o, d, lam, n_lam, prev, P->tau, C->cos_ex, &th);
         K->bounces++;
         if (K->hit_ids) K->hit_ids[seg] = s;
         rx_captures(C, K, &h, o, d, th, L, Ls, kR, R0, after_diff, ray_id);
         if (allow_edges && h.n_diff < P->max_diff && h.n < OR_MAX_INT)
             edge_captures(C, K, &h, o, d, th, L, ray_id);
         if (s < 0 || seg == refl_budget) break;
-        /* A4: reflect at the hit surfel */
+        /* A4: reflect at the hit surfel (SDF mode: at the SDF hit, its MLS normal, R44) */
         float hp[3] = {o[0] + th * d[0], o[1] + th * d[1], o[2] + th * d[2]};
-        const float* n = S->nrm + 3 * s;
+        const float* n = sdf ? nsdf : S->nrm + 3 * s;
         h.label[h.n] = S->label[s];
         h.prim[h.n] = (uint32_t)s;
         h.v[h.n][0] = hp[0];
@@ -313,7 +317,7 @@ static void trace(const ctx_t* C, sink_t* K, hist_t h, const float o0[3], const 
         lam[1] = n[1];
         lam[2] = n[2];
         n_lam = 1;
-        prev = s;
+        prev = sdf ? cell : s;
     }
 }
 

@@ -31,6 +31,15 @@ typedef struct {
 } or_edge;
 
 typedef struct or_grid or_grid;  /* tier-1 uniform grid (grid.c); NULL = brute force */
+typedef struct or_sdf or_sdf;    /* NEXT-1 AABB primitives of the SDF intersection (sdf.c) */
+
+/* NEXT-1 SDF intersection parameters (R40-R45) */
+typedef struct {
+    float cell;    /* AABB cell edge a (m); 0 = the disk intersection (R7) */
+    float r_s;     /* sample radius (coarse tracing: 0.015, Table II) */
+    float t_sdf;   /* hit threshold (coarse tracing: 0.0015, Table II) */
+    float xi;      /* sigma = xi r_s (Table I: 2) */
+} or_sdf_params;
 
 typedef struct {
     const float* p;        /* n x 3 positions */
@@ -41,6 +50,7 @@ typedef struct {
     const or_edge* edges;
     int32_t n_edges;
     const or_grid* grid;   /* optional tier-1 grid: same argmin, faster */
+    const or_sdf* sdf;     /* AABB primitives for the SDF intersection (launch sdf.cell > 0) */
 } or_scene;
 
 typedef struct {
@@ -56,6 +66,7 @@ typedef struct {
     float theta_ex_deg;    /* departure-sheet angle (R8) */
     float edge_bin;        /* event s-bin (R14) */
     int32_t rank, world;   /* ray shard i == rank (mod world) */
+    or_sdf_params sdf;     /* NEXT-1: cell > 0 selects the SDF intersection */
 } or_launch_params;
 
 /* coarse path record (R17 key + representative) */
@@ -116,6 +127,20 @@ void or_grid_info(const or_grid* G, int64_t dims[3], int64_t* n_refs, double* pa
 int64_t or_grid_nearest(const or_scene* S, const or_grid* G, const float o[3], const float d[3],
                         const float* lam, int n_lam, int64_t prev, float tau, float cos_ex,
                         float* t_hit);
+
+/* NEXT-1 (sdf.c): AABB primitives of cell edge a; the SDF intersection tier 0 */
+or_sdf* or_sdf_build(const or_scene* S, float a);
+void or_sdf_free(or_sdf* G);
+int64_t or_sdf_count(const or_sdf* G);
+void or_sdf_aabb(const or_sdf* G, int64_t j, float lo[3], float hi[3], int64_t* cell, int64_t* n_pts);
+float or_sdf_expf(float x);
+int or_sdf_eval(const or_scene* S, const or_sdf* G, int64_t j, const float x[3], float sigma, float* f,
+                float nbar[3]);
+/* nearest SDF hit of (o, d): returns the record's surfel id (-1: escape), *t_out, the hit
+ * AABB's cell (for the departure rule of the next segment) and the unit hit normal */
+int64_t or_sdf_nearest(const or_scene* S, const or_sdf* G, const or_sdf_params* Q, const float o[3],
+                       const float d[3], const float* lam, int n_lam, int64_t prev_cell, float tau,
+                       float cos_ex, float* t_out, int64_t* cell_out, float n_out[3]);
 
 /* R13 closest approach of ray (o,d) to edge E; 0 if parallel */
 int or_edge_closest(const float o[3], const float d[3], const or_edge* E, float* te, float* s,

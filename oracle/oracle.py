@@ -13,7 +13,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SRCS = ["coarse.c", "grid.c", "refine.c", "post.c"]
+_SRCS = ["coarse.c", "grid.c", "sdf.c", "refine.c", "post.c"]
 
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
           "-Wall", "-Wno-unused-function"]
@@ -56,7 +56,11 @@ class _Edge(C.Structure):
 class _Scene(C.Structure):
     _fields_ = [("p", C.c_void_p), ("nrm", C.c_void_p), ("r", C.c_void_p), ("label", C.c_void_p),
                 ("n", C.c_int64), ("edges", C.c_void_p), ("n_edges", C.c_int32),
-                ("grid", C.c_void_p)]
+                ("grid", C.c_void_p), ("sdf", C.c_void_p)]
+
+
+class _SdfParams(C.Structure):
+    _fields_ = [("cell", C.c_float), ("r_s", C.c_float), ("t_sdf", C.c_float), ("xi", C.c_float)]
 
 
 class _Params(C.Structure):
@@ -64,7 +68,7 @@ class _Params(C.Structure):
                 ("n_rays", C.c_int64), ("max_refl", C.c_int32), ("max_diff", C.c_int32),
                 ("kappa", C.c_int32), ("tau", C.c_float), ("c_R", C.c_float),
                 ("dphi_deg", C.c_float), ("theta_ex_deg", C.c_float), ("edge_bin", C.c_float),
-                ("rank", C.c_int32), ("world", C.c_int32)]
+                ("rank", C.c_int32), ("world", C.c_int32), ("sdf", _SdfParams)]
 
 
 _lib = None
@@ -107,6 +111,22 @@ def lib():
                                       C.POINTER(C.c_float), C.POINTER(C.c_float),
                                       C.POINTER(C.c_float)]
         L.or_fan_dirs.argtypes = [C.POINTER(_Edge), C.c_void_p, C.c_float, C.c_void_p, C.c_int]
+        L.or_sdf_build.argtypes = [C.POINTER(_Scene), C.c_float]
+        L.or_sdf_build.restype = C.c_void_p
+        L.or_sdf_free.argtypes = [C.c_void_p]
+        L.or_sdf_count.argtypes = [C.c_void_p]
+        L.or_sdf_count.restype = C.c_int64
+        L.or_sdf_aabb.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                  C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.or_sdf_expf.argtypes = [C.c_float]
+        L.or_sdf_expf.restype = C.c_float
+        L.or_sdf_eval.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_int64, C.c_void_p, C.c_float,
+                                  C.POINTER(C.c_float), C.c_void_p]
+        L.or_sdf_nearest.argtypes = [C.POINTER(_Scene), C.c_void_p, C.POINTER(_SdfParams),
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int64,
+                                     C.c_float, C.c_float, C.POINTER(C.c_float),
+                                     C.POINTER(C.c_int64), C.c_void_p]
+        L.or_sdf_nearest.restype = C.c_int64
         L.or_grid_build.argtypes = [C.POINTER(_Scene), C.c_double, C.c_void_p]
         L.or_grid_build.restype = C.c_void_p
         L.or_grid_free.argtypes = [C.c_void_p]
@@ -128,7 +148,7 @@ class OracleScene:
     tier-1 uniform grid (grid.c: the same argmin as the brute force, pinned to it bit for bit);
     shift (3,) moves the grid origin (invariance pins)."""
 
-    def __init__(self, scene, grid_voxel=None, shift=None):
+    def __init__(self, scene, grid_voxel=None, shift=None, sdf_cell=None):
         self.p = _f32(scene.points, (-1, 3))
         self.nrm = _f32(scene.normals, (-1, 3))
         self.r = _f32(scene.radii, (-1,))
@@ -149,6 +169,10 @@ class OracleScene:
                         self.label.ctypes.data, self.p.shape[0],
                         C.cast(self.edges, C.c_void_p), self.n_edges, None)
         self.grid = None
+        self.sdf = None
+        if sdf_cell:
+            self.sdf = lib().or_sdf_build(C.byref(self.c), float(sdf_cell))
+            self.c.sdf = self.sdf
         if grid_voxel is not None:
             sh = np.ascontiguousarray(np.zeros(3) if shift is None else shift, np.float64)
             self.grid = lib().or_grid_build(C.byref(self.c), float(grid_voxel), sh.ctypes.data)
@@ -164,8 +188,17 @@ class OracleScene:
         try:
             if self.grid:
                 lib().or_grid_free(self.grid)
+            if self.sdf:
+                lib().or_sdf_free(self.sdf)
         except Exception:
             pass
+
+
+def coarse_scene(case, **kw):
+    """The oracle scene of a coarse launch: with the NEXT-1 AABB primitives when the case asks
+    for the SDF intersection (case.sdf = dict(cell, r_s, t_sdf, xi))."""
+    sdf = getattr(case, "sdf", None)
+    return OracleScene(case.scene, sdf_cell=sdf["cell"] if sdf else None, **kw)
 
 
 def _params(case, rx=None, max_diff=None):
@@ -185,6 +218,10 @@ def _params(case, rx=None, max_diff=None):
     p.edge_bin = float(case.edge_bin)
     p.rank = 0
     p.world = 1
+    sdf = getattr(case, "sdf", None)  # NEXT-1: dict(cell=, r_s=, t_sdf=, xi=) or None
+    if sdf:
+        p.sdf.cell, p.sdf.r_s = float(sdf["cell"]), float(sdf["r_s"])
+        p.sdf.t_sdf, p.sdf.xi = float(sdf["t_sdf"]), float(sdf["xi"])
     return p, rxa
 
 
@@ -254,7 +291,7 @@ _FORK = {}
 def _primary_worker(args):
     rank, world = args
     case, max_diff = _FORK["case"], _FORK["max_diff"]
-    sc = _FORK.get("scene") or OracleScene(case.scene)
+    sc = _FORK.get("scene") or coarse_scene(case)
     p, rxa = _params(case, max_diff=max_diff)
     p.rank, p.world = rank, world
     rc, ec = 1 << 16, 1 << 16
@@ -272,7 +309,7 @@ def _primary_worker(args):
 def _fan_worker(args):
     part, parts = args
     case, max_diff, ev = _FORK["case"], _FORK["max_diff"], _FORK["events"]
-    sc = _FORK.get("scene") or OracleScene(case.scene)
+    sc = _FORK.get("scene") or coarse_scene(case)
     p, rxa = _params(case, max_diff=max_diff)
     rc = 1 << 16
     while True:
@@ -288,7 +325,7 @@ def _fan_worker(args):
 def trace_primary(case, rank=0, world=1, scene: OracleScene | None = None):
     """or_trace_primary of lattice rays i == rank (mod world): raw records, raw events,
     bounces (no fans, no dedupe)."""
-    sc = scene or OracleScene(case.scene)
+    sc = scene or coarse_scene(case)
     p, rxa = _params(case)
     p.rank, p.world = int(rank), int(world)
     rc, ec = 1 << 12, 1 << 12
@@ -347,7 +384,7 @@ def launch_phased(case, procs=1, max_diff=None, return_events=False, grid_voxel=
 
 def launch(case, scene: OracleScene | None = None, raw_cap=1 << 20, max_diff=None):
     """The coarse operation (C.1): returns (deduped records, n_raw, n_bounces)."""
-    sc = scene or OracleScene(case.scene)
+    sc = scene or coarse_scene(case)
     p, rxa = _params(case, max_diff=max_diff)
     while True:
         raw = np.zeros(raw_cap, COARSE_DTYPE)
@@ -362,7 +399,7 @@ def launch(case, scene: OracleScene | None = None, raw_cap=1 << 20, max_diff=Non
 
 def trace_rays(case, ray_ids, scene: OracleScene | None = None, raw_cap=1 << 16):
     """Primary rays only (no fans): raw records, per-segment hit ids, bounce count."""
-    sc = scene or OracleScene(case.scene)
+    sc = scene or coarse_scene(case)
     p, rxa = _params(case)
     ids = np.ascontiguousarray(ray_ids, dtype=np.uint64)
     nseg = case.max_refl + 1

@@ -1,0 +1,302 @@
+/* sdf.c — CPU ORACLE, NEXT-1: the paper's point-set SDF intersection.
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).
+ *
+ * PAPER §II-B/§II-C, readings R40-R45 of DESIGN.md:
+ *   R40 AABB primitives: the points are binned into cubic cells of edge a (the paper's
+ *       voxel / (D_v D_sv), Table I: 0.5 m / (2 * 4)); a cell's AABB per axis is the extent of
+ *       its points, or the cell's full extent on an axis where that extent exceeds a / 2.
+ *   R41 SDF of an AABB at x: Eqs. 1-4 over the AABB's own points (the "points being evaluated",
+ *       P:131), ascending id: w_i = E(-|p_i - x|^2 / (2 sigma^2)), sigma = xi r_s,
+ *       pbar = sum w p / W, nbar = sum w n / W (Eq. 3 literally, not normalised),
+ *       f = (x - pbar) . nbar; undefined ("fails") when W is not > 0.  FP32 throughout;
+ *       E = the exp of sdf_expf below, written identically in the CUDA path (like R2's sincos).
+ *   R42 march: for an AABB the ray enters (slab test, t_far >= 0), a segment of length
+ *       L = a sqrt(3) (the AABB cell's diameter, l_d / (D_v D_sv)) centred on the projection of
+ *       the AABB's centre on the ray; from its near end (clamped to t >= 0) march by |f| (r_s
+ *       where f fails) until the far end; a hit where |f(s_i)| < t_sdf, or where
+ *       sign f(s_i) != sign f(s_i+1): then at the linear zero between the two samples.
+ *   R43 the segment's hit is the lexicographic min (t, cell index) over every AABB; departure:
+ *       the cell of the previous hit is skipped, and so is every AABB whose SDF at the ray
+ *       origin is defined with |f| <= tau and a unit normal within theta_ex of a departure
+ *       normal (the R8 sheet rule with the SDF in place of the disk).
+ *   R44 at a hit x*: the reflection normal is nbar(x*) / |nbar(x*)|; label and id of the
+ *       coarse record are those of the AABB's point nearest to x* (lowest id on ties).
+ * This is tier 0 for the SDF mode: every AABB of the scene is tested for every segment.
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "oracle.h"
+
+struct or_sdf {
+    float org[3];       /* cell origin: the points' minimum */
+    float a;            /* cell edge */
+    int64_t dims[3];
+    int64_t n_aabb;
+    int64_t* cell;      /* [n_aabb] linear cell index, ascending */
+    int64_t* start;     /* [n_aabb + 1] into ids */
+    int64_t* ids;       /* point ids per AABB, ascending */
+    float* lo;          /* [3 n_aabb] AABB bounds */
+    float* hi;
+};
+
+/* R41: exp(x) for x <= 0 in FP32, fixed operation order (Cody-Waite ln2 split + degree-7
+ * Taylor polynomial, then 2^k by the exponent bits); 0 below -87 (FP32 exp underflow). */
+float or_sdf_expf(float x) {
+    if (x < -87.0f) return 0.0f;
+    float kf = floorf(x * 1.44269504f + 0.5f);
+    float r = (x - kf * 0.693359375f) - kf * -2.12194440e-4f;
+    float p = 1.98412698e-4f;
+    p = p * r + 1.38888889e-3f;
+    p = p * r + 8.33333333e-3f;
+    p = p * r + 4.16666667e-2f;
+    p = p * r + 1.66666667e-1f;
+    p = p * r + 0.5f;
+    p = p * r + 1.0f;
+    p = p * r + 1.0f;
+    int k = (int)kf;
+    union {
+        int i;
+        float f;
+    } s;
+    s.i = (k + 127) << 23;
+    return p * s.f;
+}
+
+static float dot3f(const float a[3], const float b[3]) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+
+static int cmp_key(const void* A, const void* B) {
+    const int64_t* a = (const int64_t*)A;
+    const int64_t* b = (const int64_t*)B;
+    if (a[0] != b[0]) return a[0] < b[0] ? -1 : 1;
+    return a[1] < b[1] ? -1 : a[1] > b[1];
+}
+
+or_sdf* or_sdf_build(const or_scene* S, float a) {
+    if (S->n <= 0 || !(a > 0.0f)) return NULL;
+    or_sdf* G = (or_sdf*)calloc(1, sizeof(or_sdf));
+    G->a = a;
+    float mx[3];
+    for (int k = 0; k < 3; ++k) G->org[k] = mx[k] = S->p[k];
+    for (int64_t i = 0; i < S->n; ++i)
+        for (int k = 0; k < 3; ++k) {
+            if (S->p[3 * i + k] < G->org[k]) G->org[k] = S->p[3 * i + k];
+            if (S->p[3 * i + k] > mx[k]) mx[k] = S->p[3 * i + k];
+        }
+    for (int k = 0; k < 3; ++k) G->dims[k] = (int64_t)floorf((mx[k] - G->org[k]) / a) + 1;
+    /* (cell, id) pairs sorted: cells ascending, ids ascending within a cell */
+    int64_t* kv = (int64_t*)malloc(sizeof(int64_t) * 2 * (size_t)S->n);
+    for (int64_t i = 0; i < S->n; ++i) {
+        int64_t c[3];
+        for (int k = 0; k < 3; ++k) {
+            c[k] = (int64_t)floorf((S->p[3 * i + k] - G->org[k]) / a);
+            if (c[k] < 0) c[k] = 0;
+            if (c[k] > G->dims[k] - 1) c[k] = G->dims[k] - 1;
+        }
+        kv[2 * i] = c[0] + G->dims[0] * (c[1] + G->dims[1] * c[2]);
+        kv[2 * i + 1] = i;
+    }
+    qsort(kv, (size_t)S->n, 2 * sizeof(int64_t), cmp_key);
+    int64_t na = 0;
+    for (int64_t i = 0; i < S->n; ++i)
+        if (i == 0 || kv[2 * i] != kv[2 * i - 2]) na++;
+    G->n_aabb = na;
+    G->cell = (int64_t*)malloc(sizeof(int64_t) * (size_t)na);
+    G->start = (int64_t*)malloc(sizeof(int64_t) * (size_t)(na + 1));
+    G->ids = (int64_t*)malloc(sizeof(int64_t) * (size_t)S->n);
+    G->lo = (float*)malloc(sizeof(float) * 3 * (size_t)na);
+    G->hi = (float*)malloc(sizeof(float) * 3 * (size_t)na);
+    int64_t q = -1;
+    for (int64_t i = 0; i < S->n; ++i) {
+        if (i == 0 || kv[2 * i] != kv[2 * i - 2]) {
+            ++q;
+            G->cell[q] = kv[2 * i];
+            G->start[q] = i;
+        }
+        G->ids[i] = kv[2 * i + 1];
+    }
+    G->start[na] = S->n;
+    free(kv);
+    /* R40: AABB = points' extent per axis, the cell's full extent where that exceeds a / 2 */
+    for (int64_t j = 0; j < na; ++j) {
+        int64_t c = G->cell[j];
+        int64_t ci[3] = {c % G->dims[0], (c / G->dims[0]) % G->dims[1], c / (G->dims[0] * G->dims[1])};
+        for (int k = 0; k < 3; ++k) {
+            float lo = INFINITY, hi = -INFINITY;
+            for (int64_t t = G->start[j]; t < G->start[j + 1]; ++t) {
+                float v = S->p[3 * G->ids[t] + k];
+                if (v < lo) lo = v;
+                if (v > hi) hi = v;
+            }
+            if (hi - lo > 0.5f * a) {
+                lo = G->org[k] + (float)ci[k] * a;
+                hi = G->org[k] + (float)(ci[k] + 1) * a;
+            }
+            G->lo[3 * j + k] = lo;
+            G->hi[3 * j + k] = hi;
+        }
+    }
+    return G;
+}
+
+void or_sdf_free(or_sdf* G) {
+    if (!G) return;
+    free(G->cell);
+    free(G->start);
+    free(G->ids);
+    free(G->lo);
+    free(G->hi);
+    free(G);
+}
+
+int64_t or_sdf_count(const or_sdf* G) { return G ? G->n_aabb : 0; }
+
+void or_sdf_aabb(const or_sdf* G, int64_t j, float lo[3], float hi[3], int64_t* cell, int64_t* n_pts) {
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = G->lo[3 * j + k];
+        hi[k] = G->hi[3 * j + k];
+    }
+    *cell = G->cell[j];
+    *n_pts = G->start[j + 1] - G->start[j];
+}
+
+/* R41: f of AABB j at x (and nbar, unnormalised); 0 where it fails */
+int or_sdf_eval(const or_scene* S, const or_sdf* G, int64_t j, const float x[3], float sigma, float* f,
+                float nbar[3]) {
+    const float inv = 1.0f / (2.0f * sigma * sigma);
+    float W = 0.0f, P[3] = {0.0f, 0.0f, 0.0f}, N[3] = {0.0f, 0.0f, 0.0f};
+    for (int64_t t = G->start[j]; t < G->start[j + 1]; ++t) {
+        const float* p = S->p + 3 * G->ids[t];
+        const float* n = S->nrm + 3 * G->ids[t];
+        float d[3] = {p[0] - x[0], p[1] - x[1], p[2] - x[2]};
+        float q = dot3f(d, d);
+        float w = or_sdf_expf(-(q * inv));
+        W = W + w;
+        for (int k = 0; k < 3; ++k) {
+            P[k] = P[k] + w * p[k];
+            N[k] = N[k] + w * n[k];
+        }
+    }
+    if (!(W > 0.0f)) return 0;
+    float pb[3], e[3];
+    for (int k = 0; k < 3; ++k) {
+        pb[k] = P[k] / W;
+        nbar[k] = N[k] / W;
+        e[k] = x[0 + k] - pb[k];
+    }
+    *f = dot3f(e, nbar);
+    return 1;
+}
+
+/* R42: march of AABB j along (o, d) from t >= 0; 1 and *t on a hit */
+static int march(const or_scene* S, const or_sdf* G, int64_t j, const float o[3], const float d[3],
+                 const or_sdf_params* Q, float* t_hit) {
+    float c[3], tn = 0.0f, tf = INFINITY;
+    for (int k = 0; k < 3; ++k) {
+        const float lo = G->lo[3 * j + k], hi = G->hi[3 * j + k];
+        c[k] = 0.5f * (lo + hi);
+        if (d[k] != 0.0f) {
+            float ta = (lo - o[k]) / d[k], tb = (hi - o[k]) / d[k];
+            if (ta > tb) {
+                float s = ta;
+                ta = tb;
+                tb = s;
+            }
+            if (ta > tn) tn = ta;
+            if (tb < tf) tf = tb;
+        } else if (o[k] < lo || o[k] > hi) {
+            return 0;
+        }
+    }
+    if (!(tn <= tf)) return 0;  /* the ray misses the AABB (or it lies behind the origin) */
+    const float half = 0.5f * (Q->cell * 1.7320508f);
+    float w[3] = {c[0] - o[0], c[1] - o[1], c[2] - o[2]};
+    const float tc = dot3f(w, d);
+    float t = tc - half;
+    const float te = tc + half;
+    if (t < 0.0f) t = 0.0f;
+    const float sigma = Q->xi * Q->r_s;
+    float x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+    float f0, nb[3];
+    int ok0 = or_sdf_eval(S, G, j, x, sigma, &f0, nb);
+    for (int it = 0; it < 4096; ++it) {
+        if (ok0 && fabsf(f0) < Q->t_sdf) {
+            *t_hit = t;
+            return 1;
+        }
+        const float step = ok0 ? fabsf(f0) : Q->r_s;
+        const float t1 = t + step;
+        if (t1 > te) return 0;
+        float x1[3] = {o[0] + t1 * d[0], o[1] + t1 * d[1], o[2] + t1 * d[2]};
+        float f1;
+        const int ok1 = or_sdf_eval(S, G, j, x1, sigma, &f1, nb);
+        if (ok0 && ok1 && ((f0 < 0.0f) != (f1 < 0.0f))) {
+            *t_hit = t + step * (f0 / (f0 - f1));
+            return 1;
+        }
+        t = t1;
+        f0 = f1;
+        ok0 = ok1;
+    }
+    return 0;
+}
+
+/* R43 departure sheet: AABB j is transparent to a ray leaving o with departure normals lam */
+static int excluded(const or_scene* S, const or_sdf* G, int64_t j, const float o[3], const float* lam,
+                    int n_lam, const or_sdf_params* Q, float tau, float cos_ex) {
+    if (n_lam == 0) return 0;
+    float f, nb[3];
+    if (!or_sdf_eval(S, G, j, o, Q->xi * Q->r_s, &f, nb)) return 0;
+    if (!(fabsf(f) <= tau)) return 0;
+    const float l = sqrtf(dot3f(nb, nb));
+    if (!(l > 0.0f)) return 0;
+    const float u[3] = {nb[0] / l, nb[1] / l, nb[2] / l};
+    for (int k = 0; k < n_lam; ++k)
+        if (fabsf(dot3f(u, lam + 3 * k)) >= cos_ex) return 1;
+    return 0;
+}
+
+/* R43-R44: the segment's nearest SDF hit over every AABB (tier 0) */
+int64_t or_sdf_nearest(const or_scene* S, const or_sdf* G, const or_sdf_params* Q, const float o[3],
+                       const float d[3], const float* lam, int n_lam, int64_t prev_cell, float tau,
+                       float cos_ex, float* t_out, int64_t* cell_out, float n_out[3]) {
+    float bt = INFINITY;
+    int64_t bj = -1;
+    for (int64_t j = 0; j < G->n_aabb; ++j) {
+        if (G->cell[j] == prev_cell) continue;
+        float t;
+        if (!march(S, G, j, o, d, Q, &t)) continue;
+        if (!(t < bt)) continue;  /* cells ascend: equal t keeps the lower cell */
+        if (excluded(S, G, j, o, lam, n_lam, Q, tau, cos_ex)) continue;
+        bt = t;
+        bj = j;
+    }
+    *t_out = bt;
+    if (bj < 0) {
+        *cell_out = -1;
+        return -1;
+    }
+    *cell_out = G->cell[bj];
+    float x[3] = {o[0] + bt * d[0], o[1] + bt * d[1], o[2] + bt * d[2]};
+    float f, nb[3];
+    n_out[0] = n_out[1] = n_out[2] = 0.0f;
+    if (or_sdf_eval(S, G, bj, x, Q->xi * Q->r_s, &f, nb)) {
+        const float l = sqrtf(dot3f(nb, nb));
+        if (l > 0.0f)
+            for (int k = 0; k < 3; ++k) n_out[k] = nb[k] / l;
+    }
+    /* the AABB's point nearest to the hit point: the record's label and id */
+    int64_t best = -1;
+    float bq = INFINITY;
+    for (int64_t t = G->start[bj]; t < G->start[bj + 1]; ++t) {
+        const float* p = S->p + 3 * G->ids[t];
+        float e[3] = {p[0] - x[0], p[1] - x[1], p[2] - x[2]};
+        float q = dot3f(e, e);
+        if (q < bq) {
+            bq = q;
+            best = G->ids[t];
+        }
+    }
+    return best;
+}
