@@ -71,6 +71,11 @@ typedef struct {
     nrt_mem mem;           /* where points/normals/radii/labels live */
     int32_t device;        /* CUDA device ordinal */
     void* stream;          /* cudaStream_t */
+    float sdf_cell;        /* NEXT-1: edge a (m) of the cubic cells that bin the points into AABB
+                              primitives (the paper's voxel / (D_v D_sv) = 0.0625 m,
+                              Table I), 0 = none (disk intersection only).  Each non-empty cell's
+                              AABB is its points' extent per axis, or the cell's full extent on an
+                              axis where that extent exceeds a/2 (DESIGN R40). */
 } nrt_scene_desc;
 
 /* north_star 4-argument form: host arrays, radius 0.015 m, pseudo-labels, no edges,
@@ -87,6 +92,9 @@ typedef struct {
     int32_t dims[3];
     float origin[3], voxel;
     float r_max;
+    int64_t n_aabb;        /* NEXT-1 AABB primitives (0 when sdf_cell == 0) */
+    int64_t n_aabb_refs;   /* their registrations in the AABB traversal grid */
+    float sdf_cell;
 } nrt_scene_info;
 nrt_status nrt_scene_info_get(nrt_scene s, nrt_scene_info* info);
 
@@ -112,6 +120,14 @@ typedef struct {
                              visited (nrt_paths_info); results are unchanged, speed is not */
     nrt_mem mem;          /* where tx / rx live */
     void* stream;
+    int32_t intersect;    /* 0 = oriented-surfel disk hit (R7-R9, default); 1 = NEXT-1: the
+                             paper's point-set SDF intersection (DESIGN R40-R45):
+                             per AABB primitive the ray marches Eqs. 1-4 over the AABB's points;
+                             the scene must have been built with sdf_cell > 0 (else NRT_E_STATE) */
+    float sdf_r_s;        /* NEXT-1 r_s (m): sigma = sdf_xi * sdf_r_s, and the step where the
+                             SDF fails; default 0.015 */
+    float sdf_t_sdf;      /* NEXT-1 hit threshold |f| < t_sdf; default 0.0015 */
+    float sdf_xi;         /* NEXT-1 xi; default 2 */
 } nrt_launch_desc;
 void nrt_launch_desc_default(nrt_launch_desc* d);
 

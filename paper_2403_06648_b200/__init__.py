@@ -45,20 +45,24 @@ class nrt_scene_desc(C.Structure):
     _fields_ = [("points", C.c_void_p), ("normals", C.c_void_p), ("radii", C.c_void_p),
                 ("radius", C.c_float), ("labels", C.c_void_p), ("n", C.c_int64),
                 ("voxel_size", C.c_float), ("edges", C.c_void_p), ("n_edges", C.c_int32),
-                ("mem", C.c_int), ("device", C.c_int32), ("stream", C.c_void_p)]
+                ("mem", C.c_int), ("device", C.c_int32), ("stream", C.c_void_p),
+                ("sdf_cell", C.c_float)]
 
 
 class nrt_scene_info(C.Structure):
     _fields_ = [("n_surfels", C.c_int64), ("n_refs", C.c_int64), ("n_cells", C.c_int64),
                 ("dims", C.c_int32 * 3), ("origin", C.c_float * 3), ("voxel", C.c_float),
-                ("r_max", C.c_float)]
+                ("r_max", C.c_float), ("n_aabb", C.c_int64), ("n_aabb_refs", C.c_int64),
+                ("sdf_cell", C.c_float)]
 
 
 class nrt_launch_desc(C.Structure):
     _fields_ = [("kappa", C.c_int32), ("tau", C.c_float), ("c_R", C.c_float),
                 ("dphi_deg", C.c_float), ("theta_ex_deg", C.c_float), ("edge_bin", C.c_float),
                 ("rank", C.c_int32), ("world", C.c_int32), ("stage", C.c_int32),
-                ("counters", C.c_int32), ("mem", C.c_int), ("stream", C.c_void_p)]
+                ("counters", C.c_int32), ("mem", C.c_int), ("stream", C.c_void_p),
+                ("intersect", C.c_int32), ("sdf_r_s", C.c_float), ("sdf_t_sdf", C.c_float),
+                ("sdf_xi", C.c_float)]
 
 
 class nrt_post_desc(C.Structure):
@@ -233,7 +237,8 @@ class Scene:
         _check(lib().nrt_scene_info_get(self.h, C.byref(i)))
         return {"n_surfels": i.n_surfels, "n_refs": i.n_refs, "n_cells": i.n_cells,
                 "dims": tuple(i.dims), "origin": tuple(i.origin), "voxel": i.voxel,
-                "r_max": i.r_max}
+                "r_max": i.r_max, "n_aabb": i.n_aabb, "n_aabb_refs": i.n_aabb_refs,
+                "sdf_cell": i.sdf_cell}
 
     def free(self):
         if self.h is not None and self.h.value:
@@ -329,7 +334,7 @@ def nrt_scene_build(points, normals, n, voxel_size) -> Scene:
 
 
 def nrt_scene_build_ex(points, normals, voxel_size, radii=None, radius=0.015, labels=None,
-                       edges=None, device=0, stream=None) -> Scene:
+                       edges=None, device=0, stream=None, sdf_cell=0.0) -> Scene:
     keep = []
     pp, mem = _ptr(points, np.float32, keep)
     pn, mem2 = _ptr(normals, np.float32, keep)
@@ -349,6 +354,7 @@ def nrt_scene_build_ex(points, normals, voxel_size, radii=None, radius=0.015, la
     d.mem = mems.pop()
     d.device = int(device)
     d.stream = _stream_ptr(stream)
+    d.sdf_cell = float(sdf_cell)
     h = C.c_void_p()
     _check(lib().nrt_scene_build_ex(C.byref(d), C.byref(h)))
     return Scene(h.value)
@@ -500,19 +506,31 @@ def nrt_workspace_trim() -> None:
 # convenience: a whole case (nrt_gen.LaunchCase) through the ABI
 # ------------------------------------------------------------------------------------------
 def build_case_scene(case, device_arrays=False, stream=None) -> Scene:
+    """The case's scene; with case.sdf (NEXT-1) also its AABB primitives of edge sdf["cell"]."""
     s = case.scene
+    a = float(getattr(case, "sdf", None)["cell"]) if getattr(case, "sdf", None) else 0.0
     if device_arrays:
         import torch
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
         return nrt_scene_build_ex(t(s.points), t(s.normals), case.voxel, radii=t(s.radii),
-                                  labels=t(s.labels), edges=s.edges, stream=stream)
+                                  labels=t(s.labels), edges=s.edges, stream=stream, sdf_cell=a)
     return nrt_scene_build_ex(s.points, s.normals, case.voxel, radii=s.radii, labels=s.labels,
-                              edges=s.edges, stream=stream)
+                              edges=s.edges, stream=stream, sdf_cell=a)
+
+
+def case_desc(case) -> dict:
+    """Launch-descriptor keywords of a case (with case.sdf: the NEXT-1 SDF intersection)."""
+    desc = dict(kappa=case.kappa, tau=case.tau, c_R=case.c_R, dphi_deg=case.dphi_deg,
+                theta_ex_deg=case.theta_ex_deg, edge_bin=case.edge_bin)
+    q = getattr(case, "sdf", None)
+    if q:
+        desc.update(intersect=1, sdf_r_s=float(q["r_s"]), sdf_t_sdf=float(q["t_sdf"]),
+                    sdf_xi=float(q["xi"]))
+    return desc
 
 
 def launch_case(scene: Scene, case, **kw) -> Paths:
-    desc = dict(kappa=case.kappa, tau=case.tau, c_R=case.c_R, dphi_deg=case.dphi_deg,
-                theta_ex_deg=case.theta_ex_deg, edge_bin=case.edge_bin)
+    desc = case_desc(case)
     desc.update(kw)
     return nrt_launch_ex(scene, case.tx, case.rx, case.n_rays, case.max_refl, case.max_diff,
                          **desc)

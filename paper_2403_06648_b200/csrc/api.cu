@@ -220,6 +220,14 @@ static nrt_status check_launch(nrt_scene s, const float* tx, const float* rx, in
     if (d.stage == 0 && d.world > 1 && max_diff > 0 && s->n_edges > 0)
         return set_error(NRT_E_STATE, "world > 1 with diffraction needs the two-stage protocol "
                                       "(stage 1 + event all-gather + nrt_launch_fans)");
+    if (d.intersect < 0 || d.intersect > 1) return set_error(NRT_E_INVALID, "intersect must be 0 or 1");
+    if (d.intersect == 1) {
+        if (!s->n_aabb)
+            return set_error(NRT_E_STATE, "intersect = 1 (SDF) needs a scene built with sdf_cell > 0");
+        if (!(d.sdf_r_s > 0.0f) || !(d.sdf_t_sdf > 0.0f) || !(d.sdf_xi > 0.0f) ||
+            !std::isfinite(d.sdf_r_s) || !std::isfinite(d.sdf_t_sdf) || !std::isfinite(d.sdf_xi))
+            return set_error(NRT_E_INVALID, "sdf_r_s, sdf_t_sdf, sdf_xi must be finite and > 0");
+    }
     for (int j = 0; j < s->n_edges; ++j)
         if (s->h_edges[j].len / d.edge_bin >= (float)(1 << 27))
             return set_error(NRT_E_INVALID, "edge %d too long for edge_bin", j);
@@ -294,6 +302,11 @@ void nrt_scene_free(nrt_scene s) {
     cudaFreeAsync(s->hid, nullptr);
     cudaFreeAsync(s->hoff, nullptr);
     cudaFreeAsync(s->edges, nullptr);
+    cudaFreeAsync(s->sdf_pts, nullptr);
+    cudaFreeAsync(s->sdf_box, nullptr);
+    cudaFreeAsync(s->sdf_acell, nullptr);
+    cudaFreeAsync(s->sdf_gcell, nullptr);
+    cudaFreeAsync(s->sdf_aref, nullptr);
     delete s;
 }
 
@@ -308,6 +321,9 @@ nrt_status nrt_scene_info_get(nrt_scene s, nrt_scene_info* info) {
     }
     info->voxel = s->v;
     info->r_max = s->r_max;
+    info->n_aabb = s->n_aabb;
+    info->n_aabb_refs = s->n_aref;
+    info->sdf_cell = s->sdf_a;
     return NRT_OK;
 }
 
@@ -325,6 +341,10 @@ void nrt_launch_desc_default(nrt_launch_desc* d) {
     d->stage = 0;
     d->mem = NRT_MEM_HOST;
     d->stream = nullptr;
+    d->intersect = 0;
+    d->sdf_r_s = 0.015f;
+    d->sdf_t_sdf = 0.0015f;
+    d->sdf_xi = 2.0f;
 }
 
 nrt_status nrt_launch(nrt_scene s, const float tx[3], const float* rx, int32_t n_rx, int64_t n_rays,

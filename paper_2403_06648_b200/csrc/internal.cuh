@@ -150,6 +150,23 @@ struct nrt_scene_s {
     nrt::DevEdge* edges = nullptr;
     int n_edges = 0;
     std::vector<nrt::DevEdge> h_edges;
+    // NEXT-1 AABB primitives (DESIGN R40, §6.4): the points binned into cubic cells of edge
+    // sdf_a from sdf_org (the points' minimum); one AABB per non-empty cell, ascending cell.
+    //   sdf_pts  [2n]       (p, 0), (n, id bits) of the points in (cell, id) order
+    //   sdf_box  [2 n_aabb] (lo, first point bits), (hi, end point bits)
+    //   sdf_acell[n_aabb]   linear cell index of each AABB
+    // traversal grid: cells of sdf_a from sdf_gorg = sdf_org - sdf_a (one empty margin cell),
+    // every AABB registered (sdf_aref, AABB indices) in all cells its box padded by sdf_pad
+    // overlaps; sdf_gcell = (start, end), or (D, D) for empty cells (Chebyshev skip distance).
+    float sdf_a = 0, sdf_pad = 0;
+    float sdf_org[3] = {0, 0, 0}, sdf_gorg[3] = {0, 0, 0};
+    int sdf_dims[3] = {0, 0, 0}, sdf_gdims[3] = {0, 0, 0};
+    int64_t n_aabb = 0, n_aref = 0;
+    float4* sdf_pts = nullptr;
+    float4* sdf_box = nullptr;
+    unsigned* sdf_acell = nullptr;
+    uint2* sdf_gcell = nullptr;
+    unsigned* sdf_aref = nullptr;
     // output-buffer size hints (largest counts seen by launches on this scene)
     unsigned long long hint_raw = 1 << 16, hint_ev = 1 << 14, hint_fan = 1 << 16;
 };

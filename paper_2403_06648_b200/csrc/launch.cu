@@ -66,6 +66,7 @@ struct Wave {
     float4* l0;      // [cap] departure-sheet normal 0
     float4* l1;      // [cap] departure-sheet normal 1
     float2* hit;     // [cap] (best_t, best id bits)
+    float4* hitn;    // [cap] SDF mode: (unit MLS normal at the hit, AABB cell bits)
     RayCold* cold;   // [cap]
     unsigned* alive[2];       // ping-pong live lists
     unsigned* okey[2];        // ordering keys (primary batches)
@@ -114,6 +115,16 @@ struct TP {  // trace parameters (by value into the kernels)
     unsigned long long* bounces;
     unsigned long long* counters;  // [tests, cells, nonempty cells] (instrumented build)
     int64_t* hit_out;              // debug: per-segment hit ids
+    // NEXT-1 point-set SDF intersection (DESIGN R40-R45, §6.4); sdf == 0: disk hit
+    int sdf;
+    const float4* sdf_pts;    // (p, 0), (n, id bits) in (cell, id) order
+    const float4* sdf_box;    // (lo, first point bits), (hi, end point bits) per AABB
+    const unsigned* sdf_acell;
+    const uint2* sdf_gcell;   // traversal grid (start, end) into sdf_aref, or (D, D) empty
+    const unsigned* sdf_aref;
+    float sg_o[3], sdf_a, sdf_inv_a, sdf_stop;  // sdf_stop = 2 * half + pad (early exit)
+    int sg_n[3];
+    float sdf_half, sdf_rs, sdf_tsdf, sdf_inv;  // sdf_inv = 1 / (2 sigma^2), sigma = xi r_s
 };
 
 __device__ __forceinline__ unsigned long long agg_inc(unsigned long long* ctr) {
@@ -780,6 +791,271 @@ __device__ __forceinline__ unsigned order_key(const TP& P, float3 h, float3 d) {
     return min((m << 14) | (u << 7) | v, 0xFFFFFFFEu);  // 0xFFFFFFFF pads the sorted list
 }
 
+
+// =======================================================================================
+// NEXT-1: the paper's point-set SDF intersection (DESIGN R40-R45, §6.4)
+// =======================================================================================
+// R41: FP32 exp for x <= 0, the definition's fixed operation order (identical to the oracle's)
+__device__ __forceinline__ float sdf_expf(float x) {
+    if (x < -87.0f) return 0.0f;
+    const float kf = floorf(x * 1.44269504f + 0.5f);
+    const float r = (x - kf * 0.693359375f) - kf * -2.12194440e-4f;
+    float p = 1.98412698e-4f;
+    p = p * r + 1.38888889e-3f;
+    p = p * r + 8.33333333e-3f;
+    p = p * r + 4.16666667e-2f;
+    p = p * r + 1.66666667e-1f;
+    p = p * r + 0.5f;
+    p = p * r + 1.0f;
+    p = p * r + 1.0f;
+    return p * __int_as_float(((int)kf + 127) << 23);
+}
+
+// R41: f and nbar (unnormalised) of the AABB whose points are [k0, k1) at x; false = fails
+__device__ __forceinline__ bool sdf_eval(const TP& P, unsigned k0, unsigned k1, float x0, float x1, float x2,
+                                         float& f, float& nb0, float& nb1, float& nb2) {
+    float W = 0.0f, p0 = 0.0f, p1 = 0.0f, p2 = 0.0f, n0 = 0.0f, n1 = 0.0f, n2 = 0.0f;
+    for (unsigned k = k0; k < k1; ++k) {
+        const float4 A = __ldg(&P.sdf_pts[2 * k]), B = __ldg(&P.sdf_pts[2 * k + 1]);
+        const float d0 = A.x - x0, d1 = A.y - x1, d2 = A.z - x2;
+        const float q = (d0 * d0 + d1 * d1) + d2 * d2;
+        const float w = sdf_expf(-(q * P.sdf_inv));
+        W = W + w;
+        p0 = p0 + w * A.x;
+        n0 = n0 + w * B.x;
+        p1 = p1 + w * A.y;
+        n1 = n1 + w * B.y;
+        p2 = p2 + w * A.z;
+        n2 = n2 + w * B.z;
+    }
+    if (!(W > 0.0f)) return false;
+    const float b0 = p0 / W, b1 = p1 / W, b2 = p2 / W;
+    nb0 = n0 / W;
+    nb1 = n1 / W;
+    nb2 = n2 / W;
+    const float e0 = x0 - b0, e1 = x1 - b1, e2 = x2 - b2;
+    f = (e0 * nb0 + e1 * nb1) + e2 * nb2;
+    return true;
+}
+
+// R42 slab test of AABB (L, H) against the ray (t >= 0): the entry tn, or -1 when it misses
+__device__ __forceinline__ float sdf_slab(const float3 o, const float3 d, const float4 L, const float4 H) {
+    float tn = 0.0f, tf = INFINITY;
+    const float lo[3] = {L.x, L.y, L.z}, hi[3] = {H.x, H.y, H.z}, ov[3] = {o.x, o.y, o.z},
+                dv[3] = {d.x, d.y, d.z};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (dv[k] != 0.0f) {
+            float ta = (lo[k] - ov[k]) / dv[k], tb = (hi[k] - ov[k]) / dv[k];
+            if (ta > tb) {
+                const float t = ta;
+                ta = tb;
+                tb = t;
+            }
+            if (ta > tn) tn = ta;
+            if (tb < tf) tf = tb;
+        } else if (ov[k] < lo[k] || ov[k] > hi[k]) {
+            return -1.0f;
+        }
+    }
+    return tn <= tf ? tn : -1.0f;
+}
+
+// R42: the march of AABB (L, H) along the ray; true and t on a hit
+__device__ __forceinline__ bool sdf_march(const TP& P, const float3 o, const float3 d, const float4 L,
+                                          const float4 H, float& t_hit) {
+    const unsigned k0 = __float_as_uint(L.w), k1 = __float_as_uint(H.w);
+    const float c0 = 0.5f * (L.x + H.x), c1 = 0.5f * (L.y + H.y), c2 = 0.5f * (L.z + H.z);
+    const float w0 = c0 - o.x, w1 = c1 - o.y, w2 = c2 - o.z;
+    const float tc = (w0 * d.x + w1 * d.y) + w2 * d.z;
+    float t = tc - P.sdf_half;
+    const float te = tc + P.sdf_half;
+    if (t < 0.0f) t = 0.0f;
+    float f0, f1, nb0, nb1, nb2;
+    bool ok0 = sdf_eval(P, k0, k1, o.x + t * d.x, o.y + t * d.y, o.z + t * d.z, f0, nb0, nb1, nb2);
+    for (int it = 0; it < 4096; ++it) {
+        if (ok0 && fabsf(f0) < P.sdf_tsdf) {
+            t_hit = t;
+            return true;
+        }
+        const float step = ok0 ? fabsf(f0) : P.sdf_rs;
+        const float t1 = t + step;
+        if (t1 > te) return false;
+        const bool ok1 = sdf_eval(P, k0, k1, o.x + t1 * d.x, o.y + t1 * d.y, o.z + t1 * d.z, f1, nb0, nb1, nb2);
+        if (ok0 && ok1 && ((f0 < 0.0f) != (f1 < 0.0f))) {
+            t_hit = t + step * (f0 / (f0 - f1));
+            return true;
+        }
+        t = t1;
+        f0 = f1;
+        ok0 = ok1;
+    }
+    return false;
+}
+
+// R43 departure sheet: the AABB is transparent when its SDF at the origin is defined with
+// |f| <= tau and its unit normal lies within theta_ex of a departure normal (l0, l1; zero
+// vectors stand for "no departure normal", which never excludes since cos_ex > 0)
+__device__ __forceinline__ bool sdf_excluded(const TP& P, const float3 o, const float3 l0, const float3 l1,
+                                             const float4 L, const float4 H) {
+    float f, nb0, nb1, nb2;
+    if (!sdf_eval(P, __float_as_uint(L.w), __float_as_uint(H.w), o.x, o.y, o.z, f, nb0, nb1, nb2)) return false;
+    if (!(fabsf(f) <= P.tau)) return false;
+    const float l = sqrtf((nb0 * nb0 + nb1 * nb1) + nb2 * nb2);
+    if (!(l > 0.0f)) return false;
+    const float u0 = nb0 / l, u1 = nb1 / l, u2 = nb2 / l;
+    if (fabsf((u0 * l0.x + u1 * l0.y) + u2 * l0.z) >= P.cos_ex) return true;
+    return fabsf((u0 * l1.x + u1 * l1.y) + u2 * l1.z) >= P.cos_ex;
+}
+
+// TRACE (SDF mode): per lane one segment; a 3D-DDA over the AABB traversal grid (Chebyshev
+// jumps over empty cells).  AABB j is marched once per segment, in the non-empty cell whose
+// interval [t_lo, t_out) holds its slab entry tn (t_lo = exit of the previous non-empty cell:
+// the intervals tile the segment, and the padded registration puts j in that cell); the walk
+// stops once best_t < t_out - (2 half + pad), below which no later AABB's march can start.
+// The hit is the lexicographic min (t, AABB index) = min (t, cell), as R43 defines it.
+template <bool CNT>
+__global__ void __launch_bounds__(128) k_trace_sdf(TP P, Wave W, int b) {
+    const unsigned long long n = W.n_alive[b];
+    const unsigned* alive = W.alive[b & 1];
+    unsigned long long bounces = 0;
+    Cnt cnt;
+    for (;;) {
+        const unsigned long long jj = lane_inc(&W.ctr[b]);
+        if (jj >= n) break;
+        const unsigned ray = alive[jj];
+        ++bounces;
+        const float4 o4 = W.o[ray], d4 = W.d[ray], a4 = W.l0[ray], c4 = W.l1[ray];
+        const float3 o = make_float3(o4.x, o4.y, o4.z), d = make_float3(d4.x, d4.y, d4.z);
+        const float3 l0 = make_float3(a4.x, a4.y, a4.z), l1 = make_float3(c4.x, c4.y, c4.z);
+        const bool has_lam = l0.x != 0.0f || l0.y != 0.0f || l0.z != 0.0f || l1.x != 0.0f || l1.y != 0.0f ||
+                             l1.z != 0.0f;
+        const unsigned prev = __float_as_uint(o4.w);  // cell of the previous hit (~0: none)
+        float best_t = INFINITY;
+        int best = -1;
+        // grid entry
+        const float ov[3] = {o.x, o.y, o.z}, dv[3] = {d.x, d.y, d.z};
+        float inv[3], t0 = 0.0f, t1 = INFINITY;
+        for (int k = 0; k < 3; ++k) {
+            inv[k] = rcp_approx(dv[k]);  // walk only (§6.4)
+            const float lo = P.sg_o[k], hi = P.sg_o[k] + (float)P.sg_n[k] * P.sdf_a;
+            if (dv[k] != 0.0f) {
+                const float ta = (lo - ov[k]) * inv[k], tb = (hi - ov[k]) * inv[k];
+                t0 = fmaxf(t0, fminf(ta, tb));
+                t1 = fminf(t1, fmaxf(ta, tb));
+            } else if (ov[k] < lo || ov[k] > hi) {
+                t1 = -1.0f;
+            }
+        }
+        if (t0 <= t1) {
+            int c[3];
+            float tm[3];
+            for (int k = 0; k < 3; ++k) {
+                const float p = ov[k] + t0 * dv[k];
+                c[k] = min(P.sg_n[k] - 1, max(0, (int)floorf((p - P.sg_o[k]) * P.sdf_inv_a)));
+                tm[k] = dv[k] != 0.0f ? ((P.sg_o[k] + (float)(c[k] + (dv[k] > 0.0f)) * P.sdf_a) - ov[k]) * inv[k]
+                                      : INFINITY;
+            }
+            float t_lo = t0;
+            bool first = true;
+            for (;;) {
+                const float t_out = fminf(tm[0], fminf(tm[1], tm[2]));
+                const uint2 rg = __ldg(&P.sdf_gcell[c[0] + P.sg_n[0] * (c[1] + P.sg_n[1] * c[2])]);
+                if (CNT) cnt.cells++;
+                int D = 1;
+                if (rg.y > rg.x) {
+                    if (CNT) cnt.nonempty++;
+                    for (unsigned q = rg.x; q < rg.y; ++q) {
+                        const unsigned j = __ldg(&P.sdf_aref[q]);
+                        if (__ldg(&P.sdf_acell[j]) == prev) continue;
+                        const float4 L = __ldg(&P.sdf_box[2 * j]), H = __ldg(&P.sdf_box[2 * j + 1]);
+                        const float tn = sdf_slab(o, d, L, H);
+                        if (tn < 0.0f) continue;
+                        if ((!first && tn < t_lo) || !(tn < t_out)) continue;  // owner cell only
+                        if (CNT) cnt.tests++;
+                        float t;
+                        if (!sdf_march(P, o, d, L, H, t)) continue;
+                        if (!(t < best_t || (t == best_t && (int)j < best))) continue;
+                        if (has_lam && sdf_excluded(P, o, l0, l1, L, H)) continue;
+                        best_t = t;
+                        best = (int)j;
+                    }
+                    first = false;
+                    t_lo = t_out;
+                } else {
+                    D = (int)rg.x;
+                }
+                if (best_t < t_out - P.sdf_stop) break;
+                // grid move: DDA step, or a Chebyshev jump across the empty box (as k_trace)
+                if (D <= 1) {
+                    const int ax = (tm[0] <= tm[1] && tm[0] <= tm[2]) ? 0 : (tm[1] <= tm[2] ? 1 : 2);
+                    c[ax] += dv[ax] > 0.0f ? 1 : -1;
+                    if (c[ax] < 0 || c[ax] >= P.sg_n[ax]) break;
+                    tm[ax] = ((P.sg_o[ax] + (float)(c[ax] + (dv[ax] > 0.0f)) * P.sdf_a) - ov[ax]) * inv[ax];
+                } else {
+                    const int r = D - 1;
+                    float T = INFINITY;
+                    int ax = 0;
+                    for (int k = 0; k < 3; ++k) {
+                        const int fk = dv[k] > 0.0f ? c[k] + r + 1 : c[k] - r;
+                        const float Tk = dv[k] != 0.0f ? ((P.sg_o[k] + (float)fk * P.sdf_a) - ov[k]) * inv[k] : INFINITY;
+                        if (Tk < T) {
+                            T = Tk;
+                            ax = k;
+                        }
+                    }
+                    int nc[3];
+                    for (int k = 0; k < 3; ++k) {
+                        const float pk = ov[k] + T * dv[k];
+                        nc[k] = min(c[k] + r, max(c[k] - r, (int)floorf((pk - P.sg_o[k]) * P.sdf_inv_a)));
+                    }
+                    nc[ax] = dv[ax] > 0.0f ? c[ax] + r + 1 : c[ax] - r - 1;
+                    bool out = false;
+                    for (int k = 0; k < 3; ++k) out |= nc[k] < 0 || nc[k] >= P.sg_n[k];
+                    if (out) break;
+                    for (int k = 0; k < 3; ++k) {
+                        c[k] = nc[k];
+                        tm[k] = dv[k] != 0.0f
+                                    ? ((P.sg_o[k] + (float)(c[k] + (dv[k] > 0.0f)) * P.sdf_a) - ov[k]) * inv[k]
+                                    : INFINITY;
+                    }
+                }
+            }
+        }
+        int pid = -1;
+        float4 hn = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(~0u));
+        if (best >= 0) {
+            // R44: normal nbar(x*)/|nbar(x*)|; record point = the AABB's point nearest x*
+            const float4 L = __ldg(&P.sdf_box[2 * best]), H = __ldg(&P.sdf_box[2 * best + 1]);
+            const unsigned k0 = __float_as_uint(L.w), k1 = __float_as_uint(H.w);
+            const float x0 = o.x + best_t * d.x, x1 = o.y + best_t * d.y, x2 = o.z + best_t * d.z;
+            float f, nb0, nb1, nb2;
+            if (sdf_eval(P, k0, k1, x0, x1, x2, f, nb0, nb1, nb2)) {
+                const float l = sqrtf((nb0 * nb0 + nb1 * nb1) + nb2 * nb2);
+                if (l > 0.0f) {
+                    hn.x = nb0 / l;
+                    hn.y = nb1 / l;
+                    hn.z = nb2 / l;
+                }
+            }
+            float bq = INFINITY;
+            for (unsigned k = k0; k < k1; ++k) {
+                const float4 A = __ldg(&P.sdf_pts[2 * k]);
+                const float e0 = A.x - x0, e1 = A.y - x1, e2 = A.z - x2;
+                const float q = (e0 * e0 + e1 * e1) + e2 * e2;
+                if (q < bq) {
+                    bq = q;
+                    pid = __float_as_int(__ldg(&P.sdf_pts[2 * k + 1]).w);
+                }
+            }
+            hn.w = __uint_as_float(__ldg(&P.sdf_acell[best]));
+        }
+        W.hit[ray] = make_float2(best >= 0 ? best_t : INFINITY, __int_as_float(pid));
+        W.hitn[ray] = hn;
+    }
+    flush_counts(P, bounces, cnt, CNT);
+}
+
 // live-list entries [n_alive, cap) get the largest key, so a sort of all cap entries puts the
 // live ones first (in key order) and needs no host-side count
 __global__ void k_pad_keys(unsigned* keys, const unsigned long long* n_alive, uint64_t cap) {
@@ -843,7 +1119,7 @@ __global__ void __launch_bounds__(128) k_shade(TP P, Wave W, int b) {
         if (on && sid >= 0 && c.seg < c.budget) {
             // A4: reflect at the hit surfel: d' = d - (2 d.n) n, normalised
             const float3 hp = make_float3(o.x + th * d.x, o.y + th * d.y, o.z + th * d.z);
-            const float4 nv = __ldg(&P.sn[sid]);
+            const float4 nv = P.sdf ? W.hitn[ray] : __ldg(&P.sn[sid]);  // SDF: MLS normal (R44)
             const float3 nn = make_float3(nv.x, nv.y, nv.z);
             const int hn = c.h.n;
             c.h.label[hn] = __ldg(&P.label[sid]);
@@ -856,7 +1132,7 @@ __global__ void __launch_bounds__(128) k_shade(TP P, Wave W, int b) {
             const float3 x = make_float3(d.x - k2 * nn.x, d.y - k2 * nn.y, d.z - k2 * nn.z);
             const float l = sqrtf(dot3(x, x));
             W.d[ray] = make_float4(x.x / l, x.y / l, x.z / l, 0.0f);
-            W.o[ray] = make_float4(hp.x, hp.y, hp.z, __int_as_float(sid));
+            W.o[ray] = make_float4(hp.x, hp.y, hp.z, P.sdf ? nv.w : __int_as_float(sid));  // prev: surfel / cell
             W.l0[ray] = make_float4(nn.x, nn.y, nn.z, 0.0f);
             W.l1[ray] = make_float4(nn.x, nn.y, nn.z, 0.0f);
             c.L = L + th;
@@ -1071,6 +1347,26 @@ TP make_tp(nrt_scene s, const LaunchArgs& a) {
     P.rxg_tmax = a.rxg.tmax;
     P.shade_rx = a.rxg.cell ? 0 : a.n_rx;
     P.shade_edges = s->n_edges <= kShadeEdges ? s->n_edges : 0;
+    if (a.desc.intersect == 1) {  // NEXT-1 (R40-R45): FP32 constants as the definition forms them
+        P.sdf = 1;
+        P.sdf_pts = s->sdf_pts;
+        P.sdf_box = s->sdf_box;
+        P.sdf_acell = s->sdf_acell;
+        P.sdf_gcell = s->sdf_gcell;
+        P.sdf_aref = s->sdf_aref;
+        for (int k = 0; k < 3; ++k) {
+            P.sg_o[k] = s->sdf_gorg[k];
+            P.sg_n[k] = s->sdf_gdims[k];
+        }
+        P.sdf_a = s->sdf_a;
+        P.sdf_inv_a = 1.0f / s->sdf_a;
+        P.sdf_half = 0.5f * (s->sdf_a * 1.7320508f);
+        P.sdf_stop = 2.0f * P.sdf_half + s->sdf_pad;
+        P.sdf_rs = a.desc.sdf_r_s;
+        P.sdf_tsdf = a.desc.sdf_t_sdf;
+        const float sigma = a.desc.sdf_xi * a.desc.sdf_r_s;
+        P.sdf_inv = 1.0f / (2.0f * sigma * sigma);
+    }
     return P;
 }
 
@@ -1219,7 +1515,7 @@ static bool reorder_on(nrt_scene s) {
     return (double)s->nref * 32.0 > 4.0 * (double)l2;
 }
 
-static nrt_status alloc_wave(Wave& W, uint64_t cap, int dev, cudaStream_t st) {
+static nrt_status alloc_wave(Wave& W, uint64_t cap, int dev, bool sdf, cudaStream_t st) {
     if (cap < 1) cap = 1;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t b_o = al(cap * sizeof(float4)), b_h = al(cap * sizeof(float2)),
@@ -1228,7 +1524,7 @@ static nrt_status alloc_wave(Wave& W, uint64_t cap, int dev, cudaStream_t st) {
     cub::DeviceRadixSort::SortPairs(nullptr, b_t, (unsigned*)nullptr, (unsigned*)nullptr,
                                     (unsigned*)nullptr, (unsigned*)nullptr, (int)cap, 0, 32, st);
     b_t = al(b_t);
-    const size_t total = 4 * b_o + b_h + b_c + 2 * b_a + 3 * b_a + b_t;
+    const size_t total = 4 * b_o + b_h + b_c + 2 * b_a + 3 * b_a + b_t + (sdf ? b_o : 0);
     char* p = (char*)ws_get(dev, total, st);
     if (!p) return set_error(NRT_E_NOMEM, "wavefront workspace of %zu bytes", total);
     {
@@ -1238,6 +1534,7 @@ static nrt_status alloc_wave(Wave& W, uint64_t cap, int dev, cudaStream_t st) {
         W.oval = (unsigned*)(q + 2 * b_a);
         W.otmp = q + 3 * b_a;
         W.otmp_bytes = b_t;
+        W.hitn = sdf ? (float4*)(q + 3 * b_a + b_t) : nullptr;
         W.skey = nullptr;  // per-bounce coherence reorder: see reorder_on()
     }
     W.slab = p;
@@ -1272,8 +1569,10 @@ static nrt_status run_bounces(const TP& P, Wave& W, uint64_t cap, int iters, int
 #else
 #define NRT_K_TRACE k_trace
 #endif
-    const unsigned tb = counters ? persistent_blocks(NRT_K_TRACE<true>, dev)
-                                 : persistent_blocks(NRT_K_TRACE<false>, dev);
+    const unsigned tb = P.sdf ? (counters ? persistent_blocks(k_trace_sdf<true>, dev)
+                                          : persistent_blocks(k_trace_sdf<false>, dev))
+                              : (counters ? persistent_blocks(NRT_K_TRACE<true>, dev)
+                                          : persistent_blocks(NRT_K_TRACE<false>, dev));
     const unsigned sb = (unsigned)sm_count(dev) * 8;
     const size_t shade_smem = (size_t)(P.shade_rx + P.shade_edges) * sizeof(float4);
     if (shade_smem > 48 * 1024)
@@ -1287,8 +1586,14 @@ static nrt_status run_bounces(const TP& P, Wave& W, uint64_t cap, int iters, int
     }
     for (int b = 0; b < iters; ++b) {
         cudaEventRecord(ev[3 * b], st);
-        if (counters) NRT_K_TRACE<true><<<tb, 128, 0, st>>>(P, W, b);
-        else NRT_K_TRACE<false><<<tb, 128, 0, st>>>(P, W, b);
+        if (P.sdf) {
+            if (counters) k_trace_sdf<true><<<tb, 128, 0, st>>>(P, W, b);
+            else k_trace_sdf<false><<<tb, 128, 0, st>>>(P, W, b);
+        } else if (counters) {
+            NRT_K_TRACE<true><<<tb, 128, 0, st>>>(P, W, b);
+        } else {
+            NRT_K_TRACE<false><<<tb, 128, 0, st>>>(P, W, b);
+        }
         ::nrt::count_launch();
         if (counters && P.counters && getenv("NRT_BOUNCE_STATS")) {  // diagnostics: per-bounce work
             unsigned long long c[3], na = 0;
@@ -1356,7 +1661,7 @@ nrt_status launch_primary(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw
     Wave W{};
     WaveGuard wg{&W, st};
     const uint64_t kBatch = batch_rays();
-    NRT_TRY(alloc_wave(W, n_shard < kBatch ? n_shard : kBatch, s->device, st));
+    NRT_TRY(alloc_wave(W, n_shard < kBatch ? n_shard : kBatch, s->device, P.sdf != 0, st));
     if (reorder_on(s)) W.skey = W.okey[0];
     if (getenv("NRT_PHASES")) {
         cudaStreamSynchronize(st);
@@ -1485,7 +1790,7 @@ nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev
     Counters hc{};
     Wave W{};
     WaveGuard wg{&W, st};
-    if (total > 0) NRT_TRY(alloc_wave(W, total, s->device, st));
+    if (total > 0) NRT_TRY(alloc_wave(W, total, s->device, P.sdf != 0, st));
     if (total > 0 && reorder_on(s)) W.skey = W.okey[0];
     W.n_alive = dc->n_alive;
     W.ctr = dc->ctr;
@@ -1545,7 +1850,7 @@ nrt_status debug_trace(nrt_scene s, const LaunchArgs& a, const uint64_t* ids, in
     NRT_CUDA(cudaMemcpyAsync(dids, ids, n * 8, cudaMemcpyHostToDevice, st));
     Wave W{};
     WaveGuard wg{&W, st};
-    NRT_TRY(alloc_wave(W, (uint64_t)n, s->device, st));
+    NRT_TRY(alloc_wave(W, (uint64_t)n, s->device, P.sdf != 0, st));
     if (reorder_on(s)) W.skey = W.okey[0];
     W.n_alive = dc->n_alive;
     W.ctr = dc->ctr;

@@ -252,6 +252,102 @@ __global__ void k_home_counts(const uint2* hcell, int64_t nh, unsigned* cnt) {
     cnt[c] = c < nh ? hcell[c].y - hcell[c].x : 0u;
 }
 
+
+// ---- NEXT-1 AABB primitives (DESIGN R40) ------------------------------------
+// key of point i: the linear index of the a-cell holding it (division as the definition does)
+__global__ void k_sdf_keys(const float4* sp, int64_t n, float ox, float oy, float oz, float a, int dx,
+                           int dy, int dz, unsigned* keys, unsigned* vals) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 p = sp[i];
+    const int cx = min(dx - 1, max(0, (int)floorf((p.x - ox) / a)));
+    const int cy = min(dy - 1, max(0, (int)floorf((p.y - oy) / a)));
+    const int cz = min(dz - 1, max(0, (int)floorf((p.z - oz) / a)));
+    keys[i] = (unsigned)((int64_t)cx + (int64_t)dx * ((int64_t)cy + (int64_t)dy * cz));
+    vals[i] = (unsigned)i;
+}
+// points in (cell, id) order: (p, 0), (n, id bits)
+__global__ void k_sdf_pts(const unsigned* ids, int64_t n, const float4* sp, const float4* sn, float4* pts) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const unsigned id = ids[k];
+    const float4 p = sp[id], q = sn[id];
+    pts[2 * k] = make_float4(p.x, p.y, p.z, 0.0f);
+    pts[2 * k + 1] = make_float4(q.x, q.y, q.z, __uint_as_float(id));
+}
+// R40: AABB j = its points' extent per axis, or the cell's full extent where that exceeds a/2
+__global__ void k_sdf_boxes(const unsigned* cells, const unsigned* off, int64_t na, const float4* pts,
+                            float ox, float oy, float oz, float a, int dx, int dy, float4* box) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= na) return;
+    const unsigned c = cells[j], k0 = off[j], k1 = off[j + 1];
+    const int ci[3] = {(int)(c % (unsigned)dx), (int)((c / (unsigned)dx) % (unsigned)dy),
+                       (int)(c / ((unsigned)dx * (unsigned)dy))};
+    const float org[3] = {ox, oy, oz};
+    float lo[3], hi[3];
+    for (int k = 0; k < 3; ++k) {
+        float l = INFINITY, h = -INFINITY;
+        for (unsigned t = k0; t < k1; ++t) {
+            const float4 p = pts[2 * t];
+            const float v = k == 0 ? p.x : (k == 1 ? p.y : p.z);
+            if (v < l) l = v;
+            if (v > h) h = v;
+        }
+        if (h - l > 0.5f * a) {
+            l = org[k] + (float)ci[k] * a;
+            h = org[k] + (float)(ci[k] + 1) * a;
+        }
+        lo[k] = l;
+        hi[k] = h;
+    }
+    box[2 * j] = make_float4(lo[0], lo[1], lo[2], __uint_as_float(k0));
+    box[2 * j + 1] = make_float4(hi[0], hi[1], hi[2], __uint_as_float(k1));
+}
+// traversal grid: the cells the padded AABB overlaps
+struct SdfGrid {
+    float ox, oy, oz, inv_a, pad;
+    int nx, ny, nz;
+};
+__device__ __forceinline__ void sdf_cell_box(const SdfGrid& g, const float4* box, int64_t j, int lo[3],
+                                             int hi[3]) {
+    const float4 L = box[2 * j], H = box[2 * j + 1];
+    const float l[3] = {L.x, L.y, L.z}, h[3] = {H.x, H.y, H.z}, o[3] = {g.ox, g.oy, g.oz};
+    const int dim[3] = {g.nx, g.ny, g.nz};
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = max(0, min(dim[k] - 1, (int)floorf((l[k] - g.pad - o[k]) * g.inv_a)));
+        hi[k] = max(0, min(dim[k] - 1, (int)floorf((h[k] + g.pad - o[k]) * g.inv_a)));
+    }
+}
+__global__ void k_sdf_reg_count(SdfGrid g, const float4* box, int64_t na, unsigned* cnt) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= na) return;
+    int lo[3], hi[3];
+    sdf_cell_box(g, box, j, lo, hi);
+    cnt[j] = (unsigned)((hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1));
+}
+__global__ void k_sdf_reg_emit(SdfGrid g, const float4* box, int64_t na, const unsigned* off, unsigned* keys,
+                               unsigned* vals) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= na) return;
+    int lo[3], hi[3];
+    sdf_cell_box(g, box, j, lo, hi);
+    unsigned k = off[j];
+    for (int z = lo[2]; z <= hi[2]; ++z)
+        for (int y = lo[1]; y <= hi[1]; ++y)
+            for (int x = lo[0]; x <= hi[0]; ++x) {
+                keys[k] = (unsigned)(x + g.nx * (y + g.ny * z));
+                vals[k] = (unsigned)j;
+                ++k;
+            }
+}
+__global__ void k_sdf_reg_ranges(const unsigned* keys, int64_t nr, uint2* gcell) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nr) return;
+    const unsigned key = keys[k];
+    if (k == 0 || keys[k - 1] != key) gcell[key].x = (unsigned)k;
+    if (k == nr - 1 || keys[k + 1] != key) gcell[key].y = (unsigned)(k + 1);
+}
+
 template <class T>
 nrt_status dmalloc(T** p, size_t count, cudaStream_t st) {
     if (count == 0) count = 1;
@@ -295,6 +391,155 @@ static nrt_status sort_records(const Grid& g, nrt_scene S, int64_t n, const unsi
     cudaFreeAsync(k1, st);
     cudaFreeAsync(v0, st);
     cudaFreeAsync(v1, st);
+    return NRT_OK;
+}
+
+
+static int bits_for(int64_t n) {
+    int b = 1;
+    while (((int64_t)1 << b) < n) ++b;
+    return b;
+}
+
+// NEXT-1: AABB primitives (R40) + their traversal grid.  org = the points'
+// minimum, dims = floor((max - org) / a) + 1, cell of p = floor((p - org) / a) clamped, as
+// the definition (oracle/sdf.c) states them.
+static nrt_status sdf_build(nrt_scene S, float a, const float bmin[3], const float bmax[3], cudaStream_t st) {
+    const int64_t n = S->n;
+    const unsigned nb = (unsigned)((n + 255) / 256);
+    int dims[3];
+    int64_t ncell = 1;
+    for (int k = 0; k < 3; ++k) {
+        const float q = floorf((bmax[k] - bmin[k]) / a);
+        if (!(q < (float)(1 << 20))) return set_error(NRT_E_INVALID, "sdf_cell too small for the scene");
+        dims[k] = (int)q + 1;
+        ncell *= dims[k] + 2;
+    }
+    if (ncell >= ((int64_t)1 << 31)) return set_error(NRT_E_INVALID, "sdf grid has >= 2^31 cells");
+    S->sdf_a = a;
+    for (int k = 0; k < 3; ++k) {
+        S->sdf_org[k] = bmin[k];
+        S->sdf_dims[k] = dims[k];
+        S->sdf_gorg[k] = bmin[k] - a;
+        S->sdf_gdims[k] = dims[k] + 2;
+    }
+    float ext = 0.0f;
+    for (int k = 0; k < 3; ++k) ext = fmaxf(ext, fmaxf(fabsf(bmin[k]), fabsf(bmax[k])));
+    S->sdf_pad = fmaxf(fmaxf(1e-3f * a, 2e-5f), 4e-6f * ext);
+    // (cell, id) pairs, stable radix sort: ids ascend within a cell
+    unsigned *k0 = nullptr, *k1 = nullptr, *v0 = nullptr, *v1 = nullptr;
+    NRT_TRY(dmalloc(&k0, n, st));
+    NRT_TRY(dmalloc(&k1, n, st));
+    NRT_TRY(dmalloc(&v0, n, st));
+    NRT_TRY(dmalloc(&v1, n, st));
+    k_sdf_keys<<<nb, 256, 0, st>>>(S->sp, n, bmin[0], bmin[1], bmin[2], a, dims[0], dims[1], dims[2], k0, v0);
+    ::nrt::count_launch();
+    const int cbits = bits_for((int64_t)dims[0] * dims[1] * dims[2]);
+    cub::DoubleBuffer<unsigned> kb(k0, k1), vb(v0, v1);
+    size_t tb = 0;
+    void* tmp = nullptr;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, (int)n, 0, cbits, st);
+    NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+    cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, (int)n, 0, cbits, st);
+    cudaFreeAsync(tmp, st);
+    NRT_TRY(dmalloc(&S->sdf_pts, 2 * n, st));
+    k_sdf_pts<<<nb, 256, 0, st>>>(vb.Current(), n, S->sp, S->sn, S->sdf_pts);
+    ::nrt::count_launch();
+    // runs of equal cells -> AABBs (cell, first point, count)
+    unsigned *cells = nullptr, *cnt = nullptr, *off = nullptr;
+    int64_t* nruns = nullptr;
+    NRT_TRY(dmalloc(&cells, n, st));
+    NRT_TRY(dmalloc(&cnt, n + 1, st));
+    NRT_TRY(dmalloc(&off, n + 1, st));
+    NRT_TRY(dmalloc(&nruns, 1, st));
+    tb = 0;
+    cub::DeviceRunLengthEncode::Encode(nullptr, tb, kb.Current(), cells, cnt, nruns, (int64_t)n, st);
+    NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+    cub::DeviceRunLengthEncode::Encode(tmp, tb, kb.Current(), cells, cnt, nruns, (int64_t)n, st);
+    cudaFreeAsync(tmp, st);
+    int64_t na = 0;
+    NRT_CUDA(cudaMemcpyAsync(&na, nruns, 8, cudaMemcpyDeviceToHost, st));
+    NRT_CUDA(cudaStreamSynchronize(st));
+    S->n_aabb = na;
+    NRT_CUDA(cudaMemsetAsync(cnt + na, 0, 4, st));
+    tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)(na + 1), st);
+    NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, (int)(na + 1), st);
+    cudaFreeAsync(tmp, st);
+    NRT_TRY(dmalloc(&S->sdf_box, 2 * na, st));
+    const unsigned ab = (unsigned)((na + 255) / 256);
+    k_sdf_boxes<<<ab, 256, 0, st>>>(cells, off, na, S->sdf_pts, bmin[0], bmin[1], bmin[2], a, dims[0], dims[1],
+                                    S->sdf_box);
+    ::nrt::count_launch();
+    NRT_CUDA(cudaGetLastError());
+    S->sdf_acell = cells;  // [na] cell of each AABB (the tail past na is unused)
+    cudaFreeAsync(k0, st);
+    cudaFreeAsync(k1, st);
+    cudaFreeAsync(v0, st);
+    cudaFreeAsync(v1, st);
+    // traversal grid: every AABB in all cells its padded box overlaps
+    SdfGrid g;
+    g.ox = S->sdf_gorg[0];
+    g.oy = S->sdf_gorg[1];
+    g.oz = S->sdf_gorg[2];
+    g.inv_a = 1.0f / a;
+    g.pad = S->sdf_pad;
+    g.nx = S->sdf_gdims[0];
+    g.ny = S->sdf_gdims[1];
+    g.nz = S->sdf_gdims[2];
+    k_sdf_reg_count<<<ab, 256, 0, st>>>(g, S->sdf_box, na, cnt);
+    ::nrt::count_launch();
+    NRT_CUDA(cudaMemsetAsync(cnt + na, 0, 4, st));
+    tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)(na + 1), st);
+    NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, (int)(na + 1), st);
+    cudaFreeAsync(tmp, st);
+    unsigned nr32 = 0;
+    NRT_CUDA(cudaMemcpyAsync(&nr32, off + na, 4, cudaMemcpyDeviceToHost, st));
+    NRT_CUDA(cudaStreamSynchronize(st));
+    const int64_t nr = nr32;
+    S->n_aref = nr;
+    NRT_TRY(dmalloc(&k0, nr, st));
+    NRT_TRY(dmalloc(&k1, nr, st));
+    NRT_TRY(dmalloc(&v0, nr, st));
+    NRT_TRY(dmalloc(&v1, nr, st));
+    k_sdf_reg_emit<<<ab, 256, 0, st>>>(g, S->sdf_box, na, off, k0, v0);
+    ::nrt::count_launch();
+    cub::DoubleBuffer<unsigned> rkb(k0, k1), rvb(v0, v1);
+    const int gbits = bits_for(ncell);
+    tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, rkb, rvb, (int)nr, 0, gbits, st);
+    NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+    cub::DeviceRadixSort::SortPairs(tmp, tb, rkb, rvb, (int)nr, 0, gbits, st);
+    cudaFreeAsync(tmp, st);
+    NRT_TRY(dmalloc(&S->sdf_gcell, ncell, st));
+    NRT_CUDA(cudaMemsetAsync(S->sdf_gcell, 0, ncell * sizeof(uint2), st));
+    k_sdf_reg_ranges<<<(unsigned)((nr + 255) / 256), 256, 0, st>>>(rkb.Current(), nr, S->sdf_gcell);
+    ::nrt::count_launch();
+    S->sdf_aref = rvb.Current();
+    cudaFreeAsync(rvb.Current() == v0 ? v1 : v0, st);
+    cudaFreeAsync(k0, st);
+    cudaFreeAsync(k1, st);
+    cudaFreeAsync(cnt, st);
+    cudaFreeAsync(off, st);
+    cudaFreeAsync(nruns, st);
+    // empty-space skip (Chebyshev distance), as for the surfel grid
+    {
+        unsigned char *f0 = nullptr, *f1 = nullptr;
+        NRT_TRY(dmalloc(&f0, ncell, st));
+        NRT_TRY(dmalloc(&f1, ncell, st));
+        const unsigned cb = (unsigned)((ncell + 255) / 256);
+        k_occ<<<cb, 256, 0, st>>>(S->sdf_gcell, ncell, f0); ::nrt::count_launch();
+        k_cheb_pass<<<cb, 256, 0, st>>>(f0, f1, g.nx, g.ny, g.nz, 2); ::nrt::count_launch();
+        k_cheb_pass<<<cb, 256, 0, st>>>(f1, f0, g.nx, g.ny, g.nz, 1); ::nrt::count_launch();
+        k_cheb_pass<<<cb, 256, 0, st>>>(f0, f1, g.nx, g.ny, g.nz, 0); ::nrt::count_launch();
+        k_pack_skip<<<cb, 256, 0, st>>>(S->sdf_gcell, ncell, f1); ::nrt::count_launch();
+        NRT_CUDA(cudaGetLastError());
+        cudaFreeAsync(f0, st);
+        cudaFreeAsync(f1, st);
+    }
     return NRT_OK;
 }
 
@@ -512,6 +757,7 @@ static nrt_status build_impl(const nrt_scene_desc* D, nrt_scene S, cudaStream_t 
         S->hid = hvb.Current();  // kept: surfel ids of the home records (post-processing)
         cudaFreeAsync(hvb.Current() == hv0 ? hv1 : hv0, st);
     }
+    if (D->sdf_cell > 0.0f) NRT_TRY(sdf_build(S, D->sdf_cell, bmin, bmax, st));
     // labels array (int) for the history
     {
         // sn.w holds the label bits; extract with a tiny kernel-free trick: copy strided
@@ -531,6 +777,8 @@ nrt_status scene_build(const nrt_scene_desc* D, nrt_scene* out) {
     if (!(D->voxel_size > 0.0f) || !std::isfinite(D->voxel_size))
         return set_error(NRT_E_INVALID, "voxel_size must be > 0");
     if (!D->radii && !(D->radius > 0.0f)) return set_error(NRT_E_INVALID, "radius must be > 0");
+    if (!(D->sdf_cell >= 0.0f) || !std::isfinite(D->sdf_cell))
+        return set_error(NRT_E_INVALID, "sdf_cell must be finite and >= 0");
     if (D->n_edges < 0 || (D->n_edges > 0 && !D->edges))
         return set_error(NRT_E_INVALID, "bad edge array");
     NRT_CUDA(cudaSetDevice(D->device));
