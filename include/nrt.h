@@ -241,7 +241,9 @@ typedef struct {
     int64_t n_events;        /* diffraction events after local dedupe (launch) */
     int64_t n_fan_rays;      /* fan rays traced (launch) */
     uint64_t bounces;        /* segments traced: primary + fan (launch) */
-    uint64_t surfel_tests;   /* records tested (launch with counters = 1; else 0) */
+    uint64_t surfel_tests;   /* records tested (launch with counters = 1; else 0); with
+                                intersect = 1: Gaussian terms evaluated (one point in one SDF
+                                evaluation), and cells_nonempty counts AABB marches */
     uint64_t cells_visited;  /* grid cells visited by the DDA, empty or not (idem) */
     uint64_t cells_nonempty; /* non-empty cells visited (idem) */
     float ms_trace;          /* device time of the primary traversal kernel */

@@ -10,6 +10,10 @@
  *       pbar = sum w p / W, nbar = sum w n / W (Eq. 3 literally, not normalised),
  *       f = (x - pbar) . nbar; undefined ("fails") when W is not > 0.  FP32 throughout;
  *       E = the exp of sdf_expf below, written identically in the CUDA path (like R2's sincos).
+ *       Summation order (the paper fixes none): the points in chunks of 32 consecutive ones
+ *       (the last chunk padded with zero terms); each chunk summed by the pairwise tree that
+ *       halves it in place (v[i] += v[i + s], s = 16, 8, 4, 2, 1); the chunk sums added in
+ *       ascending chunk order (R41b).
  *   R42 march: for an AABB the ray enters (slab test, t_far >= 0), a segment of length
  *       L = a sqrt(3) (the AABB cell's diameter, l_d / (D_v D_sv)) centred on the projection of
  *       the AABB's centre on the ray; from its near end (clamped to t >= 0) march by |f| (r_s
@@ -42,19 +46,21 @@ struct or_sdf {
 };
 
 /* R41: exp(x) for x <= 0 in FP32, fixed operation order (Cody-Waite ln2 split + degree-7
- * Taylor polynomial, then 2^k by the exponent bits); 0 below -87 (FP32 exp underflow). */
+ * Taylor polynomial in Horner form, every multiply-add a single-rounding fmaf, then 2^k by the
+ * exponent bits); 0 below -87 (FP32 exp underflow). */
 float or_sdf_expf(float x) {
     if (x < -87.0f) return 0.0f;
-    float kf = floorf(x * 1.44269504f + 0.5f);
-    float r = (x - kf * 0.693359375f) - kf * -2.12194440e-4f;
+    float kf = floorf(fmaf(x, 1.44269504f, 0.5f));
+    float r = fmaf(kf, -0.693359375f, x);
+    r = fmaf(kf, 2.12194440e-4f, r);
     float p = 1.98412698e-4f;
-    p = p * r + 1.38888889e-3f;
-    p = p * r + 8.33333333e-3f;
-    p = p * r + 4.16666667e-2f;
-    p = p * r + 1.66666667e-1f;
-    p = p * r + 0.5f;
-    p = p * r + 1.0f;
-    p = p * r + 1.0f;
+    p = fmaf(p, r, 1.38888889e-3f);
+    p = fmaf(p, r, 8.33333333e-3f);
+    p = fmaf(p, r, 4.16666667e-2f);
+    p = fmaf(p, r, 1.66666667e-1f);
+    p = fmaf(p, r, 0.5f);
+    p = fmaf(p, r, 1.0f);
+    p = fmaf(p, r, 1.0f);
     int k = (int)kf;
     union {
         int i;
@@ -161,23 +167,39 @@ void or_sdf_aabb(const or_sdf* G, int64_t j, float lo[3], float hi[3], int64_t* 
     *n_pts = G->start[j + 1] - G->start[j];
 }
 
+/* R41b: the pairwise tree sum of one chunk of 32 terms (halved in place) */
+static float chunk_sum(float v[32]) {
+    for (int s = 16; s >= 1; s >>= 1)
+        for (int i = 0; i < s; ++i) v[i] = v[i] + v[i + s];
+    return v[0];
+}
+
 /* R41: f of AABB j at x (and nbar, unnormalised); 0 where it fails */
 int or_sdf_eval(const or_scene* S, const or_sdf* G, int64_t j, const float x[3], float sigma, float* f,
                 float nbar[3]) {
     const float inv = 1.0f / (2.0f * sigma * sigma);
-    float W = 0.0f, P[3] = {0.0f, 0.0f, 0.0f}, N[3] = {0.0f, 0.0f, 0.0f};
-    for (int64_t t = G->start[j]; t < G->start[j + 1]; ++t) {
-        const float* p = S->p + 3 * G->ids[t];
-        const float* n = S->nrm + 3 * G->ids[t];
-        float d[3] = {p[0] - x[0], p[1] - x[1], p[2] - x[2]};
-        float q = dot3f(d, d);
-        float w = or_sdf_expf(-(q * inv));
-        W = W + w;
-        for (int k = 0; k < 3; ++k) {
-            P[k] = P[k] + w * p[k];
-            N[k] = N[k] + w * n[k];
+    /* sums[0] = W, sums[1..3] = sum w p, sums[4..6] = sum w n */
+    float sums[7] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    for (int64_t c0 = G->start[j]; c0 < G->start[j + 1]; c0 += 32) {
+        float v[7][32];
+        for (int i = 0; i < 32; ++i) {
+            const int64_t t = c0 + i;
+            for (int q = 0; q < 7; ++q) v[q][i] = 0.0f;
+            if (t >= G->start[j + 1]) continue;  /* zero padding of the last chunk */
+            const float* p = S->p + 3 * G->ids[t];
+            const float* n = S->nrm + 3 * G->ids[t];
+            float d[3] = {p[0] - x[0], p[1] - x[1], p[2] - x[2]};
+            float q = fmaf(d[2], d[2], fmaf(d[1], d[1], d[0] * d[0]));  /* R41: |p - x|^2 */
+            float w = or_sdf_expf(-(q * inv));
+            v[0][i] = w;
+            for (int k = 0; k < 3; ++k) {
+                v[1 + k][i] = w * p[k];
+                v[4 + k][i] = w * n[k];
+            }
         }
+        for (int q = 0; q < 7; ++q) sums[q] = sums[q] + chunk_sum(v[q]);
     }
+    const float W = sums[0], P[3] = {sums[1], sums[2], sums[3]}, N[3] = {sums[4], sums[5], sums[6]};
     if (!(W > 0.0f)) return 0;
     float pb[3], e[3];
     for (int k = 0; k < 3; ++k) {

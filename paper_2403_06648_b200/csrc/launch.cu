@@ -795,40 +795,78 @@ __device__ __forceinline__ unsigned order_key(const TP& P, float3 h, float3 d) {
 // =======================================================================================
 // NEXT-1: the paper's point-set SDF intersection (DESIGN R40-R45, §6.4)
 // =======================================================================================
-// R41: FP32 exp for x <= 0, the definition's fixed operation order (identical to the oracle's)
+// R41: FP32 exp for x <= 0, the definition's fixed operation order (identical to the oracle's:
+// Cody-Waite split and Horner steps as single-rounding FMAs); 0 below -87 (branch-free)
 __device__ __forceinline__ float sdf_expf(float x) {
-    if (x < -87.0f) return 0.0f;
-    const float kf = floorf(x * 1.44269504f + 0.5f);
-    const float r = (x - kf * 0.693359375f) - kf * -2.12194440e-4f;
+    const float kf = floorf(__fmaf_rn(x, 1.44269504f, 0.5f));
+    float r = __fmaf_rn(kf, -0.693359375f, x);
+    r = __fmaf_rn(kf, 2.12194440e-4f, r);
     float p = 1.98412698e-4f;
-    p = p * r + 1.38888889e-3f;
-    p = p * r + 8.33333333e-3f;
-    p = p * r + 4.16666667e-2f;
-    p = p * r + 1.66666667e-1f;
-    p = p * r + 0.5f;
-    p = p * r + 1.0f;
-    p = p * r + 1.0f;
-    return p * __int_as_float(((int)kf + 127) << 23);
+    p = __fmaf_rn(p, r, 1.38888889e-3f);
+    p = __fmaf_rn(p, r, 8.33333333e-3f);
+    p = __fmaf_rn(p, r, 4.16666667e-2f);
+    p = __fmaf_rn(p, r, 1.66666667e-1f);
+    p = __fmaf_rn(p, r, 0.5f);
+    p = __fmaf_rn(p, r, 1.0f);
+    p = __fmaf_rn(p, r, 1.0f);
+    const float e = p * __int_as_float(((int)kf + 127) << 23);
+    return x < -87.0f ? 0.0f : e;
 }
 
-// R41: f and nbar (unnormalised) of the AABB whose points are [k0, k1) at x; false = fails
+// R41/R41b: f and nbar (unnormalised) of the AABB whose points are [k0, k1) at x; false = fails.
+// Warp-cooperative (called by all 32 lanes with the same arguments).  The definition sums the
+// terms in chunks of 32 points, each chunk by the pairwise tree (pairs i, i + s for s = 16, 8,
+// 4, 2, 1), the chunk totals in ascending order.  Here half-warp h takes chunk 2m + h of
+// iteration m; its lane i computes the terms of points i and i + 16 and adds them (tree level
+// s = 16, in registers), then levels 8, 4, 2, 1 run across the half-warp's lanes as a
+// multi-value butterfly (at s = 8 a lane keeps four of the eight quantities and trades the
+// other four, at s = 4 two, at s = 2 one), so quantity q = (lane >> 1) & 7 ends in lanes 2q,
+// 2q + 1 of both halves; the two chunk totals are added to the running sums in chunk order.
+// Padding terms (past k1) are zero, as in the definition.
+template <bool CNT>
 __device__ __forceinline__ bool sdf_eval(const TP& P, unsigned k0, unsigned k1, float x0, float x1, float x2,
-                                         float& f, float& nb0, float& nb1, float& nb2) {
-    float W = 0.0f, p0 = 0.0f, p1 = 0.0f, p2 = 0.0f, n0 = 0.0f, n1 = 0.0f, n2 = 0.0f;
-    for (unsigned k = k0; k < k1; ++k) {
-        const float4 A = __ldg(&P.sdf_pts[2 * k]), B = __ldg(&P.sdf_pts[2 * k + 1]);
-        const float d0 = A.x - x0, d1 = A.y - x1, d2 = A.z - x2;
-        const float q = (d0 * d0 + d1 * d1) + d2 * d2;
-        const float w = sdf_expf(-(q * P.sdf_inv));
-        W = W + w;
-        p0 = p0 + w * A.x;
-        n0 = n0 + w * B.x;
-        p1 = p1 + w * A.y;
-        n1 = n1 + w * B.y;
-        p2 = p2 + w * A.z;
-        n2 = n2 + w * B.z;
+                                         float& f, float& nb0, float& nb1, float& nb2, Cnt& cnt) {
+    const unsigned lane = threadIdx.x & 31, i = lane & 15, h = lane >> 4;
+    if (CNT && lane == 0) cnt.tests += k1 - k0;  // Gaussian terms (the SDF mode's unit of work)
+    const bool u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
+    float acc = 0.0f;
+    for (unsigned kb = k0; kb < k1; kb += 64) {
+        float v[8];
+        v[7] = 0.0f;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const unsigned k = kb + 32 * h + i + 16 * half;
+            const unsigned kc = k < k1 ? k : k1 - 1;  // padding: a valid load, weight 0
+            const float4 A = __ldg(&P.sdf_pts[2 * kc]), B = __ldg(&P.sdf_pts[2 * kc + 1]);
+            const float d0 = A.x - x0, d1 = A.y - x1, d2 = A.z - x2;
+            const float q = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, d0 * d0));
+            const float w = k < k1 ? sdf_expf(-(q * P.sdf_inv)) : 0.0f;
+            const float t[7] = {w, w * A.x, w * A.y, w * A.z, w * B.x, w * B.y, w * B.z};
+#pragma unroll
+            for (int c = 0; c < 7; ++c) v[c] = half ? v[c] + t[c] : t[c];  // level s = 16
+        }
+        float a[4], b2[2];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float snd = u8 ? v[c] : v[c + 4], kp = u8 ? v[c + 4] : v[c];
+            a[c] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const float snd = u4 ? a[c] : a[c + 2], kp = u4 ? a[c + 2] : a[c];
+            b2[c] = kp + __shfl_xor_sync(0xffffffffu, snd, 4);
+        }
+        float t = (u2 ? b2[1] : b2[0]) + __shfl_xor_sync(0xffffffffu, u2 ? b2[0] : b2[1], 2);
+        t = t + __shfl_xor_sync(0xffffffffu, t, 1);
+        const float o = __shfl_xor_sync(0xffffffffu, t, 16);
+        acc = acc + (h ? o : t);                  // chunk 2m
+        if (kb + 32 < k1) acc = acc + (h ? t : o);  // chunk 2m + 1
     }
+    const float W = __shfl_sync(0xffffffffu, acc, 0);
     if (!(W > 0.0f)) return false;
+    const float p0 = __shfl_sync(0xffffffffu, acc, 2), p1 = __shfl_sync(0xffffffffu, acc, 4),
+                p2 = __shfl_sync(0xffffffffu, acc, 6), n0 = __shfl_sync(0xffffffffu, acc, 8),
+                n1 = __shfl_sync(0xffffffffu, acc, 10), n2 = __shfl_sync(0xffffffffu, acc, 12);
     const float b0 = p0 / W, b1 = p1 / W, b2 = p2 / W;
     nb0 = n0 / W;
     nb1 = n1 / W;
@@ -862,8 +900,9 @@ __device__ __forceinline__ float sdf_slab(const float3 o, const float3 d, const 
 }
 
 // R42: the march of AABB (L, H) along the ray; true and t on a hit
+template <bool CNT>
 __device__ __forceinline__ bool sdf_march(const TP& P, const float3 o, const float3 d, const float4 L,
-                                          const float4 H, float& t_hit) {
+                                          const float4 H, float& t_hit, Cnt& cnt) {
     const unsigned k0 = __float_as_uint(L.w), k1 = __float_as_uint(H.w);
     const float c0 = 0.5f * (L.x + H.x), c1 = 0.5f * (L.y + H.y), c2 = 0.5f * (L.z + H.z);
     const float w0 = c0 - o.x, w1 = c1 - o.y, w2 = c2 - o.z;
@@ -872,7 +911,7 @@ __device__ __forceinline__ bool sdf_march(const TP& P, const float3 o, const flo
     const float te = tc + P.sdf_half;
     if (t < 0.0f) t = 0.0f;
     float f0, f1, nb0, nb1, nb2;
-    bool ok0 = sdf_eval(P, k0, k1, o.x + t * d.x, o.y + t * d.y, o.z + t * d.z, f0, nb0, nb1, nb2);
+    bool ok0 = sdf_eval<CNT>(P, k0, k1, o.x + t * d.x, o.y + t * d.y, o.z + t * d.z, f0, nb0, nb1, nb2, cnt);
     for (int it = 0; it < 4096; ++it) {
         if (ok0 && fabsf(f0) < P.sdf_tsdf) {
             t_hit = t;
@@ -881,7 +920,8 @@ __device__ __forceinline__ bool sdf_march(const TP& P, const float3 o, const flo
         const float step = ok0 ? fabsf(f0) : P.sdf_rs;
         const float t1 = t + step;
         if (t1 > te) return false;
-        const bool ok1 = sdf_eval(P, k0, k1, o.x + t1 * d.x, o.y + t1 * d.y, o.z + t1 * d.z, f1, nb0, nb1, nb2);
+        const bool ok1 =
+            sdf_eval<CNT>(P, k0, k1, o.x + t1 * d.x, o.y + t1 * d.y, o.z + t1 * d.z, f1, nb0, nb1, nb2, cnt);
         if (ok0 && ok1 && ((f0 < 0.0f) != (f1 < 0.0f))) {
             t_hit = t + step * (f0 / (f0 - f1));
             return true;
@@ -896,10 +936,12 @@ __device__ __forceinline__ bool sdf_march(const TP& P, const float3 o, const flo
 // R43 departure sheet: the AABB is transparent when its SDF at the origin is defined with
 // |f| <= tau and its unit normal lies within theta_ex of a departure normal (l0, l1; zero
 // vectors stand for "no departure normal", which never excludes since cos_ex > 0)
+template <bool CNT>
 __device__ __forceinline__ bool sdf_excluded(const TP& P, const float3 o, const float3 l0, const float3 l1,
-                                             const float4 L, const float4 H) {
+                                             const float4 L, const float4 H, Cnt& cnt) {
     float f, nb0, nb1, nb2;
-    if (!sdf_eval(P, __float_as_uint(L.w), __float_as_uint(H.w), o.x, o.y, o.z, f, nb0, nb1, nb2)) return false;
+    if (!sdf_eval<CNT>(P, __float_as_uint(L.w), __float_as_uint(H.w), o.x, o.y, o.z, f, nb0, nb1, nb2, cnt))
+        return false;
     if (!(fabsf(f) <= P.tau)) return false;
     const float l = sqrtf((nb0 * nb0 + nb1 * nb1) + nb2 * nb2);
     if (!(l > 0.0f)) return false;
@@ -908,23 +950,32 @@ __device__ __forceinline__ bool sdf_excluded(const TP& P, const float3 o, const 
     return fabsf((u0 * l1.x + u1 * l1.y) + u2 * l1.z) >= P.cos_ex;
 }
 
-// TRACE (SDF mode): per lane one segment; a 3D-DDA over the AABB traversal grid (Chebyshev
-// jumps over empty cells).  AABB j is marched once per segment, in the non-empty cell whose
-// interval [t_lo, t_out) holds its slab entry tn (t_lo = exit of the previous non-empty cell:
-// the intervals tile the segment, and the padded registration puts j in that cell); the walk
-// stops once best_t < t_out - (2 half + pad), below which no later AABB's march can start.
-// The hit is the lexicographic min (t, AABB index) = min (t, cell), as R43 defines it.
+#ifndef NRT_SDF_MINB
+#define NRT_SDF_MINB 4  // k_trace_sdf: min resident blocks/SM (register cap 128)
+#endif
+// TRACE (SDF mode): one WARP per segment.  A 3D-DDA over the AABB traversal grid (Chebyshev
+// jumps over empty cells), executed uniformly by the warp; in a non-empty cell the lanes slab-
+// test the cell's registered AABBs in parallel, and the warp marches the candidates one after
+// the other, each SDF evaluation spread over the lanes (sdf_eval).  AABB j is marched once per
+// segment, in the non-empty cell whose interval [t_lo, t_out) holds its slab entry tn (t_lo =
+// exit of the previous non-empty cell: the intervals tile the segment, and the padded
+// registration puts j in that cell); the walk stops once best_t < t_out - (2 half + pad),
+// below which no later AABB's march can start.  The hit is the lexicographic min (t, AABB
+// index) = min (t, cell), as R43 defines it.
 template <bool CNT>
-__global__ void __launch_bounds__(128) k_trace_sdf(TP P, Wave W, int b) {
+__global__ void __launch_bounds__(128, NRT_SDF_MINB) k_trace_sdf(TP P, Wave W, int b) {
     const unsigned long long n = W.n_alive[b];
     const unsigned* alive = W.alive[b & 1];
+    const unsigned lane = threadIdx.x & 31;
     unsigned long long bounces = 0;
     Cnt cnt;
     for (;;) {
-        const unsigned long long jj = lane_inc(&W.ctr[b]);
+        unsigned long long jj = 0;
+        if (lane == 0) jj = atomicAdd(&W.ctr[b], 1ull);
+        jj = __shfl_sync(0xffffffffu, jj, 0);
         if (jj >= n) break;
         const unsigned ray = alive[jj];
-        ++bounces;
+        if (lane == 0) ++bounces;
         const float4 o4 = W.o[ray], d4 = W.d[ray], a4 = W.l0[ray], c4 = W.l1[ray];
         const float3 o = make_float3(o4.x, o4.y, o4.z), d = make_float3(d4.x, d4.y, d4.z);
         const float3 l0 = make_float3(a4.x, a4.y, a4.z), l1 = make_float3(c4.x, c4.y, c4.z);
@@ -933,9 +984,10 @@ __global__ void __launch_bounds__(128) k_trace_sdf(TP P, Wave W, int b) {
         const unsigned prev = __float_as_uint(o4.w);  // cell of the previous hit (~0: none)
         float best_t = INFINITY;
         int best = -1;
-        // grid entry
+        // grid entry (uniform across the warp)
         const float ov[3] = {o.x, o.y, o.z}, dv[3] = {d.x, d.y, d.z};
         float inv[3], t0 = 0.0f, t1 = INFINITY;
+#pragma unroll
         for (int k = 0; k < 3; ++k) {
             inv[k] = rcp_approx(dv[k]);  // walk only (§6.4)
             const float lo = P.sg_o[k], hi = P.sg_o[k] + (float)P.sg_n[k] * P.sdf_a;
@@ -950,6 +1002,7 @@ __global__ void __launch_bounds__(128) k_trace_sdf(TP P, Wave W, int b) {
         if (t0 <= t1) {
             int c[3];
             float tm[3];
+#pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const float p = ov[k] + t0 * dv[k];
                 c[k] = min(P.sg_n[k] - 1, max(0, (int)floorf((p - P.sg_o[k]) * P.sdf_inv_a)));
@@ -961,24 +1014,35 @@ __global__ void __launch_bounds__(128) k_trace_sdf(TP P, Wave W, int b) {
             for (;;) {
                 const float t_out = fminf(tm[0], fminf(tm[1], tm[2]));
                 const uint2 rg = __ldg(&P.sdf_gcell[c[0] + P.sg_n[0] * (c[1] + P.sg_n[1] * c[2])]);
-                if (CNT) cnt.cells++;
+                if (CNT && lane == 0) cnt.cells++;
                 int D = 1;
                 if (rg.y > rg.x) {
-                    if (CNT) cnt.nonempty++;
-                    for (unsigned q = rg.x; q < rg.y; ++q) {
-                        const unsigned j = __ldg(&P.sdf_aref[q]);
-                        if (__ldg(&P.sdf_acell[j]) == prev) continue;
-                        const float4 L = __ldg(&P.sdf_box[2 * j]), H = __ldg(&P.sdf_box[2 * j + 1]);
-                        const float tn = sdf_slab(o, d, L, H);
-                        if (tn < 0.0f) continue;
-                        if ((!first && tn < t_lo) || !(tn < t_out)) continue;  // owner cell only
-                        if (CNT) cnt.tests++;
-                        float t;
-                        if (!sdf_march(P, o, d, L, H, t)) continue;
-                        if (!(t < best_t || (t == best_t && (int)j < best))) continue;
-                        if (has_lam && sdf_excluded(P, o, l0, l1, L, H)) continue;
-                        best_t = t;
-                        best = (int)j;
+                    for (unsigned base = rg.x; base < rg.y; base += 32) {
+                        // lanes: slab test + owner rule of one registered AABB each
+                        const unsigned q = base + lane;
+                        unsigned j = 0;
+                        bool cand = false;
+                        if (q < rg.y) {
+                            j = __ldg(&P.sdf_aref[q]);
+                            if (__ldg(&P.sdf_acell[j]) != prev) {
+                                const float tn = sdf_slab(o, d, __ldg(&P.sdf_box[2 * j]), __ldg(&P.sdf_box[2 * j + 1]));
+                                cand = tn >= 0.0f && (first || !(tn < t_lo)) && tn < t_out;  // owner cell only
+                            }
+                        }
+                        unsigned m = __ballot_sync(0xffffffffu, cand);
+                        while (m) {  // warp: march the candidates
+                            const int src = __ffs(m) - 1;
+                            m &= m - 1;
+                            const unsigned jm = __shfl_sync(0xffffffffu, j, src);
+                            if (CNT && lane == 0) cnt.nonempty++;  // SDF mode: AABB marches
+                            const float4 L = __ldg(&P.sdf_box[2 * jm]), H = __ldg(&P.sdf_box[2 * jm + 1]);
+                            float t;
+                            if (!sdf_march<CNT>(P, o, d, L, H, t, cnt)) continue;
+                            if (!(t < best_t || (t == best_t && (int)jm < best))) continue;
+                            if (has_lam && sdf_excluded<CNT>(P, o, l0, l1, L, H, cnt)) continue;
+                            best_t = t;
+                            best = (int)jm;
+                        }
                     }
                     first = false;
                     t_lo = t_out;
@@ -989,13 +1053,22 @@ __global__ void __launch_bounds__(128) k_trace_sdf(TP P, Wave W, int b) {
                 // grid move: DDA step, or a Chebyshev jump across the empty box (as k_trace)
                 if (D <= 1) {
                     const int ax = (tm[0] <= tm[1] && tm[0] <= tm[2]) ? 0 : (tm[1] <= tm[2] ? 1 : 2);
-                    c[ax] += dv[ax] > 0.0f ? 1 : -1;
-                    if (c[ax] < 0 || c[ax] >= P.sg_n[ax]) break;
-                    tm[ax] = ((P.sg_o[ax] + (float)(c[ax] + (dv[ax] > 0.0f)) * P.sdf_a) - ov[ax]) * inv[ax];
+                    const float dva = ax == 0 ? dv[0] : (ax == 1 ? dv[1] : dv[2]);
+                    int ca = (ax == 0 ? c[0] : (ax == 1 ? c[1] : c[2])) + (dva > 0.0f ? 1 : -1);
+                    const int na = ax == 0 ? P.sg_n[0] : (ax == 1 ? P.sg_n[1] : P.sg_n[2]);
+                    if (ca < 0 || ca >= na) break;
+                    const float oa = ax == 0 ? ov[0] : (ax == 1 ? ov[1] : ov[2]);
+                    const float ia = ax == 0 ? inv[0] : (ax == 1 ? inv[1] : inv[2]);
+                    const float ga = ax == 0 ? P.sg_o[0] : (ax == 1 ? P.sg_o[1] : P.sg_o[2]);
+                    const float tn = ((ga + (float)(ca + (dva > 0.0f)) * P.sdf_a) - oa) * ia;
+                    if (ax == 0) { c[0] = ca; tm[0] = tn; }
+                    else if (ax == 1) { c[1] = ca; tm[1] = tn; }
+                    else { c[2] = ca; tm[2] = tn; }
                 } else {
                     const int r = D - 1;
                     float T = INFINITY;
                     int ax = 0;
+#pragma unroll
                     for (int k = 0; k < 3; ++k) {
                         const int fk = dv[k] > 0.0f ? c[k] + r + 1 : c[k] - r;
                         const float Tk = dv[k] != 0.0f ? ((P.sg_o[k] + (float)fk * P.sdf_a) - ov[k]) * inv[k] : INFINITY;
@@ -1005,14 +1078,16 @@ __global__ void __launch_bounds__(128) k_trace_sdf(TP P, Wave W, int b) {
                         }
                     }
                     int nc[3];
+                    bool out = false;
+#pragma unroll
                     for (int k = 0; k < 3; ++k) {
                         const float pk = ov[k] + T * dv[k];
                         nc[k] = min(c[k] + r, max(c[k] - r, (int)floorf((pk - P.sg_o[k]) * P.sdf_inv_a)));
+                        if (k == ax) nc[k] = dv[k] > 0.0f ? c[k] + r + 1 : c[k] - r - 1;
+                        out |= nc[k] < 0 || nc[k] >= P.sg_n[k];
                     }
-                    nc[ax] = dv[ax] > 0.0f ? c[ax] + r + 1 : c[ax] - r - 1;
-                    bool out = false;
-                    for (int k = 0; k < 3; ++k) out |= nc[k] < 0 || nc[k] >= P.sg_n[k];
                     if (out) break;
+#pragma unroll
                     for (int k = 0; k < 3; ++k) {
                         c[k] = nc[k];
                         tm[k] = dv[k] != 0.0f
@@ -1030,7 +1105,7 @@ __global__ void __launch_bounds__(128) k_trace_sdf(TP P, Wave W, int b) {
             const unsigned k0 = __float_as_uint(L.w), k1 = __float_as_uint(H.w);
             const float x0 = o.x + best_t * d.x, x1 = o.y + best_t * d.y, x2 = o.z + best_t * d.z;
             float f, nb0, nb1, nb2;
-            if (sdf_eval(P, k0, k1, x0, x1, x2, f, nb0, nb1, nb2)) {
+            if (sdf_eval<CNT>(P, k0, k1, x0, x1, x2, f, nb0, nb1, nb2, cnt)) {
                 const float l = sqrtf((nb0 * nb0 + nb1 * nb1) + nb2 * nb2);
                 if (l > 0.0f) {
                     hn.x = nb0 / l;
@@ -1038,20 +1113,34 @@ __global__ void __launch_bounds__(128) k_trace_sdf(TP P, Wave W, int b) {
                     hn.z = nb2 / l;
                 }
             }
+            // warp argmin of (q, k): per lane ascending k with strict <, then lexicographic
             float bq = INFINITY;
-            for (unsigned k = k0; k < k1; ++k) {
+            unsigned bk = 0xffffffffu;
+            for (unsigned k = k0 + lane; k < k1; k += 32) {
                 const float4 A = __ldg(&P.sdf_pts[2 * k]);
                 const float e0 = A.x - x0, e1 = A.y - x1, e2 = A.z - x2;
                 const float q = (e0 * e0 + e1 * e1) + e2 * e2;
                 if (q < bq) {
                     bq = q;
-                    pid = __float_as_int(__ldg(&P.sdf_pts[2 * k + 1]).w);
+                    bk = k;
                 }
             }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const float oq = __shfl_xor_sync(0xffffffffu, bq, off);
+                const unsigned ok = __shfl_xor_sync(0xffffffffu, bk, off);
+                if (oq < bq || (oq == bq && ok < bk)) {
+                    bq = oq;
+                    bk = ok;
+                }
+            }
+            pid = __float_as_int(__ldg(&P.sdf_pts[2 * bk + 1]).w);
             hn.w = __uint_as_float(__ldg(&P.sdf_acell[best]));
         }
-        W.hit[ray] = make_float2(best >= 0 ? best_t : INFINITY, __int_as_float(pid));
-        W.hitn[ray] = hn;
+        if (lane == 0) {
+            W.hit[ray] = make_float2(best >= 0 ? best_t : INFINITY, __int_as_float(pid));
+            W.hitn[ray] = hn;
+        }
     }
     flush_counts(P, bounces, cnt, CNT);
 }

@@ -39,3 +39,12 @@ for mode in (0, 1):
                               ms_trace=round(i["ms_trace"], 3), bounces=int(i["bounces"]),
                               n=int(i["n"]), n_raw=int(i["n_raw"]), fans=int(i["n_fan_rays"]),
                               gbounce_s=round(i["bounces"] / wall / 1e6, 3))))
+# work counters (instrumented kernels): per segment cells, AABB marches, Gaussian terms
+for mode in (0, 1):
+    p = N.launch_case(sc, case, intersect=mode, counters=1)
+    i = p.info()
+    b = max(1, i["bounces"])
+    print(json.dumps(dict(mode="sdf" if mode else "disk", counters=True, ms_trace=round(i["ms_trace"], 3),
+                          cells_per_seg=round(i["cells_visited"] / b, 2),
+                          nonempty_or_marches_per_seg=round(i["cells_nonempty"] / b, 2),
+                          tests_or_terms_per_seg=round(i["surfel_tests"] / b, 1))))

@@ -168,3 +168,47 @@ def test_dense_box_room_finds_every_image_path(O):
     assert set(img) <= keys, set(img) - keys
     assert len(keys - set(img)) <= 4
     assert nb == case.n_rays * 3  # closed room: every ray traces max_refl + 1 segments
+
+
+def test_sdf_eval_vs_fp64_eqs_1_4(O):
+    """R41/R41b: the FP32 chunked-tree sums agree with Eqs. 1-4 evaluated in FP64 by numpy
+    (exp from libm) within FP32 rounding, on AABBs of 1-600 noisy points (several chunks of 32
+    and a ragged last chunk), so a dropped, duplicated or mis-weighted term fails."""
+    rng = np.random.default_rng(7)
+    P = rng.uniform(-0.3, 0.3, (60_000, 3))
+    P[:, 2] = 0.02 * np.sin(7 * P[:, 0]) + rng.normal(0, 0.002, len(P))
+    P = np.concatenate([P, [[0.29, 0.29, 0.3]]])  # a lone point: a 1-point AABB
+    Nn = rng.normal(0, 0.15, (len(P), 3))
+    Nn[:, 2] += 1.0
+    Nn /= np.linalg.norm(Nn, axis=1, keepdims=True)
+    s = G.Scene(P.astype(np.float32), Nn.astype(np.float32), np.full(len(P), 0.01, np.float32),
+                np.zeros(len(P), np.int32), G.Edges.empty())
+    sc = O.OracleScene(s, sdf_cell=SDF["cell"])
+    L = O.lib()
+    sigma = np.float32(SDF["xi"] * SDF["r_s"])
+    pts64, nrm64 = s.points.astype(np.float64), s.normals.astype(np.float64)
+    org = s.points.min(axis=0)
+    a = np.float32(SDF["cell"])
+    cells = np.floor((s.points - org) / a).astype(np.int64)
+    n_aabb = L.or_sdf_count(sc.sdf)
+    sizes = []
+    for j in rng.permutation(n_aabb)[:60].tolist() + [n_aabb - 1]:
+        lo, hi = np.zeros(3, np.float32), np.zeros(3, np.float32)
+        cell, npt = C.c_int64(), C.c_int64()
+        L.or_sdf_aabb(sc.sdf, j, lo.ctypes.data, hi.ctypes.data, C.byref(cell), C.byref(npt))
+        dims = np.floor((s.points.max(axis=0) - org) / a).astype(np.int64) + 1
+        lin = cells[:, 0] + dims[0] * (cells[:, 1] + dims[1] * cells[:, 2])
+        ids = np.nonzero(lin == cell.value)[0]
+        assert len(ids) == npt.value
+        sizes.append(len(ids))
+        x = np.float32((lo + hi) / 2 + rng.uniform(-0.03, 0.03, 3))
+        f, nb = C.c_float(), np.zeros(3, np.float32)
+        assert L.or_sdf_eval(C.byref(sc.c), sc.sdf, j, x.ctypes.data, float(sigma), C.byref(f), nb.ctypes.data)
+        dd = pts64[ids] - x.astype(np.float64)
+        w = np.exp(-(dd * dd).sum(1) / (2.0 * float(sigma) ** 2))
+        pb = (w[:, None] * pts64[ids]).sum(0) / w.sum()
+        nbar = (w[:, None] * nrm64[ids]).sum(0) / w.sum()
+        f64 = float((x.astype(np.float64) - pb) @ nbar)
+        assert np.allclose(nb, nbar, rtol=0, atol=2e-6), (j, nb, nbar)
+        assert abs(f.value - f64) <= 2e-6 + 1e-5 * abs(f64), (j, f.value, f64)
+    assert max(sizes) > 64 and min(sizes) == 1
