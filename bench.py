@@ -34,6 +34,13 @@ L2_FLUSH_BYTES = 512 << 20
 # difference 3, squared distance 5, weight 1 + exp 22, sums W/P/N 13) and a derivative pass of
 # the analytic Jacobian (the same 31 + W, sum w d, sum w d d^T, sum w n, sum w n d^T = 43)
 FLOPS_VALUE, FLOPS_DERIV = 44, 74
+# NEXT-1 (--intersect sdf): FP32 operations per Gaussian term of the SDF evaluation (DESIGN.md
+# §6.4: difference 3, |p-x|^2 5, weight 1, exp 21, products 7, tree sums 7)
+FLOPS_SDF_TERM = 44
+SDF = dict(cell=0.0625, r_s=0.015, t_sdf=0.0015, xi=2.0)  # Table I / P:131 (DESIGN R40-R45)
+# FP32 peak (no measured figure in MEASURED_PEAKS.json): 148 SMs x 128 FP32 lanes x 2 flops
+# (FFMA) x 1.965 GHz (B200_PROFILING.md: SM count and clocks.max.sm)
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
 def peaks():
@@ -146,8 +153,8 @@ class Runner:
         self.tx = t(case.tx)
         self.rx = t(case.rx.reshape(-1, 3))
         self.n_rays = case.n_rays * (world if scaling == "weak" else 1)
-        self.desc = dict(kappa=case.kappa, tau=case.tau, c_R=case.c_R, dphi_deg=case.dphi_deg,
-                         theta_ex_deg=case.theta_ex_deg, edge_bin=case.edge_bin)
+        self.desc = N.case_desc(case)  # with case.sdf: intersect = 1 and the SDF parameters
+        self.sdf_cell = float(case.sdf["cell"]) if getattr(case, "sdf", None) else 0.0
         self.rdesc = dict(xi=case.xi, r_s=case.r_s, tau=case.tau, theta_ex_deg=case.theta_ex_deg)
 
     def step(self, counters=0):
@@ -157,7 +164,7 @@ class Runner:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record(self.stream)
         sc = N.nrt_scene_build_ex(self.pts, self.nrm, c.voxel, radii=self.rad, labels=self.lab,
-                                  edges=c.scene.edges, stream=self.stream)
+                                  edges=c.scene.edges, stream=self.stream, sdf_cell=self.sdf_cell)
         ev[1].record(self.stream)
         if self.world == 1:
             coarse = N.nrt_launch_ex(sc, self.tx, self.rx, self.n_rays, c.max_refl, c.max_diff,
@@ -198,10 +205,11 @@ def e2e_step(N, case, host, n_rays, world, rank, stream):
     distributed launch + refinement, D2H of the global refined set."""
     from paper_2403_06648_b200 import dist as D
     import torch
+    sdf_cell = float(case.sdf["cell"]) if getattr(case, "sdf", None) else 0.0
     sc = N.nrt_scene_build_ex(host["p"], host["n"], case.voxel, radii=host["r"],
-                              labels=host["l"], edges=case.scene.edges, stream=stream)
-    desc = dict(kappa=case.kappa, tau=case.tau, c_R=case.c_R, dphi_deg=case.dphi_deg,
-                theta_ex_deg=case.theta_ex_deg, edge_bin=case.edge_bin)
+                              labels=host["l"], edges=case.scene.edges, stream=stream,
+                              sdf_cell=sdf_cell)
+    desc = N.case_desc(case)
     if world == 1:
         coarse = N.nrt_launch_ex(sc, case.tx, case.rx, n_rays, case.max_refl, case.max_diff,
                                  stream=stream, **desc)
@@ -228,6 +236,19 @@ def oracle_voxel(case):
     return 0.03 if case.name in ("C4", "C5") else 0.05
 
 
+def oracle_scene(case):
+    """The oracle's scene: tier-1 grid (disk hit), or the tier-0 SDF tracer (case.sdf)."""
+    from oracle import oracle as O
+    if getattr(case, "sdf", None):
+        return O.OracleScene(case.scene, sdf_cell=case.sdf["cell"])
+    return O.OracleScene(case.scene, grid_voxel=oracle_voxel(case))
+
+
+def oracle_kind(case):
+    return ("tier-0 SDF oracle (oracle/sdf.c, every AABB per segment)" if getattr(case, "sdf", None)
+            else "tier-1 grid oracle")
+
+
 def _oracle_chunk(args):
     case, ids = args
     from oracle import oracle as O
@@ -242,7 +263,7 @@ def cpu_baseline(case, seconds=15.0):
     from oracle import oracle as O
     O.lib()
     P = os.cpu_count() or 1
-    O._FORK["scene"] = O.OracleScene(case.scene, grid_voxel=oracle_voxel(case))
+    O._FORK["scene"] = oracle_scene(case)
     ids = np.arange(0, case.n_rays, max(1, case.n_rays // 997), dtype=np.uint64)
     t0 = time.perf_counter()
     nb0 = _oracle_chunk((case, ids[:64]))
@@ -263,13 +284,16 @@ def cpu_baseline(case, seconds=15.0):
     return {"value": bounces / wall, "unit": UNIT, "cores": P, "kind": "oracle",
             "value_1core": one_core,
             "sample": f"{len(sample)} primary rays of {case.name}'s lattice (evenly spaced ids; "
-                      f"tier-1 grid oracle over {case.scene.n} surfels, {len(case.rx)} RX; "
+                      f"{oracle_kind(case)} over {case.scene.n} surfels, {len(case.rx)} RX; "
                       f"coarse tracing only), {wall:.1f} s wall on {P} processes"}
 
 
 def run_config(case, world, scaling):
     n_total = case.n_rays * (world if scaling == "weak" else 1)
-    return {"workload": f"{case.name}: {case.scene.name}, 1 TX/{len(case.rx)} RX, "
+    hit = (" SDF intersection (NEXT-1: AABB edge %g m, r_s %g, t_sdf %g, xi %g);"
+           % (case.sdf["cell"], case.sdf["r_s"], case.sdf["t_sdf"], case.sdf["xi"])
+           if getattr(case, "sdf", None) else "")
+    return {"workload": f"{case.name}: {case.scene.name},{hit} 1 TX/{len(case.rx)} RX, "
                         f"{n_total} rays in total ({scaling} scaling over {world} GPU(s)), "
                         f"max_refl {case.max_refl}, max_diff {case.max_diff}; "
                         f"step = scene build + launch + refine",
@@ -287,8 +311,8 @@ def run_reference(args, case):
     O.lib()
     import multiprocessing as mp
     P = os.cpu_count() or 1
-    O._FORK["scene"] = O.OracleScene(case.scene, grid_voxel=oracle_voxel(case))
-    rays_per_step = 512 * P
+    O._FORK["scene"] = oracle_scene(case)
+    rays_per_step = (64 if getattr(case, "sdf", None) else 512) * P
     times, bounces = [], []
     ctx = mp.get_context("fork")
     with ctx.Pool(P) as pool:
@@ -310,7 +334,7 @@ def run_reference(args, case):
                            sample=f"oracle: {rays_per_step} primary rays of the lattice per step"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "oracle",
                              "sample": f"{rays_per_step} primary rays per step of {case.name} "
-                                       f"(tier-1 grid oracle over {case.scene.n} surfels, "
+                                       f"({oracle_kind(case)} over {case.scene.n} surfels, "
                                        f"coarse tracing only)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -328,10 +352,14 @@ def main():
     ap.add_argument("--sigma", type=float, default=0.010)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--intersect", default="disk", choices=["disk", "sdf"],
+                    help="sdf: NEXT-1, the paper's point-set SDF intersection (secondary lines)")
     args = ap.parse_args()
 
     import nrt_gen as G
     case = G.case(args.config, sigma=args.sigma) if args.config.startswith("C2") else G.case(args.config)
+    if args.intersect == "sdf":
+        case.sdf = dict(SDF)
     if args.impl == "reference":
         run_reference(args, case)
         return
@@ -385,13 +413,27 @@ def main():
     # ---- rooflines: the traversal (HBM, BJ's "% of HBM roofline") and the refinement (FP64)
     hbm, src = peaks()
     prim_only = prim_counts(N, R, case)
-    pb = 32 * prim_only["tests"] + 8 * prim_only["cells"]
-    achieved = pb / (ms_trace / 1000.0) / 1e9
-    roof_trace = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                  "frac": achieved / hbm, "traffic": measured_traffic(case.name),
-                  "kernel": "k_trace (primary bounces)", "peak_source": src,
-                  "bytes_per_launch": pb, "bytes_per_bounce": pb / max(1, prim_only["bounces"]),
-                  "ms_per_launch": ms_trace}
+    if R.sdf_cell > 0:
+        # NEXT-1: the SDF trace is FP32-ALU bound (Gaussian terms of Eqs. 1-4)
+        fl = FLOPS_SDF_TERM * prim_only["tests"]
+        achieved = fl / (ms_trace / 1000.0) / 1e12
+        roof_trace = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+                      "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
+                      "traffic": measured_traffic(case.name + "_sdf"),
+                      "kernel": "k_trace_sdf (primary bounces; one warp per segment)",
+                      "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz",
+                      "flops_per_launch": fl, "gaussian_terms": prim_only["tests"],
+                      "terms_per_bounce": prim_only["tests"] / max(1, prim_only["bounces"]),
+                      "marches_per_bounce": prim_only["nonempty"] / max(1, prim_only["bounces"]),
+                      "ms_per_launch": ms_trace}
+    else:
+        pb = 32 * prim_only["tests"] + 8 * prim_only["cells"]
+        achieved = pb / (ms_trace / 1000.0) / 1e9
+        roof_trace = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                      "frac": achieved / hbm, "traffic": measured_traffic(case.name),
+                      "kernel": "k_trace (primary bounces)", "peak_source": src,
+                      "bytes_per_launch": pb, "bytes_per_bounce": pb / max(1, prim_only["bounces"]),
+                      "ms_per_launch": ms_trace}
     fp64 = N.nrt_probe_fp64_tflops(local)
     flops = FLOPS_VALUE * cnt["mls_value"] + FLOPS_DERIV * cnt["mls_deriv"]
     ach_f = flops / (ms_refine / 1000.0) / 1e12 if ms_refine else 0.0
@@ -468,7 +510,7 @@ def post_timing(N, R, case, reps=3):
     """Device time of nrt_postprocess on this workload's refined set (median of reps)."""
     import torch
     sc = N.nrt_scene_build_ex(R.pts, R.nrm, case.voxel, radii=R.rad, labels=R.lab,
-                              edges=case.scene.edges, stream=R.stream)
+                              edges=case.scene.edges, stream=R.stream, sdf_cell=R.sdf_cell)
     coarse = N.nrt_launch_ex(sc, R.tx, R.rx, R.n_rays, case.max_refl, case.max_diff,
                              stream=R.stream, **R.desc)
     ref = N.nrt_refine_ex(sc, coarse, stream=R.stream, **R.rdesc)
@@ -501,13 +543,14 @@ def measured_traffic(key):
 def prim_counts(N, R, case):
     """Instrumented primary-only launch (stage 1: no fans) for the k_trace byte count."""
     sc = N.nrt_scene_build_ex(R.pts, R.nrm, case.voxel, radii=R.rad, labels=R.lab,
-                              edges=case.scene.edges, stream=R.stream)
+                              edges=case.scene.edges, stream=R.stream, sdf_cell=R.sdf_cell)
     p = N.nrt_launch_ex(sc, R.tx, R.rx, R.n_rays, case.max_refl, case.max_diff, counters=1,
                         stage=1, rank=R.rank, world=R.world, stream=R.stream, **R.desc)
     i = p.info()
     p.free()
     sc.free()
-    return {"tests": i["surfel_tests"], "cells": i["cells_visited"], "bounces": i["bounces"]}
+    return {"tests": i["surfel_tests"], "cells": i["cells_visited"], "bounces": i["bounces"],
+            "nonempty": i["cells_nonempty"]}
 
 
 if __name__ == "__main__":
