@@ -222,6 +222,28 @@ int or_path_jacobian(const or_scene* S, const or_refine_params* R, const or_coar
 int or_mls(const or_scene* S, const or_refine_params* R, int32_t label, const double nseed[3],
            const double x[3], double pbar[3], double nbar[3], double* f);
 
+/* ---- NEXT-4 (gd.c): the paper's gradient-descent refinement, FP32 (R50-R56) ---- */
+typedef struct {
+    or_sdf_params sdf;     /* reprojection tracing: cell = the scene's AABB edge; r_s, t_sdf of
+                              Table II's refinement rows; xi (sigma = xi r_s also for R53) */
+    int32_t rho;           /* iterations (Table I: 2000) */
+    float alpha, beta;     /* Eq. 12 line search (Table I: 0.4, 0.4) */
+    float delta;           /* ||grad f||^2 < delta (Table I: 1e-4) */
+    float t_d, t_a_deg;    /* Table III thresholds */
+    float tau, theta_ex_deg; /* departure rule of the traces (R43) */
+    float tx[3];
+    const float* rx;       /* RX table indexed by the record's rx */
+} or_gd_params;
+/* refine every coarse record (out[q] for in[q], no dedupe); needs S->sdf; 2 if missing */
+int or_refine_gd(const or_scene* S, const or_gd_params* Q, const or_coarse* in, int64_t n,
+                 or_refined* out);
+void or_gd_basis(const float n[3], float u[3], float v[3]);
+float or_gd_line_search(const float x[3], const float P[3], const float Q3[3], const float u[3],
+                        const float v[3], int diffraction, float alpha, float beta, float y[3]);
+int64_t or_sdf_cell_of(const or_scene* S, const or_sdf* G, int64_t id);
+int or_sdf_normal27(const or_scene* S, const or_sdf* G, int64_t cell, const float x[3], float sigma,
+                    float n_out[3]);
+
 /* refined-path post-processing (post.c; NEXT-3, readings R33-R36) */
 typedef struct {
     double lambda_m;       /* wavelength of the first Fresnel zone (Eq. 13) */

@@ -13,7 +13,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SRCS = ["coarse.c", "grid.c", "sdf.c", "refine.c", "post.c"]
+_SRCS = ["coarse.c", "grid.c", "sdf.c", "refine.c", "post.c", "gd.c"]
 
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
           "-Wall", "-Wno-unused-function"]
@@ -644,3 +644,91 @@ def fresnel_dup(case, a, b, cos_max, **over):
     ra = np.ascontiguousarray(np.asarray(a, REFINED_DTYPE).reshape(1))
     rb = np.ascontiguousarray(np.asarray(b, REFINED_DTYPE).reshape(1))
     return bool(lib().or_fresnel_dup(C.byref(q), float(cos_max), ra.ctypes.data, rb.ctypes.data))
+
+
+# ---- NEXT-4: the paper's gradient-descent refinement (gd.c, readings R50-R56) ----------------
+GD_DEFAULTS = dict(cell=0.0625, r_s=0.01, t_sdf=0.001, xi=2.0, rho=2000, alpha=0.4, beta=0.4,
+                   delta=1e-4, t_d=0.02, t_a_deg=1.0)  # Tables I-III (noisy, true normals)
+
+
+class _GdParams(C.Structure):
+    _fields_ = [("sdf", _SdfParams), ("rho", C.c_int32), ("alpha", C.c_float), ("beta", C.c_float),
+                ("delta", C.c_float), ("t_d", C.c_float), ("t_a_deg", C.c_float), ("tau", C.c_float),
+                ("theta_ex_deg", C.c_float), ("tx", C.c_float * 3), ("rx", C.c_void_p)]
+
+
+def gd_settings(case, **over):
+    """The NEXT-4 parameters of a case: GD_DEFAULTS < case.gd < keyword overrides."""
+    q = dict(GD_DEFAULTS)
+    q.update(getattr(case, "gd", None) or {})
+    q.update(over)
+    return q
+
+
+def _gd_params(case, **over):
+    q = gd_settings(case, **over)
+    rxa = _f32(case.rx, (-1, 3))
+    p = _GdParams()
+    p.sdf.cell, p.sdf.r_s, p.sdf.t_sdf, p.sdf.xi = q["cell"], q["r_s"], q["t_sdf"], q["xi"]
+    p.rho, p.alpha, p.beta, p.delta = int(q["rho"]), q["alpha"], q["beta"], q["delta"]
+    p.t_d, p.t_a_deg = q["t_d"], q["t_a_deg"]
+    p.tau, p.theta_ex_deg = float(case.tau), float(case.theta_ex_deg)
+    p.tx[:] = [float(x) for x in np.asarray(case.tx, np.float32)]
+    p.rx = rxa.ctypes.data
+    return p, rxa
+
+
+def gd_scene(case, **over):
+    return OracleScene(case.scene, sdf_cell=gd_settings(case, **over)["cell"])
+
+
+def gd_lib():
+    """The oracle library with the NEXT-4 entry points' argument types set."""
+    L = lib()
+    if not hasattr(L, "_gd_setup"):
+        L.or_refine_gd.argtypes = [C.POINTER(_Scene), C.POINTER(_GdParams), C.c_void_p, C.c_int64,
+                                   C.c_void_p]
+        L.or_gd_basis.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.or_gd_line_search.argtypes = [C.c_void_p] * 5 + [C.c_int, C.c_float, C.c_float, C.c_void_p]
+        L.or_gd_line_search.restype = C.c_float
+        L.or_sdf_normal27.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_int64, C.c_void_p, C.c_float,
+                                      C.c_void_p]
+        L.or_sdf_cell_of.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_int64]
+        L.or_sdf_cell_of.restype = C.c_int64
+        L._gd_setup = True
+    return L
+
+
+def refine_gd(case, coarse, scene: OracleScene | None = None, **over):
+    """NEXT-4: refine every coarse record by the paper's GD (no dedupe), one or_refined each."""
+    L = gd_lib()
+    sc = scene or gd_scene(case, **over)
+    p, rxa = _gd_params(case, **over)
+    cin = np.ascontiguousarray(coarse, dtype=COARSE_DTYPE)
+    out = np.zeros(cin.shape[0], REFINED_DTYPE)
+    rc = L.or_refine_gd(C.byref(sc.c), C.byref(p), cin.ctypes.data, cin.shape[0], out.ctypes.data)
+    assert rc == 0, rc
+    return out
+
+
+def _gd_worker(args):
+    case, recs, over = args
+    return refine_gd(case, recs, _FORK.get("gdscene"), **over)
+
+
+def refine_gd_par(case, coarse, procs=1, **over):
+    """refine_gd() over forked single-threaded processes (out[q] is the serial result)."""
+    import multiprocessing as mp
+    lib()
+    cin = np.ascontiguousarray(coarse, dtype=COARSE_DTYPE)
+    if procs <= 1 or len(cin) < 2:
+        return refine_gd(case, cin, **over)
+    _FORK["gdscene"] = gd_scene(case, **over)
+    chunks = [cin[k::procs] for k in range(procs)]
+    with mp.get_context("fork").Pool(procs) as pool:
+        parts = pool.map(_gd_worker, [(case, c, over) for c in chunks if len(c)])
+    _FORK.pop("gdscene", None)
+    out = np.zeros(len(cin), REFINED_DTYPE)
+    for k, part in enumerate(parts):
+        out[k::procs] = part
+    return out

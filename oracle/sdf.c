@@ -322,3 +322,78 @@ int64_t or_sdf_nearest(const or_scene* S, const or_sdf* G, const or_sdf_params* 
     }
     return best;
 }
+
+/* ---- NEXT-4 helpers (gd.c) ------------------------------------------------------------ */
+/* the AABB-grid cell of point id (R40 binning) */
+int64_t or_sdf_cell_of(const or_scene* S, const or_sdf* G, int64_t id) {
+    int64_t c[3];
+    for (int k = 0; k < 3; ++k) {
+        c[k] = (int64_t)floorf((S->p[3 * id + k] - G->org[k]) / G->a);
+        if (c[k] < 0) c[k] = 0;
+        if (c[k] > G->dims[k] - 1) c[k] = G->dims[k] - 1;
+    }
+    return c[0] + G->dims[0] * (c[1] + G->dims[1] * c[2]);
+}
+
+static int64_t aabb_of_cell(const or_sdf* G, int64_t cell) {
+    int64_t lo = 0, hi = G->n_aabb - 1;
+    while (lo <= hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (G->cell[mid] == cell) return mid;
+        if (G->cell[mid] < cell) lo = mid + 1;
+        else hi = mid - 1;
+    }
+    return -1;
+}
+
+/* R53: the unit normal of Eq. 3 at x over the points of the AABBs in the 3x3x3 cells around
+ * `cell` ("additionally evaluating the points in the neighboring AABB primitives").
+ * Rows (dz, dy) ascending; a row = the points of its cells x-1..x+1 in (cell, id) order; each
+ * row summed in chunks of 32 by the R41b tree, rows and chunks added in order.  0 if W <= 0. */
+int or_sdf_normal27(const or_scene* S, const or_sdf* G, int64_t cell, const float x[3], float sigma,
+                    float n_out[3]) {
+    const float inv = 1.0f / (2.0f * sigma * sigma);
+    const int64_t cx = cell % G->dims[0], cy = (cell / G->dims[0]) % G->dims[1],
+                  cz = cell / (G->dims[0] * G->dims[1]);
+    float sums[4] = {0.0f, 0.0f, 0.0f, 0.0f}; /* W, N */
+    for (int64_t dz = -1; dz <= 1; ++dz)
+        for (int64_t dy = -1; dy <= 1; ++dy) {
+            const int64_t y = cy + dy, z = cz + dz;
+            if (y < 0 || y >= G->dims[1] || z < 0 || z >= G->dims[2]) continue;
+            /* the row's point list: cells x-1..x+1 (inside the grid), ascending; the AABBs of
+             * consecutive cells are consecutive, so the list is ids[first .. last) */
+            int64_t first = -1, last = -1;
+            for (int64_t dx = -1; dx <= 1; ++dx) {
+                const int64_t xx = cx + dx;
+                if (xx < 0 || xx >= G->dims[0]) continue;
+                const int64_t j = aabb_of_cell(G, xx + G->dims[0] * (y + G->dims[1] * z));
+                if (j < 0) continue;
+                if (first < 0) first = G->start[j];
+                last = G->start[j + 1];
+            }
+            if (first < 0) continue;
+            const int64_t* ids = G->ids + first;
+            const int64_t m = last - first;
+            for (int64_t c0 = 0; c0 < m; c0 += 32) {
+                float v[4][32];
+                for (int i = 0; i < 32; ++i) {
+                    for (int q = 0; q < 4; ++q) v[q][i] = 0.0f;
+                    if (c0 + i >= m) continue;
+                    const float* p = S->p + 3 * ids[c0 + i];
+                    const float* nn = S->nrm + 3 * ids[c0 + i];
+                    float d[3] = {p[0] - x[0], p[1] - x[1], p[2] - x[2]};
+                    float q = fmaf(d[2], d[2], fmaf(d[1], d[1], d[0] * d[0]));
+                    float w = or_sdf_expf(-(q * inv));
+                    v[0][i] = w;
+                    for (int k = 0; k < 3; ++k) v[1 + k][i] = w * nn[k];
+                }
+                for (int q = 0; q < 4; ++q) sums[q] = sums[q] + chunk_sum(v[q]);
+            }
+        }
+    if (!(sums[0] > 0.0f)) return 0;
+    float nb[3] = {sums[1] / sums[0], sums[2] / sums[0], sums[3] / sums[0]};
+    const float l = sqrtf(dot3f(nb, nb));
+    if (!(l > 0.0f)) return 0;
+    for (int k = 0; k < 3; ++k) n_out[k] = nb[k] / l;
+    return 1;
+}
