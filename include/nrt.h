@@ -175,6 +175,18 @@ typedef struct {
     int32_t counters;     /* 1 = also count the MLS candidate evaluations (nrt_paths_info
                              mls_value / mls_deriv: the algorithmic FP64 work); results are
                              unchanged */
+    int32_t method;       /* 0 = Gauss-Newton (above, default); 1 = NEXT-4: the paper's own
+                             gradient descent (DESIGN R50-R56): per interaction Eq. 12
+                             backtracking GD (alpha, beta), reflection points re-traced from
+                             I_{k-1} with the SDF intersection (sigma = xi r_s, gd_t_sdf; the
+                             scene must have sdf_cell > 0, else NRT_E_STATE), normals of Eq. 3
+                             over the hit AABB's 3x3x3 cells kept under gd_t_d / gd_t_a_deg,
+                             gd_rho iterations, valid iff ||grad f||^2 < delta, SDF visibility.
+                             FP32; tol_m, max_iter and select are not used (select must be 0) */
+    int32_t gd_rho;       /* iterations rho (Table I: 2000) */
+    double gd_t_sdf;      /* refinement t_sdf (Table II: noisy 0.001, noiseless 0.0005) */
+    double gd_t_d;        /* distance threshold t_d (m) (Table III: 0.02 noisy, 0.002 noiseless) */
+    double gd_t_a_deg;    /* angle threshold t_a (Table III: 1 with true normals, 25 estimated) */
 } nrt_refine_desc;
 void nrt_refine_desc_default(nrt_refine_desc* d);
 nrt_status nrt_refine(nrt_scene s, nrt_paths coarse, nrt_paths* refined_out);

@@ -76,7 +76,9 @@ class nrt_refine_desc(C.Structure):
                 ("delta", C.c_double), ("tau", C.c_double), ("theta_ex_deg", C.c_double),
                 ("rank", C.c_int32), ("world", C.c_int32), ("keep_invalid", C.c_int32),
                 ("select", C.c_int32), ("blocks_per_sm", C.c_int32),
-                ("stream", C.c_void_p), ("counters", C.c_int32)]
+                ("stream", C.c_void_p), ("counters", C.c_int32), ("method", C.c_int32),
+                ("gd_rho", C.c_int32), ("gd_t_sdf", C.c_double), ("gd_t_d", C.c_double),
+                ("gd_t_a_deg", C.c_double)]
 
 
 class nrt_paths_info(C.Structure):
@@ -430,6 +432,18 @@ def nrt_refine_ex(scene: Scene, coarse: Paths, **desc) -> Paths:
     h = C.c_void_p()
     _check(lib().nrt_refine_ex(scene.h, coarse.h, C.byref(d), C.byref(h)))
     return Paths(h.value)
+
+
+def gd_desc(case, **over) -> dict:
+    """NEXT-4 refine-descriptor keywords of a case (paper GD, method = 1): Tables I-III defaults
+    (noisy cloud, true normals) < case.gd < keyword overrides."""
+    q = dict(r_s=0.01, t_sdf=0.001, xi=2.0, rho=2000, alpha=0.4, beta=0.4, delta=1e-4, t_d=0.02,
+             t_a_deg=1.0)
+    q.update(getattr(case, "gd", None) or {})
+    q.update(over)
+    return dict(method=1, xi=q["xi"], r_s=q["r_s"], gd_t_sdf=q["t_sdf"], gd_rho=int(q["rho"]),
+                alpha=q["alpha"], beta=q["beta"], delta=q["delta"], gd_t_d=q["t_d"],
+                gd_t_a_deg=q["t_a_deg"], tau=case.tau, theta_ex_deg=case.theta_ex_deg)
 
 
 def nrt_postprocess(scene: Scene, refined: Paths, **desc) -> Paths:

@@ -307,6 +307,7 @@ void nrt_scene_free(nrt_scene s) {
     cudaFreeAsync(s->sdf_acell, nullptr);
     cudaFreeAsync(s->sdf_gcell, nullptr);
     cudaFreeAsync(s->sdf_aref, nullptr);
+    cudaFreeAsync(s->sdf_crange, nullptr);
     delete s;
 }
 
@@ -603,6 +604,11 @@ void nrt_refine_desc_default(nrt_refine_desc* d) {
     d->select = 0;
     d->blocks_per_sm = 0;
     d->stream = nullptr;
+    d->method = 0;
+    d->gd_rho = 2000;
+    d->gd_t_sdf = 0.001;
+    d->gd_t_d = 0.02;
+    d->gd_t_a_deg = 1.0;
 }
 
 nrt_status nrt_refine(nrt_scene s, nrt_paths coarse, nrt_paths* out) {
@@ -664,6 +670,15 @@ nrt_status nrt_refine_ex(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d
         return set_error(NRT_E_INVALID, "need 0 <= rank < world");
     if (d.select < 0 || d.select > 2) return set_error(NRT_E_INVALID, "select must be 0, 1 or 2");
     if (d.blocks_per_sm < 0) return set_error(NRT_E_INVALID, "blocks_per_sm must be >= 0");
+    if (d.method < 0 || d.method > 1) return set_error(NRT_E_INVALID, "method must be 0 or 1");
+    if (d.method == 1) {
+        if (!s->n_aabb)
+            return set_error(NRT_E_STATE, "method = 1 (paper GD) needs a scene built with sdf_cell > 0");
+        if (d.select != 0) return set_error(NRT_E_INVALID, "method = 1 supports select = 0 only");
+        if (!(d.gd_rho >= 0 && d.gd_t_sdf > 0 && d.gd_t_d >= 0 && d.gd_t_a_deg >= 0 && d.gd_t_a_deg <= 180 &&
+              d.delta > 0))
+            return set_error(NRT_E_INVALID, "bad gradient-descent parameters");
+    }
     NRT_CUDA(cudaSetDevice(s->device));
     ensure_pool(s->device);
     nrt_paths P = new nrt_paths_s();
@@ -672,7 +687,8 @@ nrt_status nrt_refine_ex(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d
     memcpy(P->tx, coarse->tx, 12);
     P->rx = coarse->rx;
     P->info.kind = NRT_PATHS_REFINED;
-    nrt_status rc = refine(s, coarse, &d, P, (cudaStream_t)d.stream);
+    nrt_status rc = d.method == 1 ? refine_gd(s, coarse, &d, P, (cudaStream_t)d.stream)
+                                  : refine(s, coarse, &d, P, (cudaStream_t)d.stream);
     if (rc == NRT_OK) pool_keep_headroom(s->device, (cudaStream_t)d.stream);
     if (rc != NRT_OK) {
         nrt_paths_free(P);

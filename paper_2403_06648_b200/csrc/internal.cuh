@@ -167,6 +167,7 @@ struct nrt_scene_s {
     unsigned* sdf_acell = nullptr;
     uint2* sdf_gcell = nullptr;
     unsigned* sdf_aref = nullptr;
+    uint2* sdf_crange = nullptr;  // [AABB-grid cells] (first, end) point of the cell's AABB (NEXT-4)
     // output-buffer size hints (largest counts seen by launches on this scene)
     unsigned long long hint_raw = 1 << 16, hint_ev = 1 << 14, hint_fan = 1 << 16;
 };
@@ -237,6 +238,8 @@ float cos_ex_of(float theta_deg);
 float cRw_of(float c_R, int64_t n_rays);
 // refine.cu
 double probe_fp64_tflops(int device);
+nrt_status refine_gd(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
+                     cudaStream_t st);  // NEXT-4 (launch.cu)
 nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
                   cudaStream_t st);
 }  // namespace nrt

@@ -125,6 +125,11 @@ struct TP {  // trace parameters (by value into the kernels)
     float sg_o[3], sdf_a, sdf_inv_a, sdf_stop;  // sdf_stop = 2 * half + pad (early exit)
     int sg_n[3];
     float sdf_half, sdf_rs, sdf_tsdf, sdf_inv;  // sdf_inv = 1 / (2 sigma^2), sigma = xi r_s
+    const uint2* sdf_crange;  // [AABB-grid cells] point range of the cell's AABB, (0, 0) if none
+    int sd_n[3];              // AABB-grid dims (R40)
+    float sd_o[3];            // AABB-grid origin (the points' minimum)
+    float sdf_sigma;          // xi r_s (FP32)
+    const float4* sn_p;       // per-point (p, r) (NEXT-4: the record point's cell)
 };
 
 __device__ __forceinline__ unsigned long long agg_inc(unsigned long long* ctr) {
@@ -824,12 +829,11 @@ __device__ __forceinline__ float sdf_expf(float x) {
 // 2q + 1 of both halves; the two chunk totals are added to the running sums in chunk order.
 // Padding terms (past k1) are zero, as in the definition.
 template <bool CNT>
-__device__ __forceinline__ bool sdf_eval(const TP& P, unsigned k0, unsigned k1, float x0, float x1, float x2,
-                                         float& f, float& nb0, float& nb1, float& nb2, Cnt& cnt) {
+__device__ __forceinline__ void sdf_accum(const TP& P, unsigned k0, unsigned k1, float x0, float x1, float x2,
+                                          float& acc, Cnt& cnt) {
     const unsigned lane = threadIdx.x & 31, i = lane & 15, h = lane >> 4;
     if (CNT && lane == 0) cnt.tests += k1 - k0;  // Gaussian terms (the SDF mode's unit of work)
     const bool u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
-    float acc = 0.0f;
     for (unsigned kb = k0; kb < k1; kb += 64) {
         float v[8];
         v[7] = 0.0f;
@@ -862,6 +866,13 @@ __device__ __forceinline__ bool sdf_eval(const TP& P, unsigned k0, unsigned k1, 
         acc = acc + (h ? o : t);                  // chunk 2m
         if (kb + 32 < k1) acc = acc + (h ? t : o);  // chunk 2m + 1
     }
+}
+
+template <bool CNT>
+__device__ __forceinline__ bool sdf_eval(const TP& P, unsigned k0, unsigned k1, float x0, float x1, float x2,
+                                         float& f, float& nb0, float& nb1, float& nb2, Cnt& cnt) {
+    float acc = 0.0f;
+    sdf_accum<CNT>(P, k0, k1, x0, x1, x2, acc, cnt);
     const float W = __shfl_sync(0xffffffffu, acc, 0);
     if (!(W > 0.0f)) return false;
     const float p0 = __shfl_sync(0xffffffffu, acc, 2), p1 = __shfl_sync(0xffffffffu, acc, 4),
@@ -873,6 +884,46 @@ __device__ __forceinline__ bool sdf_eval(const TP& P, unsigned k0, unsigned k1, 
     nb2 = n2 / W;
     const float e0 = x0 - b0, e1 = x1 - b1, e2 = x2 - b2;
     f = (e0 * nb0 + e1 * nb1) + e2 * nb2;
+    return true;
+}
+
+// R53 (NEXT-4): the unit normal of Eq. 3 at x over the points of the AABBs in the 3x3x3 cells
+// around `cell` (warp-cooperative).  Rows (dz, dy) ascending; a row = the points of its cells
+// x-1..x+1, one contiguous range of sdf_pts (AABBs of consecutive cells are consecutive), summed
+// in chunks from the row's first point (R41b); rows added in order.  false if W <= 0.
+template <bool CNT>
+__device__ __forceinline__ bool sdf_normal27(const TP& P, unsigned cell, float x0, float x1, float x2,
+                                             float& n0, float& n1, float& n2, Cnt& cnt) {
+    const int dx = P.sd_n[0], dy = P.sd_n[1], dz = P.sd_n[2];
+    const int cx = (int)(cell % (unsigned)dx), cy = (int)((cell / (unsigned)dx) % (unsigned)dy),
+              cz = (int)(cell / ((unsigned)dx * (unsigned)dy));
+    float acc = 0.0f;
+    for (int oz = -1; oz <= 1; ++oz)
+        for (int oy = -1; oy <= 1; ++oy) {
+            const int y = cy + oy, z = cz + oz;
+            if (y < 0 || y >= dy || z < 0 || z >= dz) continue;
+            unsigned first = 0xffffffffu, last = 0;
+            for (int ox = -1; ox <= 1; ++ox) {
+                const int xx = cx + ox;
+                if (xx < 0 || xx >= dx) continue;
+                const uint2 r = __ldg(&P.sdf_crange[(size_t)xx + (size_t)dx * ((size_t)y + (size_t)dy * z)]);
+                if (r.y > r.x) {
+                    if (first == 0xffffffffu) first = r.x;
+                    last = r.y;
+                }
+            }
+            if (first != 0xffffffffu) sdf_accum<CNT>(P, first, last, x0, x1, x2, acc, cnt);
+        }
+    const float W = __shfl_sync(0xffffffffu, acc, 0);
+    if (!(W > 0.0f)) return false;
+    const float a0 = __shfl_sync(0xffffffffu, acc, 8), a1 = __shfl_sync(0xffffffffu, acc, 10),
+                a2 = __shfl_sync(0xffffffffu, acc, 12);
+    const float b0 = a0 / W, b1 = a1 / W, b2 = a2 / W;
+    const float l = sqrtf((b0 * b0 + b1 * b1) + b2 * b2);
+    if (!(l > 0.0f)) return false;
+    n0 = b0 / l;
+    n1 = b1 / l;
+    n2 = b2 / l;
     return true;
 }
 
@@ -962,6 +1013,184 @@ __device__ __forceinline__ bool sdf_excluded(const TP& P, const float3 o, const 
 // registration puts j in that cell); the walk stops once best_t < t_out - (2 half + pad),
 // below which no later AABB's march can start.  The hit is the lexicographic min (t, AABB
 // index) = min (t, cell), as R43 defines it.
+// R42/R43 (warp-cooperative): the nearest SDF hit of the ray (o, d) with departure normals
+// l0, l1 (zero = none) and the previous hit's cell `prev` skipped; returns the AABB index (-1:
+// escape) and best_t.  Called by all 32 lanes with the same arguments.
+template <bool CNT>
+__device__ __forceinline__ int sdf_trace_w(const TP& P, const float3 o, const float3 d, const float3 l0,
+                                           const float3 l1, const unsigned prev, float& best_t_out, Cnt& cnt) {
+    const unsigned lane = threadIdx.x & 31;
+    const bool has_lam = l0.x != 0.0f || l0.y != 0.0f || l0.z != 0.0f || l1.x != 0.0f || l1.y != 0.0f ||
+                         l1.z != 0.0f;
+    float best_t = INFINITY;
+    int best = -1;
+    // grid entry (uniform across the warp)
+    const float ov[3] = {o.x, o.y, o.z}, dv[3] = {d.x, d.y, d.z};
+    float inv[3], t0 = 0.0f, t1 = INFINITY;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        inv[k] = rcp_approx(dv[k]);  // walk only (§6.4)
+        const float lo = P.sg_o[k], hi = P.sg_o[k] + (float)P.sg_n[k] * P.sdf_a;
+        if (dv[k] != 0.0f) {
+            const float ta = (lo - ov[k]) * inv[k], tb = (hi - ov[k]) * inv[k];
+            t0 = fmaxf(t0, fminf(ta, tb));
+            t1 = fminf(t1, fmaxf(ta, tb));
+        } else if (ov[k] < lo || ov[k] > hi) {
+            t1 = -1.0f;
+        }
+    }
+    if (t0 <= t1) {
+        int c[3];
+        float tm[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float p = ov[k] + t0 * dv[k];
+            c[k] = min(P.sg_n[k] - 1, max(0, (int)floorf((p - P.sg_o[k]) * P.sdf_inv_a)));
+            tm[k] = dv[k] != 0.0f ? ((P.sg_o[k] + (float)(c[k] + (dv[k] > 0.0f)) * P.sdf_a) - ov[k]) * inv[k]
+                                  : INFINITY;
+        }
+        float t_lo = t0;
+        bool first = true;
+        for (;;) {
+            const float t_out = fminf(tm[0], fminf(tm[1], tm[2]));
+            const uint2 rg = __ldg(&P.sdf_gcell[c[0] + P.sg_n[0] * (c[1] + P.sg_n[1] * c[2])]);
+            if (CNT && lane == 0) cnt.cells++;
+            int D = 1;
+            if (rg.y > rg.x) {
+                for (unsigned base = rg.x; base < rg.y; base += 32) {
+                    // lanes: slab test + owner rule of one registered AABB each
+                    const unsigned q = base + lane;
+                    unsigned j = 0;
+                    bool cand = false;
+                    if (q < rg.y) {
+                        j = __ldg(&P.sdf_aref[q]);
+                        if (__ldg(&P.sdf_acell[j]) != prev) {
+                            const float tn = sdf_slab(o, d, __ldg(&P.sdf_box[2 * j]), __ldg(&P.sdf_box[2 * j + 1]));
+                            cand = tn >= 0.0f && (first || !(tn < t_lo)) && tn < t_out;  // owner cell only
+                        }
+                    }
+                    unsigned m = __ballot_sync(0xffffffffu, cand);
+                    while (m) {  // warp: march the candidates
+                        const int src = __ffs(m) - 1;
+                        m &= m - 1;
+                        const unsigned jm = __shfl_sync(0xffffffffu, j, src);
+                        if (CNT && lane == 0) cnt.nonempty++;  // SDF mode: AABB marches
+                        const float4 L = __ldg(&P.sdf_box[2 * jm]), H = __ldg(&P.sdf_box[2 * jm + 1]);
+                        float t;
+                        if (!sdf_march<CNT>(P, o, d, L, H, t, cnt)) continue;
+                        if (!(t < best_t || (t == best_t && (int)jm < best))) continue;
+                        if (has_lam && sdf_excluded<CNT>(P, o, l0, l1, L, H, cnt)) continue;
+                        best_t = t;
+                        best = (int)jm;
+                    }
+                }
+                first = false;
+                t_lo = t_out;
+            } else {
+                D = (int)rg.x;
+            }
+            if (best_t < t_out - P.sdf_stop) break;
+            // grid move: DDA step, or a Chebyshev jump across the empty box (as k_trace)
+            if (D <= 1) {
+                const int ax = (tm[0] <= tm[1] && tm[0] <= tm[2]) ? 0 : (tm[1] <= tm[2] ? 1 : 2);
+                const float dva = ax == 0 ? dv[0] : (ax == 1 ? dv[1] : dv[2]);
+                int ca = (ax == 0 ? c[0] : (ax == 1 ? c[1] : c[2])) + (dva > 0.0f ? 1 : -1);
+                const int na = ax == 0 ? P.sg_n[0] : (ax == 1 ? P.sg_n[1] : P.sg_n[2]);
+                if (ca < 0 || ca >= na) break;
+                const float oa = ax == 0 ? ov[0] : (ax == 1 ? ov[1] : ov[2]);
+                const float ia = ax == 0 ? inv[0] : (ax == 1 ? inv[1] : inv[2]);
+                const float ga = ax == 0 ? P.sg_o[0] : (ax == 1 ? P.sg_o[1] : P.sg_o[2]);
+                const float tn = ((ga + (float)(ca + (dva > 0.0f)) * P.sdf_a) - oa) * ia;
+                if (ax == 0) { c[0] = ca; tm[0] = tn; }
+                else if (ax == 1) { c[1] = ca; tm[1] = tn; }
+                else { c[2] = ca; tm[2] = tn; }
+            } else {
+                const int r = D - 1;
+                float T = INFINITY;
+                int ax = 0;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const int fk = dv[k] > 0.0f ? c[k] + r + 1 : c[k] - r;
+                    const float Tk = dv[k] != 0.0f ? ((P.sg_o[k] + (float)fk * P.sdf_a) - ov[k]) * inv[k] : INFINITY;
+                    if (Tk < T) {
+                        T = Tk;
+                        ax = k;
+                    }
+                }
+                int nc[3];
+                bool out = false;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const float pk = ov[k] + T * dv[k];
+                    nc[k] = min(c[k] + r, max(c[k] - r, (int)floorf((pk - P.sg_o[k]) * P.sdf_inv_a)));
+                    if (k == ax) nc[k] = dv[k] > 0.0f ? c[k] + r + 1 : c[k] - r - 1;
+                    out |= nc[k] < 0 || nc[k] >= P.sg_n[k];
+                }
+                if (out) break;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    c[k] = nc[k];
+                    tm[k] = dv[k] != 0.0f
+                                ? ((P.sg_o[k] + (float)(c[k] + (dv[k] > 0.0f)) * P.sdf_a) - ov[k]) * inv[k]
+                                : INFINITY;
+                }
+            }
+        }
+    }
+    best_t_out = best_t;
+    return best;
+}
+
+// R44 (warp-cooperative): the unit MLS normal at the hit (zero if undefined, cell bits in .w)
+// and the AABB's point nearest to the hit point (its id)
+template <bool CNT>
+__device__ __forceinline__ void sdf_hit_attr(const TP& P, const int best, const float best_t, const float3 o,
+                                             const float3 d, float4& hn_out, int& pid_out, Cnt& cnt) {
+    const unsigned lane = threadIdx.x & 31;
+    int pid = -1;
+    float4 hn = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(~0u));
+    if (best >= 0) {
+        // R44: normal nbar(x*)/|nbar(x*)|; record point = the AABB's point nearest x*
+        const float4 L = __ldg(&P.sdf_box[2 * best]), H = __ldg(&P.sdf_box[2 * best + 1]);
+        const unsigned k0 = __float_as_uint(L.w), k1 = __float_as_uint(H.w);
+        const float x0 = o.x + best_t * d.x, x1 = o.y + best_t * d.y, x2 = o.z + best_t * d.z;
+        float f, nb0, nb1, nb2;
+        if (sdf_eval<CNT>(P, k0, k1, x0, x1, x2, f, nb0, nb1, nb2, cnt)) {
+            const float l = sqrtf((nb0 * nb0 + nb1 * nb1) + nb2 * nb2);
+            if (l > 0.0f) {
+                hn.x = nb0 / l;
+                hn.y = nb1 / l;
+                hn.z = nb2 / l;
+            }
+        }
+        // warp argmin of (q, k): per lane ascending k with strict <, then lexicographic
+        float bq = INFINITY;
+        unsigned bk = 0xffffffffu;
+        for (unsigned k = k0 + lane; k < k1; k += 32) {
+            const float4 A = __ldg(&P.sdf_pts[2 * k]);
+            const float e0 = A.x - x0, e1 = A.y - x1, e2 = A.z - x2;
+            const float q = (e0 * e0 + e1 * e1) + e2 * e2;
+            if (q < bq) {
+                bq = q;
+                bk = k;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float oq = __shfl_xor_sync(0xffffffffu, bq, off);
+            const unsigned ok = __shfl_xor_sync(0xffffffffu, bk, off);
+            if (oq < bq || (oq == bq && ok < bk)) {
+                bq = oq;
+                bk = ok;
+            }
+        }
+        pid = __float_as_int(__ldg(&P.sdf_pts[2 * bk + 1]).w);
+        hn.w = __uint_as_float(__ldg(&P.sdf_acell[best]));
+    }
+    hn_out = hn;
+    pid_out = pid;
+}
+
 template <bool CNT>
 __global__ void __launch_bounds__(128, NRT_SDF_MINB) k_trace_sdf(TP P, Wave W, int b) {
     const unsigned long long n = W.n_alive[b];
@@ -979,170 +1208,345 @@ __global__ void __launch_bounds__(128, NRT_SDF_MINB) k_trace_sdf(TP P, Wave W, i
         const float4 o4 = W.o[ray], d4 = W.d[ray], a4 = W.l0[ray], c4 = W.l1[ray];
         const float3 o = make_float3(o4.x, o4.y, o4.z), d = make_float3(d4.x, d4.y, d4.z);
         const float3 l0 = make_float3(a4.x, a4.y, a4.z), l1 = make_float3(c4.x, c4.y, c4.z);
-        const bool has_lam = l0.x != 0.0f || l0.y != 0.0f || l0.z != 0.0f || l1.x != 0.0f || l1.y != 0.0f ||
-                             l1.z != 0.0f;
         const unsigned prev = __float_as_uint(o4.w);  // cell of the previous hit (~0: none)
-        float best_t = INFINITY;
-        int best = -1;
-        // grid entry (uniform across the warp)
-        const float ov[3] = {o.x, o.y, o.z}, dv[3] = {d.x, d.y, d.z};
-        float inv[3], t0 = 0.0f, t1 = INFINITY;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            inv[k] = rcp_approx(dv[k]);  // walk only (§6.4)
-            const float lo = P.sg_o[k], hi = P.sg_o[k] + (float)P.sg_n[k] * P.sdf_a;
-            if (dv[k] != 0.0f) {
-                const float ta = (lo - ov[k]) * inv[k], tb = (hi - ov[k]) * inv[k];
-                t0 = fmaxf(t0, fminf(ta, tb));
-                t1 = fminf(t1, fmaxf(ta, tb));
-            } else if (ov[k] < lo || ov[k] > hi) {
-                t1 = -1.0f;
-            }
-        }
-        if (t0 <= t1) {
-            int c[3];
-            float tm[3];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const float p = ov[k] + t0 * dv[k];
-                c[k] = min(P.sg_n[k] - 1, max(0, (int)floorf((p - P.sg_o[k]) * P.sdf_inv_a)));
-                tm[k] = dv[k] != 0.0f ? ((P.sg_o[k] + (float)(c[k] + (dv[k] > 0.0f)) * P.sdf_a) - ov[k]) * inv[k]
-                                      : INFINITY;
-            }
-            float t_lo = t0;
-            bool first = true;
-            for (;;) {
-                const float t_out = fminf(tm[0], fminf(tm[1], tm[2]));
-                const uint2 rg = __ldg(&P.sdf_gcell[c[0] + P.sg_n[0] * (c[1] + P.sg_n[1] * c[2])]);
-                if (CNT && lane == 0) cnt.cells++;
-                int D = 1;
-                if (rg.y > rg.x) {
-                    for (unsigned base = rg.x; base < rg.y; base += 32) {
-                        // lanes: slab test + owner rule of one registered AABB each
-                        const unsigned q = base + lane;
-                        unsigned j = 0;
-                        bool cand = false;
-                        if (q < rg.y) {
-                            j = __ldg(&P.sdf_aref[q]);
-                            if (__ldg(&P.sdf_acell[j]) != prev) {
-                                const float tn = sdf_slab(o, d, __ldg(&P.sdf_box[2 * j]), __ldg(&P.sdf_box[2 * j + 1]));
-                                cand = tn >= 0.0f && (first || !(tn < t_lo)) && tn < t_out;  // owner cell only
-                            }
-                        }
-                        unsigned m = __ballot_sync(0xffffffffu, cand);
-                        while (m) {  // warp: march the candidates
-                            const int src = __ffs(m) - 1;
-                            m &= m - 1;
-                            const unsigned jm = __shfl_sync(0xffffffffu, j, src);
-                            if (CNT && lane == 0) cnt.nonempty++;  // SDF mode: AABB marches
-                            const float4 L = __ldg(&P.sdf_box[2 * jm]), H = __ldg(&P.sdf_box[2 * jm + 1]);
-                            float t;
-                            if (!sdf_march<CNT>(P, o, d, L, H, t, cnt)) continue;
-                            if (!(t < best_t || (t == best_t && (int)jm < best))) continue;
-                            if (has_lam && sdf_excluded<CNT>(P, o, l0, l1, L, H, cnt)) continue;
-                            best_t = t;
-                            best = (int)jm;
-                        }
-                    }
-                    first = false;
-                    t_lo = t_out;
-                } else {
-                    D = (int)rg.x;
-                }
-                if (best_t < t_out - P.sdf_stop) break;
-                // grid move: DDA step, or a Chebyshev jump across the empty box (as k_trace)
-                if (D <= 1) {
-                    const int ax = (tm[0] <= tm[1] && tm[0] <= tm[2]) ? 0 : (tm[1] <= tm[2] ? 1 : 2);
-                    const float dva = ax == 0 ? dv[0] : (ax == 1 ? dv[1] : dv[2]);
-                    int ca = (ax == 0 ? c[0] : (ax == 1 ? c[1] : c[2])) + (dva > 0.0f ? 1 : -1);
-                    const int na = ax == 0 ? P.sg_n[0] : (ax == 1 ? P.sg_n[1] : P.sg_n[2]);
-                    if (ca < 0 || ca >= na) break;
-                    const float oa = ax == 0 ? ov[0] : (ax == 1 ? ov[1] : ov[2]);
-                    const float ia = ax == 0 ? inv[0] : (ax == 1 ? inv[1] : inv[2]);
-                    const float ga = ax == 0 ? P.sg_o[0] : (ax == 1 ? P.sg_o[1] : P.sg_o[2]);
-                    const float tn = ((ga + (float)(ca + (dva > 0.0f)) * P.sdf_a) - oa) * ia;
-                    if (ax == 0) { c[0] = ca; tm[0] = tn; }
-                    else if (ax == 1) { c[1] = ca; tm[1] = tn; }
-                    else { c[2] = ca; tm[2] = tn; }
-                } else {
-                    const int r = D - 1;
-                    float T = INFINITY;
-                    int ax = 0;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        const int fk = dv[k] > 0.0f ? c[k] + r + 1 : c[k] - r;
-                        const float Tk = dv[k] != 0.0f ? ((P.sg_o[k] + (float)fk * P.sdf_a) - ov[k]) * inv[k] : INFINITY;
-                        if (Tk < T) {
-                            T = Tk;
-                            ax = k;
-                        }
-                    }
-                    int nc[3];
-                    bool out = false;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        const float pk = ov[k] + T * dv[k];
-                        nc[k] = min(c[k] + r, max(c[k] - r, (int)floorf((pk - P.sg_o[k]) * P.sdf_inv_a)));
-                        if (k == ax) nc[k] = dv[k] > 0.0f ? c[k] + r + 1 : c[k] - r - 1;
-                        out |= nc[k] < 0 || nc[k] >= P.sg_n[k];
-                    }
-                    if (out) break;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        c[k] = nc[k];
-                        tm[k] = dv[k] != 0.0f
-                                    ? ((P.sg_o[k] + (float)(c[k] + (dv[k] > 0.0f)) * P.sdf_a) - ov[k]) * inv[k]
-                                    : INFINITY;
-                    }
-                }
-            }
-        }
-        int pid = -1;
-        float4 hn = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(~0u));
-        if (best >= 0) {
-            // R44: normal nbar(x*)/|nbar(x*)|; record point = the AABB's point nearest x*
-            const float4 L = __ldg(&P.sdf_box[2 * best]), H = __ldg(&P.sdf_box[2 * best + 1]);
-            const unsigned k0 = __float_as_uint(L.w), k1 = __float_as_uint(H.w);
-            const float x0 = o.x + best_t * d.x, x1 = o.y + best_t * d.y, x2 = o.z + best_t * d.z;
-            float f, nb0, nb1, nb2;
-            if (sdf_eval<CNT>(P, k0, k1, x0, x1, x2, f, nb0, nb1, nb2, cnt)) {
-                const float l = sqrtf((nb0 * nb0 + nb1 * nb1) + nb2 * nb2);
-                if (l > 0.0f) {
-                    hn.x = nb0 / l;
-                    hn.y = nb1 / l;
-                    hn.z = nb2 / l;
-                }
-            }
-            // warp argmin of (q, k): per lane ascending k with strict <, then lexicographic
-            float bq = INFINITY;
-            unsigned bk = 0xffffffffu;
-            for (unsigned k = k0 + lane; k < k1; k += 32) {
-                const float4 A = __ldg(&P.sdf_pts[2 * k]);
-                const float e0 = A.x - x0, e1 = A.y - x1, e2 = A.z - x2;
-                const float q = (e0 * e0 + e1 * e1) + e2 * e2;
-                if (q < bq) {
-                    bq = q;
-                    bk = k;
-                }
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const float oq = __shfl_xor_sync(0xffffffffu, bq, off);
-                const unsigned ok = __shfl_xor_sync(0xffffffffu, bk, off);
-                if (oq < bq || (oq == bq && ok < bk)) {
-                    bq = oq;
-                    bk = ok;
-                }
-            }
-            pid = __float_as_int(__ldg(&P.sdf_pts[2 * bk + 1]).w);
-            hn.w = __uint_as_float(__ldg(&P.sdf_acell[best]));
-        }
+        float best_t;
+        const int best = sdf_trace_w<CNT>(P, o, d, l0, l1, prev, best_t, cnt);
+        float4 hn;
+        int pid;
+        sdf_hit_attr<CNT>(P, best, best_t, o, d, hn, pid, cnt);
         if (lane == 0) {
             W.hit[ray] = make_float2(best >= 0 ? best_t : INFINITY, __int_as_float(pid));
             W.hitn[ray] = hn;
         }
     }
     flush_counts(P, bounces, cnt, CNT);
+}
+
+// =======================================================================================
+// NEXT-4: the paper's gradient-descent refinement (Tables I-III; DESIGN R50-R56)
+// =======================================================================================
+// One warp per coarse path; every lane computes the same scalars (uniform control flow), the
+// warp-cooperative pieces are the reprojection traces (sdf_trace_w), the hit attributes and
+// the 27-cell normals.  FP32 throughout, every operation in the oracle's order (gd.c).
+struct GdArgs {
+    const nrt_coarse_rec* in;
+    int64_t n_in;
+    int rank, world;
+    nrt_refined_rec* out;
+    unsigned long long* n_ok;   // valid records written (keep_invalid == 0)
+    unsigned long long* work;   // path counter
+    unsigned long long* terms;  // Gaussian terms (counters)
+    int keep_invalid;
+    const float* rx;
+    float tx[3];
+    int rho;
+    float alpha, beta, delta, t_d, cos_ta, margin;  // margin = 2 sigma (R56)
+};
+
+struct GdVert {  // per-warp shared state of one interaction (written identically by all lanes)
+    float x[3], n[3], u[3], v[3], w[3], a[3];
+    float len;
+    unsigned cell;
+    int pid, kind, edge;
+};
+
+__device__ __forceinline__ float gd_dot(const float* a, const float* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+
+// R54
+__device__ __forceinline__ void gd_basis(const float* n, float* u, float* v) {
+    int ax = 0;
+    if (fabsf(n[1]) < fabsf(n[ax])) ax = 1;
+    if (fabsf(n[2]) < fabsf(n[ax])) ax = 2;
+    const float a0 = ax == 0 ? 1.0f : 0.0f, a1 = ax == 1 ? 1.0f : 0.0f, a2 = ax == 2 ? 1.0f : 0.0f;
+    const float c0 = n[1] * a2 - n[2] * a1, c1 = n[2] * a0 - n[0] * a2, c2 = n[0] * a1 - n[1] * a0;
+    const float l = sqrtf((c0 * c0 + c1 * c1) + c2 * c2);
+    u[0] = c0 / l;
+    u[1] = c1 / l;
+    u[2] = c2 / l;
+    v[0] = n[1] * u[2] - n[2] * u[1];
+    v[1] = n[2] * u[0] - n[0] * u[2];
+    v[2] = n[0] * u[1] - n[1] * u[0];
+}
+
+__device__ __forceinline__ float gd_fk(const float* y, const float* P, const float* Q) {
+    const float e1[3] = {y[0] - Q[0], y[1] - Q[1], y[2] - Q[2]};
+    const float e2[3] = {y[0] - P[0], y[1] - P[1], y[2] - P[2]};
+    return sqrtf(gd_dot(e1, e1)) + sqrtf(gd_dot(e2, e2));
+}
+__device__ __forceinline__ float gd_grad(const float* x, const float* P, const float* Q, float* g) {
+    const float e1[3] = {x[0] - Q[0], x[1] - Q[1], x[2] - Q[2]};
+    const float e2[3] = {x[0] - P[0], x[1] - P[1], x[2] - P[2]};
+    const float l1 = sqrtf(gd_dot(e1, e1)), l2 = sqrtf(gd_dot(e2, e2));
+#pragma unroll
+    for (int i = 0; i < 3; ++i) g[i] = e1[i] / l1 + e2[i] / l2;
+    return l1 + l2;
+}
+
+// the SDF trace from vertex j (0 = TX) toward direction d: departure rule of vertex j (R55)
+template <bool CNT>
+__device__ __forceinline__ int gd_trace(const TP& P, const GdVert* V, int j, const float* o, const float* d,
+                                        float& t, Cnt& cnt) {
+    float3 l0 = make_float3(0.0f, 0.0f, 0.0f), l1 = l0;
+    unsigned prev = ~0u;
+    if (j > 0) {
+        const GdVert& A = V[j - 1];
+        if (A.kind == 0) {
+            l0 = l1 = make_float3(A.n[0], A.n[1], A.n[2]);
+            prev = A.cell;
+        } else {
+            const DevEdge& E = P.edges[A.edge];
+            l0 = make_float3(E.n0[0], E.n0[1], E.n0[2]);
+            l1 = make_float3(E.n1[0], E.n1[1], E.n1[2]);
+        }
+    }
+    return sdf_trace_w<CNT>(P, make_float3(o[0], o[1], o[2]), make_float3(d[0], d[1], d[2]), l0, l1, prev, t, cnt);
+}
+
+template <bool CNT>
+__global__ void __launch_bounds__(128, NRT_SDF_MINB) k_refine_gd(TP P, GdArgs A) {
+    __shared__ GdVert sv[4][NRT_MAX_INT];
+    const unsigned lane = threadIdx.x & 31;
+    GdVert* V = sv[threadIdx.x >> 5];
+    Cnt cnt;
+    const int64_t n_mine = A.n_in > A.rank ? (A.n_in - A.rank + A.world - 1) / A.world : 0;
+    for (;;) {
+        unsigned long long jq = 0;
+        if (lane == 0) jq = atomicAdd(A.work, 1ull);
+        jq = __shfl_sync(0xffffffffu, jq, 0);
+        if ((int64_t)jq >= n_mine) break;
+        const nrt_coarse_rec& c = A.in[A.rank + (int64_t)jq * A.world];
+        const int N = c.n_int;
+        const float TX[3] = {A.tx[0], A.tx[1], A.tx[2]};
+        const float RX[3] = {A.rx[3 * c.rx], A.rx[3 * c.rx + 1], A.rx[3 * c.rx + 2]};
+        int status = NRT_REF_OK;
+        // R50
+        for (int k = 0; k < N; ++k) {
+            GdVert& Vk = V[k];
+            for (int i = 0; i < 3; ++i) Vk.n[i] = Vk.u[i] = Vk.v[i] = Vk.w[i] = Vk.a[i] = 0.0f;
+            Vk.len = 0.0f;
+            Vk.x[0] = c.v[k][0];
+            Vk.x[1] = c.v[k][1];
+            Vk.x[2] = c.v[k][2];
+            if ((c.kinds >> k) & 1) {
+                const DevEdge& E = P.edges[c.prim[k]];
+                Vk.kind = 1;
+                Vk.edge = (int)c.prim[k];
+                for (int i = 0; i < 3; ++i) {
+                    Vk.w[i] = E.e[i];
+                    Vk.a[i] = E.a[i];
+                }
+                Vk.len = E.len;
+            } else {
+                Vk.kind = 0;
+                Vk.pid = (int)c.prim[k];
+                // R40 cell of the record point
+                const float4 p = __ldg(&P.sn_p[c.prim[k]]);
+                const float pp[3] = {p.x, p.y, p.z};
+                int ci[3];
+                for (int i = 0; i < 3; ++i)
+                    ci[i] = min(P.sd_n[i] - 1, max(0, (int)floorf((pp[i] - P.sd_o[i]) / P.sdf_a)));
+                Vk.cell = (unsigned)(ci[0] + P.sd_n[0] * (ci[1] + P.sd_n[1] * ci[2]));
+            }
+            __syncwarp();
+            if (Vk.kind == 0) {
+                float n0, n1, n2;
+                if (!sdf_normal27<CNT>(P, Vk.cell, Vk.x[0], Vk.x[1], Vk.x[2], n0, n1, n2, cnt)) {
+                    status = NRT_REF_NO_SUPPORT;
+                } else {
+                    Vk.n[0] = n0;
+                    Vk.n[1] = n1;
+                    Vk.n[2] = n2;
+                    gd_basis(Vk.n, Vk.u, Vk.v);
+                }
+            }
+            __syncwarp();
+        }
+        int it = 0;
+        for (; it < A.rho && status == NRT_REF_OK; ++it) {
+            for (int k = 0; k < N && status == NRT_REF_OK; ++k) {  // R51
+                GdVert& Vk = V[k];
+                float Pp[3], Qq[3], x[3];
+                for (int i = 0; i < 3; ++i) {
+                    Pp[i] = k == 0 ? TX[i] : V[k - 1].x[i];
+                    Qq[i] = k == N - 1 ? RX[i] : V[k + 1].x[i];
+                    x[i] = Vk.x[i];
+                }
+                float g[3], y[3];
+                const float f0 = gd_grad(x, Pp, Qq, g);
+                if (Vk.kind == 0) {
+                    const float gu = gd_dot(g, Vk.u), gv = gd_dot(g, Vk.v);
+                    const float slope = -(gu * gu + gv * gv);
+                    float gam = 1.0f;
+                    bool ok = false;
+                    for (int s = 0; s < 64; ++s) {
+                        const float du = -gu * gam, dv = -gv * gam;
+                        for (int i = 0; i < 3; ++i) y[i] = (x[i] + du * Vk.u[i]) + dv * Vk.v[i];
+                        if (!(gd_fk(y, Pp, Qq) > f0 + (A.alpha * gam) * slope)) {
+                            ok = true;
+                            break;
+                        }
+                        gam = A.beta * gam;
+                    }
+                    if (!ok)
+                        for (int i = 0; i < 3; ++i) y[i] = x[i];
+                    // R55: reproject by tracing from I_{k-1} toward y
+                    float d[3] = {y[0] - Pp[0], y[1] - Pp[1], y[2] - Pp[2]};
+                    const float ld = sqrtf(gd_dot(d, d));
+                    for (int i = 0; i < 3; ++i) d[i] = d[i] / ld;
+                    float t;
+                    const int best = gd_trace<CNT>(P, V, k, Pp, d, t, cnt);
+                    if (best < 0) {
+                        status = NRT_REF_NO_SUPPORT;
+                        break;
+                    }
+                    float4 hn;
+                    int pid;
+                    sdf_hit_attr<CNT>(P, best, t, make_float3(Pp[0], Pp[1], Pp[2]), make_float3(d[0], d[1], d[2]),
+                                      hn, pid, cnt);
+                    const float xn[3] = {Pp[0] + t * d[0], Pp[1] + t * d[1], Pp[2] + t * d[2]};
+                    const unsigned cell = __ldg(&P.sdf_acell[best]);
+                    float nn[3];
+                    float nu[3] = {Vk.n[0], Vk.n[1], Vk.n[2]}, uu[3] = {Vk.u[0], Vk.u[1], Vk.u[2]},
+                          vv[3] = {Vk.v[0], Vk.v[1], Vk.v[2]};
+                    if (sdf_normal27<CNT>(P, cell, xn[0], xn[1], xn[2], nn[0], nn[1], nn[2], cnt)) {
+                        const float dx[3] = {xn[0] - x[0], xn[1] - x[1], xn[2] - x[2]};
+                        const float dist = fabsf(gd_dot(dx, nu));
+                        const float ca = gd_dot(nu, nn);
+                        if (!(dist < A.t_d && ca > A.cos_ta)) {
+                            for (int i = 0; i < 3; ++i) nu[i] = nn[i];
+                            gd_basis(nu, uu, vv);
+                        }
+                    }
+                    __syncwarp();
+                    for (int i = 0; i < 3; ++i) {
+                        Vk.x[i] = xn[i];
+                        Vk.n[i] = nu[i];
+                        Vk.u[i] = uu[i];
+                        Vk.v[i] = vv[i];
+                    }
+                    Vk.cell = cell;
+                    Vk.pid = pid;
+                    __syncwarp();
+                } else {
+                    const float gw = gd_dot(g, Vk.w);
+                    const float slope = -(gw * gw);
+                    float gam = 1.0f;
+                    bool ok = false;
+                    for (int s = 0; s < 64; ++s) {
+                        const float dw = -gw * gam;
+                        for (int i = 0; i < 3; ++i) y[i] = x[i] + dw * Vk.w[i];
+                        if (!(gd_fk(y, Pp, Qq) > f0 + (A.alpha * gam) * slope)) {
+                            ok = true;
+                            break;
+                        }
+                        gam = A.beta * gam;
+                    }
+                    if (!ok)
+                        for (int i = 0; i < 3; ++i) y[i] = x[i];
+                    const float ya[3] = {y[0] - Vk.a[0], y[1] - Vk.a[1], y[2] - Vk.a[2]};
+                    const float s = gd_dot(ya, Vk.w);
+                    if (!(s >= 0.0f && s <= Vk.len)) {  // R52
+                        status = NRT_REF_OFF_EDGE;
+                        break;
+                    }
+                    __syncwarp();
+                    for (int i = 0; i < 3; ++i) Vk.x[i] = y[i];
+                    __syncwarp();
+                }
+            }
+        }
+        // R56
+        float gs = 0.0f;
+        for (int k = 0; k < N; ++k) {
+            float Pp[3], Qq[3], g[3];
+            for (int i = 0; i < 3; ++i) {
+                Pp[i] = k == 0 ? TX[i] : V[k - 1].x[i];
+                Qq[i] = k == N - 1 ? RX[i] : V[k + 1].x[i];
+            }
+            gd_grad(V[k].x, Pp, Qq, g);
+            if (V[k].kind == 0) {
+                const float gu = gd_dot(g, V[k].u), gv = gd_dot(g, V[k].v);
+                gs = gs + (gu * gu + gv * gv);
+            } else {
+                const float gw = gd_dot(g, V[k].w);
+                gs = gs + gw * gw;
+            }
+        }
+        if (status == NRT_REF_OK && !(gs < A.delta)) status = NRT_REF_NO_CONVERGE;
+        for (int j = 0; j <= N && status == NRT_REF_OK; ++j) {
+            const float* o = j == 0 ? TX : V[j - 1].x;
+            const float* to = j == N ? RX : V[j].x;
+            float d[3] = {to[0] - o[0], to[1] - o[1], to[2] - o[2]};
+            const float L = sqrtf(gd_dot(d, d));
+            for (int i = 0; i < 3; ++i) d[i] = d[i] / L;
+            float t;
+            float oo[3] = {o[0], o[1], o[2]};
+            if (gd_trace<CNT>(P, V, j, oo, d, t, cnt) >= 0 && t < L - A.margin) status = NRT_REF_OCCLUDED;
+        }
+        // output (FP64 from the FP32 points, as the oracle)
+        if (lane == 0 && (A.keep_invalid || status == NRT_REF_OK)) {
+            nrt_refined_rec r;
+            memset(&r, 0, sizeof(r));
+            r.rx = c.rx;
+            r.n_int = c.n_int;
+            r.n_diff = c.n_diff;
+            r.kinds = c.kinds;
+            r.ray_id = c.ray_id;
+            r.status = status;
+            r.iters = it;
+            r.gradsq = (double)gs;
+            double I[NRT_MAX_INT + 2][3];
+            for (int i = 0; i < 3; ++i) {
+                I[0][i] = TX[i];
+                I[N + 1][i] = RX[i];
+            }
+            for (int k = 0; k < N; ++k) {
+                for (int i = 0; i < 3; ++i) {
+                    I[k + 1][i] = V[k].x[i];
+                    r.v[k][i] = V[k].x[i];
+                }
+                if (V[k].kind == 0) {
+                    r.prim[k] = (uint32_t)V[k].pid;
+                    r.label[k] = __ldg(&P.label[V[k].pid]);
+                } else {
+                    r.prim[k] = c.prim[k];
+                    r.label[k] = c.label[k];
+                }
+            }
+            double L = 0.0;
+            for (int j = 0; j <= N; ++j) {
+                const double s0 = I[j + 1][0] - I[j][0], s1 = I[j + 1][1] - I[j][1], s2 = I[j + 1][2] - I[j][2];
+                L += sqrt(s0 * s0 + s1 * s1 + s2 * s2);
+            }
+            r.L = L;
+            r.delay = L / 299792458.0;
+            const double d0[3] = {I[1][0] - I[0][0], I[1][1] - I[0][1], I[1][2] - I[0][2]};
+            const double l0 = sqrt(d0[0] * d0[0] + d0[1] * d0[1] + d0[2] * d0[2]);
+            const double dl[3] = {I[N][0] - I[N + 1][0], I[N][1] - I[N + 1][1], I[N][2] - I[N + 1][2]};
+            const double ll = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+            const double R2D = 180.0 / 3.14159265358979323846;
+            r.aod_az = (float)(atan2(d0[1], d0[0]) * R2D);
+            r.aod_el = (float)(asin(fmax(-1.0, fmin(1.0, d0[2] / l0))) * R2D);
+            r.aoa_az = (float)(atan2(dl[1], dl[0]) * R2D);
+            r.aoa_el = (float)(asin(fmax(-1.0, fmin(1.0, dl[2] / ll))) * R2D);
+            for (int k = 0; k < N; ++k) {
+                const double din[3] = {I[k + 1][0] - I[k][0], I[k + 1][1] - I[k][1], I[k + 1][2] - I[k][2]};
+                const double l = sqrt(din[0] * din[0] + din[1] * din[1] + din[2] * din[2]);
+                const float* ax = V[k].kind == 0 ? V[k].n : V[k].w;
+                double c2 = (din[0] * ax[0] + din[1] * ax[1] + din[2] * ax[2]) / l;
+                if (V[k].kind == 0) c2 = fabs(c2);
+                r.inc[k] = (float)(acos(fmax(-1.0, fmin(1.0, c2))) * R2D);
+            }
+            const unsigned long long at = A.keep_invalid ? jq : atomicAdd(A.n_ok, 1ull);
+            A.out[at] = r;
+        }
+        __syncwarp();
+    }
+    if (CNT && A.terms) {
+        unsigned long long t = cnt.tests;
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_down_sync(0xffffffffu, t, off);
+        if (lane == 0 && t) atomicAdd(A.terms, t);
+    }
 }
 
 // live-list entries [n_alive, cap) get the largest key, so a sort of all cap entries puts the
@@ -1443,10 +1847,14 @@ TP make_tp(nrt_scene s, const LaunchArgs& a) {
         P.sdf_acell = s->sdf_acell;
         P.sdf_gcell = s->sdf_gcell;
         P.sdf_aref = s->sdf_aref;
+        P.sdf_crange = s->sdf_crange;
         for (int k = 0; k < 3; ++k) {
             P.sg_o[k] = s->sdf_gorg[k];
             P.sg_n[k] = s->sdf_gdims[k];
+            P.sd_n[k] = s->sdf_dims[k];
+            P.sd_o[k] = s->sdf_org[k];
         }
+        P.sn_p = s->sp;
         P.sdf_a = s->sdf_a;
         P.sdf_inv_a = 1.0f / s->sdf_a;
         P.sdf_half = 0.5f * (s->sdf_a * 1.7320508f);
@@ -1454,6 +1862,7 @@ TP make_tp(nrt_scene s, const LaunchArgs& a) {
         P.sdf_rs = a.desc.sdf_r_s;
         P.sdf_tsdf = a.desc.sdf_t_sdf;
         const float sigma = a.desc.sdf_xi * a.desc.sdf_r_s;
+        P.sdf_sigma = sigma;
         P.sdf_inv = 1.0f / (2.0f * sigma * sigma);
     }
     return P;
@@ -1919,6 +2328,118 @@ nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev
     *raw_out = raw;
     *n_raw = (int64_t)hc.raw_n;
     *bounces = hc.bounces;
+    return NRT_OK;
+}
+
+// NEXT-4 host side: one warp per path of the shard j == rank (mod world); valid paths (or all,
+// keep_invalid) -> R28 shortest per key, as the Gauss-Newton refinement's output
+nrt_status refine_gd(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out, cudaStream_t st) {
+    const int64_t n = coarse->n;
+    out->n = 0;
+    TP P{};
+    P.label = s->label;
+    P.edges = s->edges;
+    P.n_edges = s->n_edges;
+    P.sdf = 1;
+    P.sdf_pts = s->sdf_pts;
+    P.sdf_box = s->sdf_box;
+    P.sdf_acell = s->sdf_acell;
+    P.sdf_gcell = s->sdf_gcell;
+    P.sdf_aref = s->sdf_aref;
+    P.sdf_crange = s->sdf_crange;
+    P.sn_p = s->sp;
+    for (int k = 0; k < 3; ++k) {
+        P.sg_o[k] = s->sdf_gorg[k];
+        P.sg_n[k] = s->sdf_gdims[k];
+        P.sd_n[k] = s->sdf_dims[k];
+        P.sd_o[k] = s->sdf_org[k];
+    }
+    P.sdf_a = s->sdf_a;
+    P.sdf_inv_a = 1.0f / s->sdf_a;
+    P.sdf_half = 0.5f * (s->sdf_a * 1.7320508f);
+    P.sdf_stop = 2.0f * P.sdf_half + s->sdf_pad;
+    // FP32 parameters as the definition forms them (R50-R56)
+    P.sdf_rs = (float)d->r_s;
+    P.sdf_tsdf = (float)d->gd_t_sdf;
+    const float sigma = (float)d->xi * (float)d->r_s;
+    P.sdf_sigma = sigma;
+    P.sdf_inv = 1.0f / (2.0f * sigma * sigma);
+    P.tau = (float)d->tau;
+    P.cos_ex = cos_ex_of((float)d->theta_ex_deg);
+    GdArgs A{};
+    A.in = (const nrt_coarse_rec*)coarse->d_rec;
+    A.n_in = n;
+    A.rank = d->rank;
+    A.world = d->world;
+    A.keep_invalid = d->keep_invalid;
+    for (int k = 0; k < 3; ++k) A.tx[k] = coarse->tx[k];
+    A.rho = d->gd_rho;
+    A.alpha = (float)d->alpha;
+    A.beta = (float)d->beta;
+    A.delta = (float)d->delta;
+    A.t_d = (float)d->gd_t_d;
+    A.cos_ta = cos_ex_of((float)d->gd_t_a_deg);
+    A.margin = 2.0f * sigma;
+    const int64_t n_mine = n > d->rank ? (n - d->rank + d->world - 1) / d->world : 0;
+    float* d_rx = nullptr;
+    const size_t nrx = coarse->rx.size();
+    NRT_CUDA(cudaMallocAsync(&d_rx, (nrx ? nrx : 3) * sizeof(float), st));
+    if (nrx) NRT_CUDA(cudaMemcpyAsync(d_rx, coarse->rx.data(), nrx * sizeof(float), cudaMemcpyHostToDevice, st));
+    A.rx = d_rx;
+    nrt_refined_rec* o = nullptr;
+    NRT_CUDA(cudaMallocAsync(&o, (size_t)(n_mine > 0 ? n_mine : 1) * sizeof(nrt_refined_rec), st));
+    unsigned long long* ctr = nullptr;
+    NRT_CUDA(cudaMallocAsync(&ctr, 3 * sizeof(unsigned long long), st));
+    NRT_CUDA(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), st));
+    A.out = o;
+    A.n_ok = ctr;
+    A.work = ctr + 1;
+    A.terms = d->counters ? ctr + 2 : nullptr;
+    const int dev = s->device;
+    int per_sm = 0;
+    if (d->counters) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_gd<true>, 128, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_gd<false>, 128, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = (int64_t)sm_count(dev) * per_sm;
+    if (blocks > (n_mine + 3) / 4) blocks = (n_mine + 3) / 4;
+    if (blocks < 1) blocks = 1;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    if (n_mine > 0) {
+        if (d->counters) k_refine_gd<true><<<(unsigned)blocks, 128, 0, st>>>(P, A);
+        else k_refine_gd<false><<<(unsigned)blocks, 128, 0, st>>>(P, A);
+        ::nrt::count_launch();
+    }
+    cudaEventRecord(e1, st);
+    NRT_CUDA(cudaGetLastError());
+    unsigned long long hctr[3] = {0, 0, 0};
+    NRT_CUDA(cudaMemcpyAsync(hctr, ctr, sizeof(hctr), cudaMemcpyDeviceToHost, st));
+    NRT_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    out->info.ms_refine = ms;
+    out->info.mls_value = hctr[2];  // Gaussian terms of the SDF evaluations (counters)
+    cudaFreeAsync(d_rx, st);
+    cudaFreeAsync(ctr, st);
+    if (d->keep_invalid) {
+        out->d_rec = o;
+        out->n = n_mine;
+    } else {
+        nrt_refined_rec* u = nullptr;
+        NRT_CUDA(cudaMallocAsync(&u, (size_t)(hctr[0] > 0 ? hctr[0] : 1) * sizeof(nrt_refined_rec), st));
+        int64_t m = 0;
+        NRT_TRY(dedupe_refined(o, (int64_t)hctr[0], u, &m, st));
+        cudaFreeAsync(o, st);
+        out->d_rec = u;
+        out->n = m;
+    }
+    NRT_CUDA(cudaStreamSynchronize(st));
+    out->info.n = out->n;
+    out->info.n_raw = n_mine;
     return NRT_OK;
 }
 

@@ -303,6 +303,12 @@ __global__ void k_sdf_boxes(const unsigned* cells, const unsigned* off, int64_t 
     box[2 * j] = make_float4(lo[0], lo[1], lo[2], __uint_as_float(k0));
     box[2 * j + 1] = make_float4(hi[0], hi[1], hi[2], __uint_as_float(k1));
 }
+// cell -> point range of its AABB (NEXT-4 neighbourhood normals)
+__global__ void k_sdf_crange(const unsigned* cells, const float4* box, int64_t na, uint2* crange) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= na) return;
+    crange[cells[j]] = make_uint2(__float_as_uint(box[2 * j].w), __float_as_uint(box[2 * j + 1].w));
+}
 // traversal grid: the cells the padded AABB overlaps
 struct SdfGrid {
     float ox, oy, oz, inv_a, pad;
@@ -474,6 +480,13 @@ static nrt_status sdf_build(nrt_scene S, float a, const float bmin[3], const flo
     ::nrt::count_launch();
     NRT_CUDA(cudaGetLastError());
     S->sdf_acell = cells;  // [na] cell of each AABB (the tail past na is unused)
+    {
+        const int64_t nc = (int64_t)dims[0] * dims[1] * dims[2];
+        NRT_TRY(dmalloc(&S->sdf_crange, nc, st));
+        NRT_CUDA(cudaMemsetAsync(S->sdf_crange, 0, nc * sizeof(uint2), st));
+        k_sdf_crange<<<ab, 256, 0, st>>>(cells, S->sdf_box, na, S->sdf_crange);
+        ::nrt::count_launch();
+    }
     cudaFreeAsync(k0, st);
     cudaFreeAsync(k1, st);
     cudaFreeAsync(v0, st);
