@@ -154,8 +154,11 @@ class Runner:
         self.rx = t(case.rx.reshape(-1, 3))
         self.n_rays = case.n_rays * (world if scaling == "weak" else 1)
         self.desc = N.case_desc(case)  # with case.sdf: intersect = 1 and the SDF parameters
-        self.sdf_cell = float(case.sdf["cell"]) if getattr(case, "sdf", None) else 0.0
+        self.sdf_cell = (float(case.sdf["cell"]) if getattr(case, "sdf", None)
+                         else SDF["cell"] if getattr(case, "gd", None) is not None else 0.0)
         self.rdesc = dict(xi=case.xi, r_s=case.r_s, tau=case.tau, theta_ex_deg=case.theta_ex_deg)
+        if getattr(case, "gd", None) is not None:  # NEXT-4: the paper's GD refinement
+            self.rdesc = N.gd_desc(case)
 
     def step(self, counters=0):
         from paper_2403_06648_b200 import dist as D
@@ -205,7 +208,8 @@ def e2e_step(N, case, host, n_rays, world, rank, stream):
     distributed launch + refinement, D2H of the global refined set."""
     from paper_2403_06648_b200 import dist as D
     import torch
-    sdf_cell = float(case.sdf["cell"]) if getattr(case, "sdf", None) else 0.0
+    sdf_cell = (float(case.sdf["cell"]) if getattr(case, "sdf", None)
+                else SDF["cell"] if getattr(case, "gd", None) is not None else 0.0)
     sc = N.nrt_scene_build_ex(host["p"], host["n"], case.voxel, radii=host["r"],
                               labels=host["l"], edges=case.scene.edges, stream=stream,
                               sdf_cell=sdf_cell)
@@ -220,10 +224,11 @@ def e2e_step(N, case, host, n_rays, world, rank, stream):
                                          device=torch.device("cuda", torch.cuda.current_device()),
                                          stream=stream, **desc)
     b = coarse.info()["bounces"]
+    rdesc = (N.gd_desc(case) if getattr(case, "gd", None) is not None else
+             dict(xi=case.xi, r_s=case.r_s, tau=case.tau, theta_ex_deg=case.theta_ex_deg))
     ref, _ = D.refine_distributed(N, sc, coarse, case.tx, case.rx, rank, world,
                                   device=torch.device("cuda", torch.cuda.current_device()),
-                                  stream=stream, xi=case.xi, r_s=case.r_s, tau=case.tau,
-                                  theta_ex_deg=case.theta_ex_deg)
+                                  stream=stream, **rdesc)
     out = ref.export()  # D2H of the result
     for h in (ref, coarse, sc):
         h.free()
@@ -293,6 +298,10 @@ def run_config(case, world, scaling):
     hit = (" SDF intersection (NEXT-1: AABB edge %g m, r_s %g, t_sdf %g, xi %g);"
            % (case.sdf["cell"], case.sdf["r_s"], case.sdf["t_sdf"], case.sdf["xi"])
            if getattr(case, "sdf", None) else "")
+    if getattr(case, "gd", None) is not None:
+        hit += " the paper's GD refinement (NEXT-4: %s);" % ", ".join(
+            "%s %s" % kv for kv in sorted(__import__("paper_2403_06648_b200").gd_desc(case).items())
+            if kv[0] not in ("tau", "theta_ex_deg", "method"))
     return {"workload": f"{case.name}: {case.scene.name},{hit} 1 TX/{len(case.rx)} RX, "
                         f"{n_total} rays in total ({scaling} scaling over {world} GPU(s)), "
                         f"max_refl {case.max_refl}, max_diff {case.max_diff}; "
@@ -354,12 +363,17 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--intersect", default="disk", choices=["disk", "sdf"],
                     help="sdf: NEXT-1, the paper's point-set SDF intersection (secondary lines)")
+    ap.add_argument("--refine", default="gn", choices=["gn", "gd"],
+                    help="gd: NEXT-4, the paper's gradient-descent refinement (needs the AABB "
+                         "primitives: implies sdf_cell; secondary lines)")
     args = ap.parse_args()
 
     import nrt_gen as G
     case = G.case(args.config, sigma=args.sigma) if args.config.startswith("C2") else G.case(args.config)
     if args.intersect == "sdf":
         case.sdf = dict(SDF)
+    if args.refine == "gd":
+        case.gd = {"t_a_deg": 25.0} if args.config in ("C3", "C4", "C5") else {}  # Table III
     if args.impl == "reference":
         run_reference(args, case)
         return
@@ -436,6 +450,7 @@ def main():
                       "ms_per_launch": ms_trace}
     fp64 = N.nrt_probe_fp64_tflops(local)
     flops = FLOPS_VALUE * cnt["mls_value"] + FLOPS_DERIV * cnt["mls_deriv"]
+    gd = getattr(case, "gd", None) is not None
     ach_f = flops / (ms_refine / 1000.0) / 1e12 if ms_refine else 0.0
     roof_refine = {"bound": "alu", "achieved": ach_f, "peak": fp64, "unit": "TFLOP/s",
                    "frac": ach_f / fp64 if fp64 > 0 else None,
@@ -445,6 +460,16 @@ def main():
                                   "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s",
                    "flops_per_launch": flops, "ms_per_launch": ms_refine,
                    "mls_terms": [cnt["mls_value"], cnt["mls_deriv"]]}
+    if gd:
+        # NEXT-4: FP32 ALU, Gaussian terms of its SDF evaluations (counted on device)
+        fl = FLOPS_SDF_TERM * cnt["mls_value"]
+        ach = fl / (ms_refine / 1000.0) / 1e12 if ms_refine else 0.0
+        roof_refine = {"bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                       "frac": ach / FP32_PEAK_TFLOPS, "traffic": None,
+                       "kernel": "k_refine_gd (the paper's GD, one warp per path)",
+                       "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz",
+                       "flops_per_launch": fl, "gaussian_terms": cnt["mls_value"],
+                       "ms_per_launch": ms_refine}
     dominant_refine = ms_refine > ms_trace + ms_fans
     roof = roof_refine if dominant_refine else roof_trace
     post = post_timing(N, R, case) if world == 1 else None
