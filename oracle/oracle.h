@@ -244,6 +244,19 @@ int64_t or_sdf_cell_of(const or_scene* S, const or_sdf* G, int64_t id);
 int or_sdf_normal27(const or_scene* S, const or_sdf* G, int64_t cell, const float x[3], float sigma,
                     float n_out[3]);
 
+/* ---- NEXT-2 (env.c): environment-driven launch + voxel cone tracing (R60-R67) ---- */
+typedef struct or_env or_env;
+or_env* or_env_build(const or_scene* S, const float* rx, int32_t n_rx);  /* needs S->sdf */
+void or_env_free(or_env* E);
+int64_t or_env_count(const or_env* E, int64_t* n_pc);
+void or_env_ie(const or_env* E, int64_t i, float p[3], int32_t* kind, int32_t* label, int64_t* voxel);
+void or_env_grid(const or_env* E, int64_t vd[3], float* V, float* tan_c, const int32_t** march);
+void or_env_march(const float vpos[3], const float dir[3], int32_t a_dist, float out[3]);
+int or_env_cone_sphere(const float o[3], const float d[3], float tan_c, float sec_c, const float c[3], float r);
+/* transmission to IEs i == part (mod parts) + their propagation; raw records (not deduped) */
+int or_env_launch(const or_scene* S, const or_launch_params* P, const or_env* E, int32_t part, int32_t parts,
+                  or_coarse* raw, int64_t raw_cap, int64_t* n_raw, uint64_t* n_rays);
+
 /* refined-path post-processing (post.c; NEXT-3, readings R33-R36) */
 typedef struct {
     double lambda_m;       /* wavelength of the first Fresnel zone (Eq. 13) */

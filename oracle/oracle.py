@@ -13,7 +13,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SRCS = ["coarse.c", "grid.c", "sdf.c", "refine.c", "post.c", "gd.c"]
+_SRCS = ["coarse.c", "grid.c", "sdf.c", "refine.c", "post.c", "gd.c", "env.c"]
 
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
           "-Wall", "-Wno-unused-function"]
@@ -732,3 +732,94 @@ def refine_gd_par(case, coarse, procs=1, **over):
     for k, part in enumerate(parts):
         out[k::procs] = part
     return out
+
+
+# ---- NEXT-2: environment-driven launch + voxel cone tracing (env.c, readings R60-R67) -------
+def env_lib():
+    L = lib()
+    if not hasattr(L, "_env_setup"):
+        L.or_env_build.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_int32]
+        L.or_env_build.restype = C.c_void_p
+        L.or_env_free.argtypes = [C.c_void_p]
+        L.or_env_count.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+        L.or_env_count.restype = C.c_int64
+        L.or_env_ie.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_int32),
+                                C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+        L.or_env_grid.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                  C.POINTER(C.c_void_p)]
+        L.or_env_march.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+        L.or_env_cone_sphere.argtypes = [C.c_void_p, C.c_void_p, C.c_float, C.c_float, C.c_void_p,
+                                         C.c_float]
+        L.or_env_launch.argtypes = [C.POINTER(_Scene), C.POINTER(_Params), C.c_void_p, C.c_int32,
+                                    C.c_int32, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_uint64)]
+        L._env_setup = True
+    return L
+
+
+class EnvScene:
+    """The oracle scene with its SDF AABBs and the NEXT-2 IE tables for a case's RX set."""
+
+    def __init__(self, case):
+        self.sc = coarse_scene(case)
+        self.rx = _f32(case.rx, (-1, 3))
+        self.E = env_lib().or_env_build(C.byref(self.sc.c), self.rx.ctypes.data, self.rx.shape[0])
+        assert self.E
+
+    def count(self):
+        n_pc = C.c_int64()
+        n = env_lib().or_env_count(self.E, C.byref(n_pc))
+        return int(n), int(n_pc.value)
+
+    def ie(self, i):
+        p = np.zeros(3, np.float32)
+        kind, label, vox = C.c_int32(), C.c_int32(), C.c_int64()
+        env_lib().or_env_ie(self.E, int(i), p.ctypes.data, C.byref(kind), C.byref(label), C.byref(vox))
+        return p, int(kind.value), int(label.value), int(vox.value)
+
+    def grid(self):
+        vd = np.zeros(3, np.int64)
+        V, tc, mp = C.c_float(), C.c_float(), C.c_void_p()
+        env_lib().or_env_grid(self.E, vd.ctypes.data, C.byref(V), C.byref(tc), C.byref(mp))
+        nv = int(np.prod(vd))
+        march = np.ctypeslib.as_array(C.cast(mp, C.POINTER(C.c_int32)), shape=(nv,)).copy()
+        return vd, float(V.value), float(tc.value), march
+
+    def __del__(self):
+        try:
+            env_lib().or_env_free(self.E)
+        except Exception:
+            pass
+
+
+def _env_worker(args):
+    case, part, parts = args
+    es = _FORK["env"]
+    p, rxa = _params(case)
+    L = env_lib()
+    cap = 1 << 16
+    while True:
+        raw = np.zeros(cap, COARSE_DTYPE)
+        n, nr = C.c_int64(), C.c_uint64()
+        st = L.or_env_launch(C.byref(es.sc.c), C.byref(p), es.E, part, parts, raw.ctypes.data, cap,
+                             C.byref(n), C.byref(nr))
+        if st == 0:
+            return raw[: n.value].copy(), int(nr.value)
+        cap = int(n.value) + 1
+
+
+def env_launch(case, procs=1):
+    """NEXT-2 coarse set: transmission + cone tracing over forked processes (IE shards), then
+    the R17 kappa dedupe -> (records, raw count, validation rays traced)."""
+    import multiprocessing as mp
+    env_lib()
+    _FORK["env"] = EnvScene(case)
+    parts = max(1, procs)
+    if parts == 1:
+        res = [_env_worker((case, 0, 1))]
+    else:
+        with mp.get_context("fork").Pool(parts) as pool:
+            res = pool.map(_env_worker, [(case, k, parts) for k in range(parts)])
+    _FORK.pop("env", None)
+    raw = np.concatenate([r for r, _ in res]) if res else np.zeros(0, COARSE_DTYPE)
+    return dedupe(raw, case.kappa), len(raw), sum(n for _, n in res)

@@ -397,3 +397,12 @@ int or_sdf_normal27(const or_scene* S, const or_sdf* G, int64_t cell, const floa
     for (int k = 0; k < 3; ++k) n_out[k] = nb[k] / l;
     return 1;
 }
+
+/* NEXT-2 helper (env.c): the AABB grid's geometry */
+void or_sdf_geometry(const or_sdf* G, float org[3], float* a, int64_t dims[3]) {
+    for (int k = 0; k < 3; ++k) {
+        org[k] = G->org[k];
+        dims[k] = G->dims[k];
+    }
+    *a = G->a;
+}
