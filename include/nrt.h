@@ -128,6 +128,13 @@ typedef struct {
                              SDF fails; default 0.015 */
     float sdf_t_sdf;      /* NEXT-1 hit threshold |f| < t_sdf; default 0.0015 */
     float sdf_xi;         /* NEXT-1 xi; default 2 */
+    int32_t tracer;       /* 0 = Fibonacci-lattice wavefront (north_star, default); 1 = NEXT-2:
+                             the paper's environment-driven launch + voxel cone tracing (P:86-180,
+                             Alg. 1; DESIGN R60-R67): IEs on voxels of 8 sdf_cell, rays
+                             from the TX to every IE, cone rays marched with the voxels' march
+                             distances, every candidate validated by the SDF trace (needs
+                             intersect = 1); n_rays is unused; bounces = validation rays; rank /
+                             world shard the TX->IE rays */
 } nrt_launch_desc;
 void nrt_launch_desc_default(nrt_launch_desc* d);
 

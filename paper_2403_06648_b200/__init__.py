@@ -62,7 +62,7 @@ class nrt_launch_desc(C.Structure):
                 ("rank", C.c_int32), ("world", C.c_int32), ("stage", C.c_int32),
                 ("counters", C.c_int32), ("mem", C.c_int), ("stream", C.c_void_p),
                 ("intersect", C.c_int32), ("sdf_r_s", C.c_float), ("sdf_t_sdf", C.c_float),
-                ("sdf_xi", C.c_float)]
+                ("sdf_xi", C.c_float), ("tracer", C.c_int32)]
 
 
 class nrt_post_desc(C.Structure):

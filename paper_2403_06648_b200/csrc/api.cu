@@ -221,6 +221,9 @@ static nrt_status check_launch(nrt_scene s, const float* tx, const float* rx, in
         return set_error(NRT_E_STATE, "world > 1 with diffraction needs the two-stage protocol "
                                       "(stage 1 + event all-gather + nrt_launch_fans)");
     if (d.intersect < 0 || d.intersect > 1) return set_error(NRT_E_INVALID, "intersect must be 0 or 1");
+    if (d.tracer < 0 || d.tracer > 1) return set_error(NRT_E_INVALID, "tracer must be 0 or 1");
+    if (d.tracer == 1 && d.intersect != 1)
+        return set_error(NRT_E_STATE, "tracer = 1 (cone tracing) validates with the SDF: needs intersect = 1");
     if (d.intersect == 1) {
         if (!s->n_aabb)
             return set_error(NRT_E_STATE, "intersect = 1 (SDF) needs a scene built with sdf_cell > 0");
@@ -343,6 +346,7 @@ void nrt_launch_desc_default(nrt_launch_desc* d) {
     d->mem = NRT_MEM_HOST;
     d->stream = nullptr;
     d->intersect = 0;
+    d->tracer = 0;
     d->sdf_r_s = 0.015f;
     d->sdf_t_sdf = 0.0015f;
     d->sdf_xi = 2.0f;
@@ -407,6 +411,7 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
     a.max_refl = max_refl;
     a.max_diff = max_diff;
     a.desc = d;
+    a.h_rx = hrx.data();
     float r_prim = 0, r_fan = 0;
     capture_radius_bounds(s, a, &r_prim, &r_fan);
     NRT_TRY(rxgrid_build(s, hrx.data(), n_rx, r_prim, &a.rxg, st));
@@ -428,6 +433,27 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
 
     EventTimer total(st);
     PhaseLog ph(st);
+    if (d.tracer == 1) {  // NEXT-2: environment-driven launch + voxel cone tracing
+        nrt_coarse_rec* raw = nullptr;
+        int64_t n_raw = 0;
+        uint64_t rays = 0;
+        float ms = 0.0f;
+        nrt_status rc = launch_env(s, a, &raw, &n_raw, &rays, &ms, st);
+        cudaFreeAsync(d_rx, st);
+        P->info.bounces = rays;
+        P->info.ms_trace = ms;
+        P->info.n_raw = n_raw;
+        if (rc == NRT_OK) rc = finish_coarse(P, raw, n_raw, d.kappa, st);
+        cudaFreeAsync(raw, st);
+        if (rc != NRT_OK) {
+            nrt_paths_free(P);
+            return rc;
+        }
+        P->info.ms_total = total.stop();
+        pool_keep_headroom(s->device, st);
+        *out = P;
+        return NRT_OK;
+    }
     nrt_coarse_rec* raw = nullptr;
     nrt_event_rec* ev = nullptr;
     int64_t n_raw = 0, n_ev = 0;

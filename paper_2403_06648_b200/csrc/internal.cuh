@@ -159,6 +159,7 @@ struct nrt_scene_s {
     // every AABB registered (sdf_aref, AABB indices) in all cells its box padded by sdf_pad
     // overlaps; sdf_gcell = (start, end), or (D, D) for empty cells (Chebyshev skip distance).
     float sdf_a = 0, sdf_pad = 0;
+    float sdf_bmax[3] = {0, 0, 0};  // the points' maximum (NEXT-2 cone angle: the scene diagonal)
     float sdf_org[3] = {0, 0, 0}, sdf_gorg[3] = {0, 0, 0};
     int sdf_dims[3] = {0, 0, 0}, sdf_gdims[3] = {0, 0, 0};
     int64_t n_aabb = 0, n_aref = 0;
@@ -216,6 +217,7 @@ struct LaunchArgs {
     int32_t max_refl, max_diff;
     nrt_launch_desc desc;
     RxGrid rxg;
+    const float* h_rx = nullptr;  // host copy of the receivers (NEXT-2 IE tables)
 };
 // build / free the receiver grid for rx (host, n_rx x 3) around the scene grid
 nrt_status rxgrid_build(nrt_scene s, const float* rx, int32_t n_rx, float rreg, RxGrid* g,
@@ -238,6 +240,8 @@ float cos_ex_of(float theta_deg);
 float cRw_of(float c_R, int64_t n_rays);
 // refine.cu
 double probe_fp64_tflops(int device);
+nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out, int64_t* n_raw,
+                      uint64_t* rays, float* ms_kernel, cudaStream_t st);  // NEXT-2 (launch.cu)
 nrt_status refine_gd(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
                      cudaStream_t st);  // NEXT-4 (launch.cu)
 nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,

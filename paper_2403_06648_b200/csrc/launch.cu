@@ -1549,6 +1549,357 @@ __global__ void __launch_bounds__(128, NRT_SDF_MINB) k_refine_gd(TP P, GdArgs A)
     }
 }
 
+// =======================================================================================
+// NEXT-2: the paper's environment-driven launch + voxel cone tracing (P:86-95, P:145-180,
+// Alg. 1; DESIGN R60-R67).  Level-synchronous wavefront of cone rays: level 0 is the
+// transmission (one work item per IE), level k the cone rays spawned at level k-1.  One warp per
+// item; every candidate is validated by the warp SDF trace of NEXT-1.
+// =======================================================================================
+struct EHist {
+    int n, n_diff, n_refl;
+    unsigned kinds;
+    int label[NRT_MAX_INT];
+    unsigned prim[NRT_MAX_INT];
+    float v[NRT_MAX_INT][3];
+    float s_edge;
+    unsigned long long hash;
+};
+struct CRay {
+    float o[3], d[3], nf[3], nlo[3], nhi[3], lam[6];
+    int kind, n_lam;
+    unsigned prev;
+    int src;
+    float L;
+    EHist h;
+};
+struct EnvIE {
+    float p[3];
+    int kind, label, ref;
+    int sub[3];
+    float s_edge;
+};
+struct EnvArgs {
+    const EnvIE* ie;
+    int n_ie;
+    const int* pc_of_sub;
+    const int* vstart;
+    const int* vids;
+    const int* march;
+    int vd[3], sv[3], sd[3];
+    float org[3], V, S, a, tan_c, sec_c;
+    float tx[3];
+    int max_refl, max_diff;
+    float dphi_deg;
+    int rank, world;
+    // queues
+    const CRay* in;
+    unsigned long long n_in;
+    CRay* out;
+    unsigned long long out_cap;
+    unsigned long long* n_out;
+    unsigned long long* work;
+    unsigned long long* rays;  // validation traces
+    nrt_coarse_rec* raw;
+    unsigned long long raw_cap;
+    unsigned long long* raw_n;
+};
+
+__device__ __forceinline__ unsigned long long env_mix(unsigned long long h, unsigned long long v) {
+    return (h ^ v) * 1099511628211ull;
+}
+__device__ __forceinline__ float e_dot(const float* a, const float* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+
+// R62
+__device__ __forceinline__ bool env_cone_sphere(const float* o, const float* d, float tan_c, float sec_c, const float* c,
+                                                float r) {
+    const float v[3] = {c[0] - o[0], c[1] - o[1], c[2] - o[2]};
+    const float t = e_dot(v, d);
+    if (t < -r) return false;
+    const float w[3] = {v[0] - t * d[0], v[1] - t * d[1], v[2] - t * d[2]};
+    return sqrtf(e_dot(w, w)) <= t * tan_c + r * sec_c;
+}
+
+// Alg. 1
+__device__ __forceinline__ void env_march(float* vpos, const float* dir, int a_dist) {
+    float T[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float C = floorf(vpos[k]);
+        const float L = dir[k] >= 0.0f ? 1.0f : 0.0f;
+        const float su = 1.0f / fmaxf(fabsf(dir[k]), 1e-16f);
+        const float dn = fabsf(L - (vpos[k] - C));
+        T[k] = dn * su + su * (float)(a_dist - 1);
+    }
+    float st;
+    if (T[0] <= T[1] && T[0] <= T[2]) st = T[0];
+    else if (T[1] < T[0] && T[1] <= T[2]) st = T[1];
+    else st = T[2];
+    st = st + 1e-2f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) vpos[k] = vpos[k] + dir[k] * st;
+}
+
+__device__ void env_emit(const EnvArgs& A, const EHist& h, int rx, float L) {
+    const unsigned long long slot = atomicAdd(A.raw_n, 1ull);
+    if (slot >= A.raw_cap) return;
+    nrt_coarse_rec c;
+    memset(&c, 0, sizeof(c));
+    c.rx = (uint32_t)rx;
+    c.n_int = (uint8_t)h.n;
+    c.n_diff = (uint8_t)h.n_diff;
+    c.kinds = (uint16_t)h.kinds;
+    for (int k = 0; k < h.n; ++k) {
+        c.label[k] = h.label[k];
+        c.prim[k] = h.prim[k];
+        c.v[k][0] = h.v[k][0];
+        c.v[k][1] = h.v[k][1];
+        c.v[k][2] = h.v[k][2];
+    }
+    c.s_edge = h.s_edge;
+    c.L = L;
+    c.ray_id = env_mix(h.hash, (1ull << 62) | (unsigned long long)rx) & ~(1ull << 63);
+    A.raw[slot] = c;
+}
+
+__device__ __forceinline__ CRay* env_push(const EnvArgs& A) {
+    const unsigned long long slot = atomicAdd(A.n_out, 1ull);
+    return slot < A.out_cap ? &A.out[slot] : nullptr;
+}
+
+// R66 + R65 for IE i from source o (departure normals lam / n_lam, previous cell) with history
+// h and length L0 so far.  Called by the whole warp (uniform); lane 0 writes children/records.
+template <bool CNT>
+__device__ void env_try_ie(const TP& P, const EnvArgs& A, const EHist& h, const float* o, const float* lam, int n_lam,
+                           unsigned prev, int i, float L0, Cnt& cnt) {
+    const unsigned lane = threadIdx.x & 31;
+    const EnvIE I = A.ie[i];
+    const float dv[3] = {I.p[0] - o[0], I.p[1] - o[1], I.p[2] - o[2]};
+    const float Ls = sqrtf(e_dot(dv, dv));
+    if (!(Ls > 0.0f)) return;
+    const float d[3] = {dv[0] / Ls, dv[1] / Ls, dv[2] / Ls};
+    float3 l0 = make_float3(0.0f, 0.0f, 0.0f), l1 = l0;
+    if (n_lam == 1) l0 = l1 = make_float3(lam[0], lam[1], lam[2]);
+    if (n_lam == 2) {
+        l0 = make_float3(lam[0], lam[1], lam[2]);
+        l1 = make_float3(lam[3], lam[4], lam[5]);
+    }
+    if (lane == 0) atomicAdd(A.rays, 1ull);
+    float t;
+    const int best = sdf_trace_w<CNT>(P, make_float3(o[0], o[1], o[2]), make_float3(d[0], d[1], d[2]), l0, l1, prev, t, cnt);
+    if (I.kind == 2) {  // RXIE
+        if (best >= 0 && t < Ls) return;
+        if (lane == 0) env_emit(A, h, I.ref, L0 + Ls);
+        return;
+    }
+    if (I.kind == 1) {  // DEIE
+        if (best >= 0 && t < Ls - 0.5f * A.a) return;
+        if (h.n_diff >= A.max_diff || h.n >= NRT_MAX_INT) return;
+        const DevEdge& E = P.edges[I.ref];
+        const float ev[3] = {E.b_[0] - E.a[0], E.b_[1] - E.a[1], E.b_[2] - E.a[2]};
+        const float len = sqrtf(e_dot(ev, ev));
+        const float e[3] = {ev[0] / len, ev[1] / len, ev[2] / len};
+        const double ct = (double)e_dot(d, e);
+        const double st = sqrt(fmax(0.0, 1.0 - ct * ct));
+        if (st < 1e-6) return;
+        const int M0 = (int)ceil((double)E.n_exp * 180.0 / (double)A.dphi_deg);
+        int M = (int)ceil((double)M0 * st);
+        if (M < 1) M = 1;
+        const double wedge = (double)E.n_exp * 3.14159265358979311600;
+        if (lane != 0) return;
+        for (int m = 0; m < M; ++m) {
+            CRay* R = env_push(A);
+            if (!R) continue;
+            CRay r;
+            r.h = h;
+            r.h.label[r.h.n] = I.label;
+            r.h.prim[r.h.n] = (unsigned)I.ref;
+            for (int k = 0; k < 3; ++k) r.h.v[r.h.n][k] = I.p[k];
+            r.h.kinds = r.h.kinds | (1u << r.h.n);
+            r.h.n++;
+            r.h.n_diff++;
+            r.h.s_edge = I.s_edge;
+            r.h.hash = env_mix(h.hash, ((unsigned long long)i << 12) | (unsigned long long)(m + 1));
+            r.kind = 1;
+            double sp, cp, sl, cl, sh, ch;
+            nrt_sincos((((double)m + 0.5) * wedge) / (double)M, &sp, &cp);
+            nrt_sincos(((double)m * wedge) / (double)M, &sl, &cl);
+            nrt_sincos((((double)m + 1.0) * wedge) / (double)M, &sh, &ch);
+            for (int k = 0; k < 3; ++k) {
+                const double x2 = cp * (double)E.t0[k] + sp * (double)E.n0[k];
+                r.d[k] = (float)(x2 * st + (double)e[k] * ct);
+                r.nlo[k] = (float)(-sl * (double)E.t0[k] + cl * (double)E.n0[k]);
+                r.nhi[k] = (float)(sh * (double)E.t0[k] - ch * (double)E.n0[k]);
+                r.o[k] = I.p[k];
+                r.nf[k] = 0.0f;
+                r.lam[k] = E.n0[k];
+                r.lam[3 + k] = E.n1[k];
+            }
+            r.n_lam = 2;
+            r.prev = ~0u;
+            r.src = i;
+            r.L = L0 + Ls;
+            *R = r;
+        }
+        return;
+    }
+    // PCIE: the first hit must lie in one of its AABBs
+    if (best < 0) return;
+    const unsigned cell = __ldg(&P.sdf_acell[best]);
+    {
+        const int c0 = (int)(cell % (unsigned)A.sd[0]), c1 = (int)((cell / (unsigned)A.sd[0]) % (unsigned)A.sd[1]),
+                  c2 = (int)(cell / ((unsigned)A.sd[0] * (unsigned)A.sd[1]));
+        const int s = c0 / 4 + A.sv[0] * (c1 / 4 + A.sv[1] * (c2 / 4));
+        if (A.pc_of_sub[s] != i) return;
+    }
+    if (h.n_refl >= A.max_refl || h.n >= NRT_MAX_INT) return;
+    float4 hn;
+    int pid;
+    sdf_hit_attr<CNT>(P, best, t, make_float3(o[0], o[1], o[2]), make_float3(d[0], d[1], d[2]), hn, pid, cnt);
+    if (lane != 0) return;
+    CRay* R = env_push(A);
+    if (!R) return;
+    CRay r;
+    r.h = h;
+    const float x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+    r.h.label[r.h.n] = I.label;
+    r.h.prim[r.h.n] = (unsigned)pid;
+    for (int k = 0; k < 3; ++k) r.h.v[r.h.n][k] = x[k];
+    r.h.n++;
+    r.h.n_refl++;
+    r.h.hash = env_mix(h.hash, (unsigned long long)i << 12);
+    r.kind = 0;
+    const float nh[3] = {hn.x, hn.y, hn.z};
+    const float k2 = 2.0f * e_dot(d, nh);
+    const float xr[3] = {d[0] - k2 * nh[0], d[1] - k2 * nh[1], d[2] - k2 * nh[2]};
+    const float l = sqrtf(e_dot(xr, xr));
+    for (int k = 0; k < 3; ++k) r.d[k] = xr[k] / l;
+    const float sg = e_dot(r.d, nh) >= 0.0f ? 1.0f : -1.0f;
+    for (int k = 0; k < 3; ++k) {
+        r.o[k] = x[k];
+        r.nf[k] = sg * nh[k];
+        r.lam[k] = nh[k];
+        r.lam[3 + k] = 0.0f;
+        r.nlo[k] = r.nhi[k] = 0.0f;
+    }
+    r.n_lam = 1;
+    r.prev = cell;
+    r.src = i;
+    r.L = L0 + Ls;
+    *R = r;
+}
+
+// level 0: transmission from the TX to IEs i == rank (mod world)
+template <bool CNT>
+__global__ void __launch_bounds__(128, NRT_SDF_MINB) k_env_tx(TP P, EnvArgs A) {
+    const unsigned lane = threadIdx.x & 31;
+    Cnt cnt;
+    EHist h0;
+    memset(&h0, 0, sizeof(h0));
+    h0.hash = 14695981039346656037ull;
+    const int n_mine = A.n_ie > A.rank ? (A.n_ie - A.rank + A.world - 1) / A.world : 0;
+    for (;;) {
+        unsigned long long q = 0;
+        if (lane == 0) q = atomicAdd(A.work, 1ull);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if ((long long)q >= n_mine) break;
+        env_try_ie<CNT>(P, A, h0, A.tx, nullptr, 0, ~0u, A.rank + (int)q * A.world, 0.0f, cnt);
+        __syncwarp();
+    }
+}
+
+// levels >= 1: one cone ray per warp (R64)
+template <bool CNT>
+__global__ void __launch_bounds__(128, NRT_SDF_MINB) k_env_prop(TP P, EnvArgs A) {
+    __shared__ CRay sray[4];
+    __shared__ int sring[4][64];
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    CRay& R = sray[wid];
+    int* ring = sring[wid];
+    Cnt cnt;
+    for (;;) {
+        unsigned long long q = 0;
+        if (lane == 0) q = atomicAdd(A.work, 1ull);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (q >= A.n_in) break;
+        if (lane == 0) R = A.in[q];
+        ring[lane] = -1;
+        ring[lane + 32] = -1;
+        __syncwarp();
+        int head = 0, nring = 0;
+        float vpos[3];
+        for (int k = 0; k < 3; ++k) vpos[k] = (R.o[k] - A.org[k]) / A.V;
+        const float rv = A.V * 0.8660254f, rs = A.S * 0.8660254f;
+        for (int it = 0; it < (1 << 16); ++it) {
+            int c[3];
+            bool out = false;
+            for (int k = 0; k < 3; ++k) {
+                c[k] = (int)floorf(vpos[k]);
+                out |= c[k] < 0 || c[k] >= A.vd[k];
+            }
+            if (out) break;
+            const int cv = c[0] + A.vd[0] * (c[1] + A.vd[1] * c[2]);
+            const int am = __ldg(&A.march[cv]);
+            if (__ldg(&A.vstart[cv + 1]) > __ldg(&A.vstart[cv]) || am == 1) {
+                for (int dz = -1; dz <= 1; ++dz)
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            const int q3[3] = {c[0] + dx, c[1] + dy, c[2] + dz};
+                            if (q3[0] < 0 || q3[0] >= A.vd[0] || q3[1] < 0 || q3[1] >= A.vd[1] || q3[2] < 0 ||
+                                q3[2] >= A.vd[2])
+                                continue;
+                            const int qv = q3[0] + A.vd[0] * (q3[1] + A.vd[1] * q3[2]);
+                            const bool hit = (lane < (unsigned)nring && ring[lane] == qv) ||
+                                             (lane + 32 < (unsigned)nring && ring[lane + 32] == qv);
+                            if (__any_sync(0xffffffffu, hit)) continue;
+                            __syncwarp();
+                            if (lane == 0) ring[head] = qv;
+                            __syncwarp();
+                            head = (head + 1) & 63;
+                            if (nring < 64) nring++;
+                            const int u0 = __ldg(&A.vstart[qv]), u1 = __ldg(&A.vstart[qv + 1]);
+                            if (u1 == u0) continue;
+                            float cq[3];
+                            for (int k = 0; k < 3; ++k) cq[k] = A.org[k] + ((float)q3[k] + 0.5f) * A.V;
+                            if (!env_cone_sphere(R.o, R.d, A.tan_c, A.sec_c, cq, rv)) continue;
+                            for (int base = u0; base < u1; base += 32) {
+                                // lanes: the candidate tests of one IE each (ascending)
+                                const int uu = base + (int)lane;
+                                bool cand = false;
+                                int i = -1;
+                                if (uu < u1) {
+                                    i = __ldg(&A.vids[uu]);
+                                    if (i != R.src) {
+                                        const EnvIE I = A.ie[i];
+                                        if (I.kind == 2 && R.h.n <= 2) {
+                                            cand = true;
+                                        } else {
+                                            float cs[3];
+                                            for (int k = 0; k < 3; ++k) cs[k] = A.org[k] + ((float)I.sub[k] + 0.5f) * A.S;
+                                            if (env_cone_sphere(R.o, R.d, A.tan_c, A.sec_c, cs, rs)) {
+                                                const float w[3] = {I.p[0] - R.o[0], I.p[1] - R.o[1], I.p[2] - R.o[2]};
+                                                cand = R.kind == 0 ? e_dot(w, R.nf) > 0.0f
+                                                                   : (e_dot(w, R.nlo) >= 0.0f && e_dot(w, R.nhi) >= 0.0f);
+                                            }
+                                        }
+                                    }
+                                }
+                                unsigned m = __ballot_sync(0xffffffffu, cand);
+                                while (m) {
+                                    const int src = __ffs(m) - 1;
+                                    m &= m - 1;
+                                    const int ic = __shfl_sync(0xffffffffu, i, src);
+                                    env_try_ie<CNT>(P, A, R.h, R.o, R.lam, R.n_lam, R.prev, ic, R.L, cnt);
+                                    __syncwarp();
+                                }
+                            }
+                        }
+            }
+            env_march(vpos, R.d, am);
+        }
+        __syncwarp();
+    }
+}
+
 // live-list entries [n_alive, cap) get the largest key, so a sort of all cap entries puts the
 // live ones first (in key order) and needs no host-side count
 __global__ void k_pad_keys(unsigned* keys, const unsigned long long* n_alive, uint64_t cap) {
@@ -2330,6 +2681,334 @@ nrt_status launch_fans(nrt_scene s, const LaunchArgs& a, const nrt_event_rec* ev
     *bounces = hc.bounces;
     return NRT_OK;
 }
+
+// ---- NEXT-2 host side --------------------------------------------------------------------
+// PCIE formation (R60) on the device: points sorted by (subvoxel, id); one thread per PCIE
+__global__ void k_env_keys(const float4* sp, int64_t n, float ox, float oy, float oz, float a, int sd0, int sd1,
+                           int sd2, int sv0, int sv1, unsigned* keys, unsigned* vals) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 p = sp[i];
+    const int c0 = min(sd0 - 1, max(0, (int)floorf((p.x - ox) / a)));
+    const int c1 = min(sd1 - 1, max(0, (int)floorf((p.y - oy) / a)));
+    const int c2 = min(sd2 - 1, max(0, (int)floorf((p.z - oz) / a)));
+    keys[i] = (unsigned)(c0 / 4 + sv0 * (c1 / 4 + sv1 * (c2 / 4)));
+    vals[i] = (unsigned)i;
+}
+__global__ void k_env_pcie(const unsigned* subs, const unsigned* off, int64_t npc, const unsigned* ids, const float4* sp,
+                           const int32_t* label, float ox, float oy, float oz, float S, int sv0, int sv1, EnvIE* out) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= npc) return;
+    const unsigned s = subs[j];
+    const int sb[3] = {(int)(s % (unsigned)sv0), (int)((s / (unsigned)sv0) % (unsigned)sv1),
+                       (int)(s / ((unsigned)sv0 * (unsigned)sv1))};
+    const float c[3] = {ox + ((float)sb[0] + 0.5f) * S, oy + ((float)sb[1] + 0.5f) * S, oz + ((float)sb[2] + 0.5f) * S};
+    double sum[3] = {0.0, 0.0, 0.0};
+    float bq = INFINITY;
+    int lab = 0;
+    const unsigned k0 = off[j], k1 = off[j + 1];
+    for (unsigned k = k0; k < k1; ++k) {
+        const unsigned id = ids[k];
+        const float4 p = sp[id];
+        sum[0] += (double)p.x;
+        sum[1] += (double)p.y;
+        sum[2] += (double)p.z;
+        const float d[3] = {p.x - c[0], p.y - c[1], p.z - c[2]};
+        const float q = (d[0] * d[0] + d[1] * d[1]) + d[2] * d[2];
+        if (q < bq) {
+            bq = q;
+            lab = label[id];
+        }
+    }
+    EnvIE I;
+    const double cnt = (double)(k1 - k0);
+    I.p[0] = (float)(sum[0] / cnt);
+    I.p[1] = (float)(sum[1] / cnt);
+    I.p[2] = (float)(sum[2] / cnt);
+    I.kind = 0;
+    I.label = lab;
+    I.ref = (int)s;
+    I.sub[0] = sb[0];
+    I.sub[1] = sb[1];
+    I.sub[2] = sb[2];
+    I.s_edge = 0.0f;
+    out[j] = I;
+}
+
+nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out, int64_t* n_raw, uint64_t* rays,
+                      float* ms_kernel, cudaStream_t st) {
+    *raw_out = nullptr;
+    *n_raw = 0;
+    *rays = 0;
+    const TP P = make_tp(s, a);
+    const int64_t n = s->n;
+    const float A0 = s->sdf_a, V = 8.0f * A0, S = 4.0f * A0;
+    int sd[3], sv[3], vd[3];
+    for (int k = 0; k < 3; ++k) {
+        sd[k] = s->sdf_dims[k];
+        sv[k] = (sd[k] + 3) / 4;
+        vd[k] = (sd[k] + 7) / 8;
+    }
+    const int64_t nsub = (int64_t)sv[0] * sv[1] * sv[2];
+    // ---- PCIEs (device)
+    std::vector<EnvIE> ies;
+    {
+        unsigned *k0 = nullptr, *k1 = nullptr, *v0 = nullptr, *v1 = nullptr, *uniq = nullptr, *cnt = nullptr,
+                 *off = nullptr;
+        int64_t* nr = nullptr;
+        NRT_CUDA(cudaMallocAsync(&k0, n * 4, st));
+        NRT_CUDA(cudaMallocAsync(&k1, n * 4, st));
+        NRT_CUDA(cudaMallocAsync(&v0, n * 4, st));
+        NRT_CUDA(cudaMallocAsync(&v1, n * 4, st));
+        NRT_CUDA(cudaMallocAsync(&uniq, n * 4, st));
+        NRT_CUDA(cudaMallocAsync(&cnt, (n + 1) * 4, st));
+        NRT_CUDA(cudaMallocAsync(&off, (n + 1) * 4, st));
+        NRT_CUDA(cudaMallocAsync(&nr, 8, st));
+        const unsigned nb = (unsigned)((n + 255) / 256);
+        k_env_keys<<<nb, 256, 0, st>>>(s->sp, n, s->sdf_org[0], s->sdf_org[1], s->sdf_org[2], A0, sd[0], sd[1], sd[2],
+                                       sv[0], sv[1], k0, v0);
+        ::nrt::count_launch();
+        int bits = 1;
+        while (((int64_t)1 << bits) < nsub) ++bits;
+        cub::DoubleBuffer<unsigned> kb(k0, k1), vb(v0, v1);
+        size_t tb = 0;
+        void* tmp = nullptr;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, (int)n, 0, bits, st);
+        NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+        cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, (int)n, 0, bits, st);
+        cudaFreeAsync(tmp, st);
+        tb = 0;
+        cub::DeviceRunLengthEncode::Encode(nullptr, tb, kb.Current(), uniq, cnt, nr, (int64_t)n, st);
+        NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+        cub::DeviceRunLengthEncode::Encode(tmp, tb, kb.Current(), uniq, cnt, nr, (int64_t)n, st);
+        cudaFreeAsync(tmp, st);
+        int64_t npc = 0;
+        NRT_CUDA(cudaMemcpyAsync(&npc, nr, 8, cudaMemcpyDeviceToHost, st));
+        NRT_CUDA(cudaStreamSynchronize(st));
+        NRT_CUDA(cudaMemsetAsync(cnt + npc, 0, 4, st));
+        tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)(npc + 1), st);
+        NRT_CUDA(cudaMallocAsync(&tmp, tb, st));
+        cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, (int)(npc + 1), st);
+        cudaFreeAsync(tmp, st);
+        EnvIE* d_pc = nullptr;
+        NRT_CUDA(cudaMallocAsync(&d_pc, (npc > 0 ? npc : 1) * sizeof(EnvIE), st));
+        k_env_pcie<<<(unsigned)((npc + 127) / 128), 128, 0, st>>>(uniq, off, npc, vb.Current(), s->sp, s->label,
+                                                                    s->sdf_org[0], s->sdf_org[1], s->sdf_org[2], S,
+                                                                    sv[0], sv[1], d_pc);
+        ::nrt::count_launch();
+        ies.resize(npc);
+        NRT_CUDA(cudaMemcpyAsync(ies.data(), d_pc, npc * sizeof(EnvIE), cudaMemcpyDeviceToHost, st));
+        NRT_CUDA(cudaStreamSynchronize(st));
+        for (void* p : {(void*)k0, (void*)k1, (void*)v0, (void*)v1, (void*)uniq, (void*)cnt, (void*)off, (void*)nr,
+                        (void*)d_pc})
+            cudaFreeAsync(p, st);
+    }
+    const int npc = (int)ies.size();
+    std::vector<int> pc_of_sub(nsub, -1);
+    for (int j = 0; j < npc; ++j) pc_of_sub[ies[j].ref] = j;
+    // ---- DEIEs and RXIEs (host, the definition's FP32 arithmetic)
+    for (int j = 0; j < s->n_edges; ++j) {
+        const DevEdge& E = s->h_edges[j];
+        const float ev[3] = {E.b_[0] - E.a[0], E.b_[1] - E.a[1], E.b_[2] - E.a[2]};
+        const float len = sqrtf((ev[0] * ev[0] + ev[1] * ev[1]) + ev[2] * ev[2]);
+        std::vector<float> ts{0.0f};
+        for (int k = 0; k < 3; ++k) {
+            if (ev[k] == 0.0f) continue;
+            const float lo = fminf(E.a[k], E.b_[k]), hi = fmaxf(E.a[k], E.b_[k]);
+            const int64_t m0 = (int64_t)floorf((lo - s->sdf_org[k]) / S), m1 = (int64_t)floorf((hi - s->sdf_org[k]) / S) + 1;
+            for (int64_t m = m0; m <= m1 && ts.size() < 4094; ++m) {
+                const float t = ((s->sdf_org[k] + (float)m * S) - E.a[k]) / ev[k];
+                if (t > 0.0f && t < 1.0f) ts.push_back(t);
+            }
+        }
+        ts.push_back(1.0f);
+        std::sort(ts.begin(), ts.end());
+        for (size_t q = 0; q + 1 < ts.size(); ++q) {
+            if (!(ts[q + 1] > ts[q])) continue;
+            const float tm = 0.5f * (ts[q] + ts[q + 1]);
+            EnvIE I{};
+            for (int k = 0; k < 3; ++k) I.p[k] = E.a[k] + tm * ev[k];
+            I.kind = 1;
+            I.label = E.label;
+            I.ref = j;
+            I.s_edge = tm * len;
+            ies.push_back(I);
+        }
+    }
+    for (int j = 0; j < a.n_rx; ++j) {
+        EnvIE I{};
+        for (int k = 0; k < 3; ++k) I.p[k] = a.h_rx[3 * j + k];
+        I.kind = 2;
+        I.label = j;
+        I.ref = j;
+        ies.push_back(I);
+    }
+    for (size_t i = npc; i < ies.size(); ++i)
+        for (int k = 0; k < 3; ++k) {
+            int64_t c = (int64_t)floorf((ies[i].p[k] - s->sdf_org[k]) / S);
+            if (c < 0) c = 0;
+            if (c > sv[k] - 1) c = sv[k] - 1;
+            ies[i].sub[k] = (int)c;
+        }
+    const int n_ie = (int)ies.size();
+    // R61: voxel lists, march distances, cone
+    const int nv = vd[0] * vd[1] * vd[2];
+    std::vector<int> vstart(nv + 1, 0), vids(n_ie > 0 ? n_ie : 1), vox(n_ie > 0 ? n_ie : 1), march(nv);
+    for (int i = 0; i < n_ie; ++i) {
+        int v3[3];
+        for (int k = 0; k < 3; ++k) v3[k] = std::min(ies[i].sub[k] / 2, vd[k] - 1);
+        vox[i] = v3[0] + vd[0] * (v3[1] + vd[1] * v3[2]);
+        vstart[vox[i] + 1]++;
+    }
+    for (int v = 0; v < nv; ++v) vstart[v + 1] += vstart[v];
+    {
+        std::vector<int> fill(nv, 0);
+        for (int i = 0; i < n_ie; ++i) vids[vstart[vox[i]] + fill[vox[i]]++] = i;
+    }
+    std::vector<int> occ;
+    for (int u = 0; u < nv; ++u)
+        if (vstart[u + 1] > vstart[u]) occ.push_back(u);
+    for (int v = 0; v < nv; ++v) {
+        const int x = v % vd[0], y = (v / vd[0]) % vd[1], z = v / (vd[0] * vd[1]);
+        int best = 1 << 20;
+        for (int u : occ) {
+            const int ux = u % vd[0], uy = (u / vd[0]) % vd[1], uz = u / (vd[0] * vd[1]);
+            const int dd = std::max(std::abs(ux - x), std::max(std::abs(uy - y), std::abs(uz - z)));
+            best = std::min(best, dd);
+        }
+        march[v] = best < 1 ? 1 : best;
+    }
+    const float dg[3] = {s->sdf_bmax[0] - s->sdf_org[0], s->sdf_bmax[1] - s->sdf_org[1], s->sdf_bmax[2] - s->sdf_org[2]};
+    const float D = sqrtf((dg[0] * dg[0] + dg[1] * dg[1]) + dg[2] * dg[2]);
+    EnvArgs A{};
+    A.tan_c = V / D;
+    A.sec_c = sqrtf(1.0f + A.tan_c * A.tan_c);
+    for (int k = 0; k < 3; ++k) {
+        A.vd[k] = vd[k];
+        A.sv[k] = sv[k];
+        A.sd[k] = sd[k];
+        A.org[k] = s->sdf_org[k];
+        A.tx[k] = a.tx[k];
+    }
+    A.V = V;
+    A.S = S;
+    A.a = A0;
+    A.n_ie = n_ie;
+    A.max_refl = a.max_refl;
+    A.max_diff = a.max_diff;
+    A.dphi_deg = a.desc.dphi_deg;
+    A.rank = a.desc.rank;
+    A.world = a.desc.world;
+    // ---- upload
+    EnvIE* d_ie = nullptr;
+    int *d_pcs = nullptr, *d_vs = nullptr, *d_vi = nullptr, *d_m = nullptr;
+    unsigned long long* ctr = nullptr;  // [raw_n, n_out, work, rays]
+    NRT_CUDA(cudaMallocAsync(&d_ie, (n_ie > 0 ? n_ie : 1) * sizeof(EnvIE), st));
+    NRT_CUDA(cudaMallocAsync(&d_pcs, nsub * 4, st));
+    NRT_CUDA(cudaMallocAsync(&d_vs, (nv + 1) * 4, st));
+    NRT_CUDA(cudaMallocAsync(&d_vi, (n_ie > 0 ? n_ie : 1) * 4, st));
+    NRT_CUDA(cudaMallocAsync(&d_m, nv * 4, st));
+    NRT_CUDA(cudaMallocAsync(&ctr, 4 * 8, st));
+    NRT_CUDA(cudaMemcpyAsync(d_ie, ies.data(), n_ie * sizeof(EnvIE), cudaMemcpyHostToDevice, st));
+    NRT_CUDA(cudaMemcpyAsync(d_pcs, pc_of_sub.data(), nsub * 4, cudaMemcpyHostToDevice, st));
+    NRT_CUDA(cudaMemcpyAsync(d_vs, vstart.data(), (nv + 1) * 4, cudaMemcpyHostToDevice, st));
+    NRT_CUDA(cudaMemcpyAsync(d_vi, vids.data(), n_ie * 4, cudaMemcpyHostToDevice, st));
+    NRT_CUDA(cudaMemcpyAsync(d_m, march.data(), nv * 4, cudaMemcpyHostToDevice, st));
+    NRT_CUDA(cudaMemsetAsync(ctr, 0, 4 * 8, st));
+    A.ie = d_ie;
+    A.pc_of_sub = d_pcs;
+    A.vstart = d_vs;
+    A.vids = d_vi;
+    A.march = d_m;
+    A.raw_n = ctr;
+    A.n_out = ctr + 1;
+    A.work = ctr + 2;
+    A.rays = ctr + 3;
+    // ---- levels
+    unsigned long long raw_cap = 1 << 16, out_cap = 1 << 16;
+    nrt_coarse_rec* raw = nullptr;
+    NRT_CUDA(cudaMallocAsync(&raw, raw_cap * sizeof(nrt_coarse_rec), st));
+    CRay *qin = nullptr, *qout = nullptr;
+    unsigned long long n_in = 0;
+    NRT_CUDA(cudaMallocAsync(&qout, out_cap * sizeof(CRay), st));
+    const int sms = sm_count(s->device);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_env_prop<false>, 128, 0);
+    if (per_sm < 1) per_sm = 1;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float tot = 0.0f;
+    for (int level = 0; level <= NRT_MAX_INT; ++level) {
+        if (level > 0 && n_in == 0) break;
+        unsigned long long h[4];
+        NRT_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
+        NRT_CUDA(cudaStreamSynchronize(st));
+        const unsigned long long raw0 = h[0], rays0 = h[3];
+        for (int attempt = 0; attempt < 4; ++attempt) {
+            unsigned long long z[4] = {raw0, 0, 0, rays0};  // a re-run starts from the level's counts
+            NRT_CUDA(cudaMemcpyAsync(ctr, z, 4 * 8, cudaMemcpyHostToDevice, st));
+            A.raw = raw;
+            A.raw_cap = raw_cap;
+            A.out = qout;
+            A.out_cap = out_cap;
+            A.in = qin;
+            A.n_in = n_in;
+            const unsigned long long items = level == 0 ? (unsigned long long)n_ie : n_in;
+            unsigned blocks = (unsigned)std::min<unsigned long long>((unsigned long long)sms * per_sm, (items + 3) / 4);
+            if (blocks < 1) blocks = 1;
+            cudaEventRecord(e0, st);
+            if (level == 0) k_env_tx<false><<<blocks, 128, 0, st>>>(P, A);
+            else k_env_prop<false><<<blocks, 128, 0, st>>>(P, A);
+            ::nrt::count_launch();
+            cudaEventRecord(e1, st);
+            NRT_CUDA(cudaGetLastError());
+            NRT_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
+            NRT_CUDA(cudaStreamSynchronize(st));
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (h[0] <= raw_cap && h[1] <= out_cap) {
+                tot += ms;
+                break;
+            }
+            // overflow: grow and re-run this level (deterministic: the same inputs)
+            if (h[0] > raw_cap) {
+                nrt_coarse_rec* nr2 = nullptr;
+                const unsigned long long cap2 = h[0] + h[0] / 2 + 1024;
+                NRT_CUDA(cudaMallocAsync(&nr2, cap2 * sizeof(nrt_coarse_rec), st));
+                NRT_CUDA(cudaMemcpyAsync(nr2, raw, raw0 * sizeof(nrt_coarse_rec), cudaMemcpyDeviceToDevice, st));
+                cudaFreeAsync(raw, st);
+                raw = nr2;
+                raw_cap = cap2;
+            }
+            if (h[1] > out_cap) {
+                cudaFreeAsync(qout, st);
+                out_cap = h[1] + h[1] / 2 + 1024;
+                NRT_CUDA(cudaMallocAsync(&qout, out_cap * sizeof(CRay), st));
+            }
+        }
+        // the children become the next level's input
+        n_in = h[1];
+        if (qin) cudaFreeAsync(qin, st);
+        qin = qout;
+        qout = nullptr;
+        NRT_CUDA(cudaMallocAsync(&qout, out_cap * sizeof(CRay), st));
+    }
+    unsigned long long h[4];
+    NRT_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
+    NRT_CUDA(cudaStreamSynchronize(st));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (void* p : {(void*)d_ie, (void*)d_pcs, (void*)d_vs, (void*)d_vi, (void*)d_m, (void*)ctr, (void*)qin, (void*)qout})
+        if (p) cudaFreeAsync(p, st);
+    *raw_out = raw;
+    *n_raw = (int64_t)h[0];
+    *rays = h[3];
+    *ms_kernel = tot;
+    return NRT_OK;
+}
+
 
 // NEXT-4 host side: one warp per path of the shard j == rank (mod world); valid paths (or all,
 // keep_invalid) -> R28 shortest per key, as the Gauss-Newton refinement's output

@@ -425,6 +425,7 @@ static nrt_status sdf_build(nrt_scene S, float a, const float bmin[3], const flo
     S->sdf_a = a;
     for (int k = 0; k < 3; ++k) {
         S->sdf_org[k] = bmin[k];
+        S->sdf_bmax[k] = bmax[k];
         S->sdf_dims[k] = dims[k];
         S->sdf_gorg[k] = bmin[k] - a;
         S->sdf_gdims[k] = dims[k] + 2;
