@@ -154,6 +154,8 @@ class Runner:
         self.rx = t(case.rx.reshape(-1, 3))
         self.n_rays = case.n_rays * (world if scaling == "weak" else 1)
         self.desc = N.case_desc(case)  # with case.sdf: intersect = 1 and the SDF parameters
+        if getattr(case, "tracer", 0):
+            self.desc["tracer"] = 1
         self.sdf_cell = (float(case.sdf["cell"]) if getattr(case, "sdf", None)
                          else SDF["cell"] if getattr(case, "gd", None) is not None else 0.0)
         self.rdesc = dict(xi=case.xi, r_s=case.r_s, tau=case.tau, theta_ex_deg=case.theta_ex_deg)
@@ -214,6 +216,8 @@ def e2e_step(N, case, host, n_rays, world, rank, stream):
                               labels=host["l"], edges=case.scene.edges, stream=stream,
                               sdf_cell=sdf_cell)
     desc = N.case_desc(case)
+    if getattr(case, "tracer", 0):
+        desc["tracer"] = 1
     if world == 1:
         coarse = N.nrt_launch_ex(sc, case.tx, case.rx, n_rays, case.max_refl, case.max_diff,
                                  stream=stream, **desc)
@@ -293,11 +297,40 @@ def cpu_baseline(case, seconds=15.0):
                       f"coarse tracing only), {wall:.1f} s wall on {P} processes"}
 
 
+def _env_chunk(args):
+    case, part, parts = args
+    from oracle import oracle as O
+    return O._env_worker((case, part, parts))[1]
+
+
+def cpu_baseline_env(case, parts=512):
+    """NEXT-2: the oracle (env.c, tier-0 SDF validation) on this host's cores over the first P of
+    `parts` transmission shards (IE i == k mod parts): validation rays per second."""
+    import multiprocessing as mp
+    from oracle import oracle as O
+    O.env_lib()
+    P = os.cpu_count() or 1
+    O._FORK["env"] = O.EnvScene(case)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(P) as pool:
+        res = pool.map(_env_chunk, [(case, k, parts) for k in range(min(P, parts))])
+    wall = time.perf_counter() - t0
+    O._FORK.pop("env", None)
+    return {"value": sum(res) / wall, "unit": UNIT, "cores": P, "kind": "oracle",
+            "sample": f"transmission shards 0..{min(P, parts) - 1} of {parts} of {case.name} (NEXT-2 "
+                      f"oracle, tier-0 SDF validation rays and their cone-traced subtrees), {wall:.1f} s "
+                      f"wall on {P} processes"}
+
+
 def run_config(case, world, scaling):
     n_total = case.n_rays * (world if scaling == "weak" else 1)
     hit = (" SDF intersection (NEXT-1: AABB edge %g m, r_s %g, t_sdf %g, xi %g);"
            % (case.sdf["cell"], case.sdf["r_s"], case.sdf["t_sdf"], case.sdf["xi"])
            if getattr(case, "sdf", None) else "")
+    if getattr(case, "tracer", 0):
+        hit += (" the paper's environment-driven launch + voxel cone tracing (NEXT-2; value = "
+                "SDF validation rays/s, kappa %d);" % case.kappa)
     if getattr(case, "gd", None) is not None:
         hit += " the paper's GD refinement (NEXT-4: %s);" % ", ".join(
             "%s %s" % kv for kv in sorted(__import__("paper_2403_06648_b200").gd_desc(case).items())
@@ -363,6 +396,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--intersect", default="disk", choices=["disk", "sdf"],
                     help="sdf: NEXT-1, the paper's point-set SDF intersection (secondary lines)")
+    ap.add_argument("--tracer", default="fib", choices=["fib", "env"],
+                    help="env: NEXT-2, the paper's environment-driven launch + voxel cone tracing "
+                         "(implies --intersect sdf, kappa 100; secondary lines)")
     ap.add_argument("--refine", default="gn", choices=["gn", "gd"],
                     help="gd: NEXT-4, the paper's gradient-descent refinement (needs the AABB "
                          "primitives: implies sdf_cell; secondary lines)")
@@ -370,6 +406,10 @@ def main():
 
     import nrt_gen as G
     case = G.case(args.config, sigma=args.sigma) if args.config.startswith("C2") else G.case(args.config)
+    if args.tracer == "env":
+        args.intersect = "sdf"
+        case.kappa = 100  # Table I
+        case.tracer = 1
     if args.intersect == "sdf":
         case.sdf = dict(SDF)
     if args.refine == "gd":
@@ -434,7 +474,9 @@ def main():
         roof_trace = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
                       "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
                       "traffic": measured_traffic(case.name + "_sdf"),
-                      "kernel": "k_trace_sdf (primary bounces; one warp per segment)",
+                      "kernel": ("k_env_tx + k_env_prop (cone tracing; SDF validation rays, one warp per "
+                                 "ray)" if getattr(case, "tracer", 0) else
+                                 "k_trace_sdf (primary bounces; one warp per segment)"),
                       "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz",
                       "flops_per_launch": fl, "gaussian_terms": prim_only["tests"],
                       "terms_per_bounce": prim_only["tests"] / max(1, prim_only["bounces"]),
@@ -524,7 +566,7 @@ def main():
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(case)
+        line["cpu_baseline"] = cpu_baseline_env(case) if getattr(case, "tracer", 0) else cpu_baseline(case)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -30,7 +30,8 @@
  *   R66 validation: the SDF trace from the source toward the reception point (departure rule
  *       of the source): a PCIE is valid iff the first hit lies in one of its AABBs; a DEIE iff
  *       no hit before its distance - a/2 ("reduce the maximum length by a small bias");
- *       an RXIE iff no hit before its distance.
+ *       an RXIE iff no hit before its distance.  A PCIE / DEIE the interaction caps would not
+ *       let the path take is not validated (no ray is traced for it).
  *   R67 records: key as R17, L = the unfolded length, ray id = FNV-1a of the IE sequence; the
  *       kappa shortest per key (Table I: kappa = 100).
  */
@@ -351,6 +352,9 @@ static void try_ie(ectx* C, const ehist* h, const float o[3], const float* lam, 
                    int64_t i, float L0) {
     const or_env* E = C->E;
     const ie_t* I = &E->ie[i];
+    /* R66: an interaction the caps do not allow is not validated (it could not extend the path) */
+    if (I->kind == IE_PC && (h->n_refl >= C->P->max_refl || h->n >= OR_MAX_INT)) return;
+    if (I->kind == IE_DE && (h->n_diff >= C->P->max_diff || h->n >= OR_MAX_INT)) return;
     float dv[3] = {I->p[0] - o[0], I->p[1] - o[1], I->p[2] - o[2]};
     const float Ls = sqrtf(dot3(dv, dv));
     if (!(Ls > 0.0f)) return;

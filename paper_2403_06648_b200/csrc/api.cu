@@ -438,9 +438,11 @@ nrt_status nrt_launch_ex(nrt_scene s, const float tx[3], const float* rx, int32_
         int64_t n_raw = 0;
         uint64_t rays = 0;
         float ms = 0.0f;
-        nrt_status rc = launch_env(s, a, &raw, &n_raw, &rays, &ms, st);
+        uint64_t terms = 0;
+        nrt_status rc = launch_env(s, a, &raw, &n_raw, &rays, &ms, &terms, st);
         cudaFreeAsync(d_rx, st);
         P->info.bounces = rays;
+        P->info.surfel_tests = terms;  // Gaussian terms of the validation traces (counters = 1)
         P->info.ms_trace = ms;
         P->info.n_raw = n_raw;
         if (rc == NRT_OK) rc = finish_coarse(P, raw, n_raw, d.kappa, st);

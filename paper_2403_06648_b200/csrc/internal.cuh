@@ -241,7 +241,7 @@ float cRw_of(float c_R, int64_t n_rays);
 // refine.cu
 double probe_fp64_tflops(int device);
 nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out, int64_t* n_raw,
-                      uint64_t* rays, float* ms_kernel, cudaStream_t st);  // NEXT-2 (launch.cu)
+                      uint64_t* rays, float* ms_kernel, uint64_t* terms, cudaStream_t st);  // NEXT-2
 nrt_status refine_gd(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,
                      cudaStream_t st);  // NEXT-4 (launch.cu)
 nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_paths out,

@@ -1017,8 +1017,12 @@ __device__ __forceinline__ bool sdf_excluded(const TP& P, const float3 o, const 
 // l0, l1 (zero = none) and the previous hit's cell `prev` skipped; returns the AABB index (-1:
 // escape) and best_t.  Called by all 32 lanes with the same arguments.
 template <bool CNT>
+// t_max (optional, exact): the caller only needs hits with t <= t_max; the walk then also stops
+// once no AABB owned by a later cell can produce a hit before t_max (t_out - (L + pad) > t_max).
+// Every hit with t <= t_max is found exactly; a returned hit with t > t_max may not be the first.
 __device__ __forceinline__ int sdf_trace_w(const TP& P, const float3 o, const float3 d, const float3 l0,
-                                           const float3 l1, const unsigned prev, float& best_t_out, Cnt& cnt) {
+                                           const float3 l1, const unsigned prev, float& best_t_out, Cnt& cnt,
+                                           const float t_max = INFINITY) {
     const unsigned lane = threadIdx.x & 31;
     const bool has_lam = l0.x != 0.0f || l0.y != 0.0f || l0.z != 0.0f || l1.x != 0.0f || l1.y != 0.0f ||
                          l1.z != 0.0f;
@@ -1089,7 +1093,7 @@ __device__ __forceinline__ int sdf_trace_w(const TP& P, const float3 o, const fl
             } else {
                 D = (int)rg.x;
             }
-            if (best_t < t_out - P.sdf_stop) break;
+            if (best_t < t_out - P.sdf_stop || t_out - P.sdf_stop > t_max) break;
             // grid move: DDA step, or a Chebyshev jump across the empty box (as k_trace)
             if (D <= 1) {
                 const int ax = (tm[0] <= tm[1] && tm[0] <= tm[2]) ? 0 : (tm[1] <= tm[2] ? 1 : 2);
@@ -1285,7 +1289,7 @@ __device__ __forceinline__ float gd_grad(const float* x, const float* P, const f
 // the SDF trace from vertex j (0 = TX) toward direction d: departure rule of vertex j (R55)
 template <bool CNT>
 __device__ __forceinline__ int gd_trace(const TP& P, const GdVert* V, int j, const float* o, const float* d,
-                                        float& t, Cnt& cnt) {
+                                        float& t, Cnt& cnt, const float t_max = INFINITY) {
     float3 l0 = make_float3(0.0f, 0.0f, 0.0f), l1 = l0;
     unsigned prev = ~0u;
     if (j > 0) {
@@ -1299,7 +1303,8 @@ __device__ __forceinline__ int gd_trace(const TP& P, const GdVert* V, int j, con
             l1 = make_float3(E.n1[0], E.n1[1], E.n1[2]);
         }
     }
-    return sdf_trace_w<CNT>(P, make_float3(o[0], o[1], o[2]), make_float3(d[0], d[1], d[2]), l0, l1, prev, t, cnt);
+    return sdf_trace_w<CNT>(P, make_float3(o[0], o[1], o[2]), make_float3(d[0], d[1], d[2]), l0, l1, prev, t, cnt,
+                            t_max);
 }
 
 template <bool CNT>
@@ -1481,7 +1486,7 @@ __global__ void __launch_bounds__(128, NRT_SDF_MINB) k_refine_gd(TP P, GdArgs A)
             for (int i = 0; i < 3; ++i) d[i] = d[i] / L;
             float t;
             float oo[3] = {o[0], o[1], o[2]};
-            if (gd_trace<CNT>(P, V, j, oo, d, t, cnt) >= 0 && t < L - A.margin) status = NRT_REF_OCCLUDED;
+            if (gd_trace<CNT>(P, V, j, oo, d, t, cnt, L) >= 0 && t < L - A.margin) status = NRT_REF_OCCLUDED;
         }
         // output (FP64 from the FP32 points, as the oracle)
         if (lane == 0 && (A.keep_invalid || status == NRT_REF_OK)) {
@@ -1599,6 +1604,7 @@ struct EnvArgs {
     unsigned long long* n_out;
     unsigned long long* work;
     unsigned long long* rays;  // validation traces
+    unsigned long long* terms; // Gaussian terms (counters)
     nrt_coarse_rec* raw;
     unsigned long long raw_cap;
     unsigned long long* raw_n;
@@ -1673,6 +1679,9 @@ __device__ void env_try_ie(const TP& P, const EnvArgs& A, const EHist& h, const 
                            unsigned prev, int i, float L0, Cnt& cnt) {
     const unsigned lane = threadIdx.x & 31;
     const EnvIE I = A.ie[i];
+    // R66: an interaction the caps do not allow is not validated
+    if (I.kind == 0 && (h.n_refl >= A.max_refl || h.n >= NRT_MAX_INT)) return;
+    if (I.kind == 1 && (h.n_diff >= A.max_diff || h.n >= NRT_MAX_INT)) return;
     const float dv[3] = {I.p[0] - o[0], I.p[1] - o[1], I.p[2] - o[2]};
     const float Ls = sqrtf(e_dot(dv, dv));
     if (!(Ls > 0.0f)) return;
@@ -1684,8 +1693,12 @@ __device__ void env_try_ie(const TP& P, const EnvArgs& A, const EHist& h, const 
         l1 = make_float3(lam[3], lam[4], lam[5]);
     }
     if (lane == 0) atomicAdd(A.rays, 1ull);
+    // the validation only needs hits up to: the receiver / the edge point; for a PCIE the first
+    // hit, if it lies in one of its AABBs, is within Ls + S sqrt3 (subvoxel) + L (march window)
+    const float t_max = I.kind == 0 ? Ls + (A.S * 1.7320508f + 2.0f * P.sdf_stop) : Ls;
     float t;
-    const int best = sdf_trace_w<CNT>(P, make_float3(o[0], o[1], o[2]), make_float3(d[0], d[1], d[2]), l0, l1, prev, t, cnt);
+    const int best = sdf_trace_w<CNT>(P, make_float3(o[0], o[1], o[2]), make_float3(d[0], d[1], d[2]), l0, l1, prev, t,
+                                      cnt, t_max);
     if (I.kind == 2) {  // RXIE
         if (best >= 0 && t < Ls) return;
         if (lane == 0) env_emit(A, h, I.ref, L0 + Ls);
@@ -1742,8 +1755,8 @@ __device__ void env_try_ie(const TP& P, const EnvArgs& A, const EHist& h, const 
         }
         return;
     }
-    // PCIE: the first hit must lie in one of its AABBs
-    if (best < 0) return;
+    // PCIE: the first hit must lie in one of its AABBs (within t_max, see above)
+    if (best < 0 || t > t_max) return;
     const unsigned cell = __ldg(&P.sdf_acell[best]);
     {
         const int c0 = (int)(cell % (unsigned)A.sd[0]), c1 = (int)((cell / (unsigned)A.sd[0]) % (unsigned)A.sd[1]),
@@ -1805,6 +1818,7 @@ __global__ void __launch_bounds__(128, NRT_SDF_MINB) k_env_tx(TP P, EnvArgs A) {
         env_try_ie<CNT>(P, A, h0, A.tx, nullptr, 0, ~0u, A.rank + (int)q * A.world, 0.0f, cnt);
         __syncwarp();
     }
+    if (CNT && A.terms && lane == 0 && cnt.tests) atomicAdd(A.terms, cnt.tests);
 }
 
 // levels >= 1: one cone ray per warp (R64)
@@ -1898,6 +1912,7 @@ __global__ void __launch_bounds__(128, NRT_SDF_MINB) k_env_prop(TP P, EnvArgs A)
         }
         __syncwarp();
     }
+    if (CNT && A.terms && lane == 0 && cnt.tests) atomicAdd(A.terms, cnt.tests);
 }
 
 // live-list entries [n_alive, cap) get the largest key, so a sort of all cap entries puts the
@@ -2736,7 +2751,7 @@ __global__ void k_env_pcie(const unsigned* subs, const unsigned* off, int64_t np
 }
 
 nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out, int64_t* n_raw, uint64_t* rays,
-                      float* ms_kernel, cudaStream_t st) {
+                      float* ms_kernel, uint64_t* terms_out, cudaStream_t st) {
     *raw_out = nullptr;
     *n_raw = 0;
     *rays = 0;
@@ -2903,19 +2918,21 @@ nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out
     // ---- upload
     EnvIE* d_ie = nullptr;
     int *d_pcs = nullptr, *d_vs = nullptr, *d_vi = nullptr, *d_m = nullptr;
-    unsigned long long* ctr = nullptr;  // [raw_n, n_out, work, rays]
+    unsigned long long* ctr = nullptr;  // [raw_n, n_out, work, rays, terms]
     NRT_CUDA(cudaMallocAsync(&d_ie, (n_ie > 0 ? n_ie : 1) * sizeof(EnvIE), st));
     NRT_CUDA(cudaMallocAsync(&d_pcs, nsub * 4, st));
     NRT_CUDA(cudaMallocAsync(&d_vs, (nv + 1) * 4, st));
     NRT_CUDA(cudaMallocAsync(&d_vi, (n_ie > 0 ? n_ie : 1) * 4, st));
     NRT_CUDA(cudaMallocAsync(&d_m, nv * 4, st));
-    NRT_CUDA(cudaMallocAsync(&ctr, 4 * 8, st));
+    NRT_CUDA(cudaMallocAsync(&ctr, 5 * 8, st));
     NRT_CUDA(cudaMemcpyAsync(d_ie, ies.data(), n_ie * sizeof(EnvIE), cudaMemcpyHostToDevice, st));
     NRT_CUDA(cudaMemcpyAsync(d_pcs, pc_of_sub.data(), nsub * 4, cudaMemcpyHostToDevice, st));
     NRT_CUDA(cudaMemcpyAsync(d_vs, vstart.data(), (nv + 1) * 4, cudaMemcpyHostToDevice, st));
     NRT_CUDA(cudaMemcpyAsync(d_vi, vids.data(), n_ie * 4, cudaMemcpyHostToDevice, st));
     NRT_CUDA(cudaMemcpyAsync(d_m, march.data(), nv * 4, cudaMemcpyHostToDevice, st));
-    NRT_CUDA(cudaMemsetAsync(ctr, 0, 4 * 8, st));
+    NRT_CUDA(cudaMemsetAsync(ctr, 0, 5 * 8, st));
+    const bool counters = a.desc.counters != 0;
+    A.terms = counters ? ctr + 4 : nullptr;
     A.ie = d_ie;
     A.pc_of_sub = d_pcs;
     A.vstart = d_vs;
@@ -2945,10 +2962,13 @@ nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out
         unsigned long long h[4];
         NRT_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
         NRT_CUDA(cudaStreamSynchronize(st));
-        const unsigned long long raw0 = h[0], rays0 = h[3];
+        unsigned long long t5 = 0;
+        NRT_CUDA(cudaMemcpyAsync(&t5, ctr + 4, 8, cudaMemcpyDeviceToHost, st));
+        NRT_CUDA(cudaStreamSynchronize(st));
+        const unsigned long long raw0 = h[0], rays0 = h[3], terms0 = t5;
         for (int attempt = 0; attempt < 4; ++attempt) {
-            unsigned long long z[4] = {raw0, 0, 0, rays0};  // a re-run starts from the level's counts
-            NRT_CUDA(cudaMemcpyAsync(ctr, z, 4 * 8, cudaMemcpyHostToDevice, st));
+            unsigned long long z[5] = {raw0, 0, 0, rays0, terms0};  // a re-run starts from the level's counts
+            NRT_CUDA(cudaMemcpyAsync(ctr, z, 5 * 8, cudaMemcpyHostToDevice, st));
             A.raw = raw;
             A.raw_cap = raw_cap;
             A.out = qout;
@@ -2956,11 +2976,37 @@ nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out
             A.in = qin;
             A.n_in = n_in;
             const unsigned long long items = level == 0 ? (unsigned long long)n_ie : n_in;
+            // grow the record buffer ahead of the level (a re-run costs the whole level)
+            const unsigned long long rest = std::min<unsigned long long>(raw0 + 8 * items + 4096, 1ull << 25);
+            if (attempt == 0 && raw_cap < rest) {
+                nrt_coarse_rec* nr2 = nullptr;
+                NRT_CUDA(cudaMallocAsync(&nr2, rest * sizeof(nrt_coarse_rec), st));
+                if (raw0) NRT_CUDA(cudaMemcpyAsync(nr2, raw, raw0 * sizeof(nrt_coarse_rec), cudaMemcpyDeviceToDevice, st));
+                cudaFreeAsync(raw, st);
+                raw = nr2;
+                raw_cap = rest;
+                A.raw = raw;
+                A.raw_cap = raw_cap;
+            }
+            const unsigned long long est = std::min<unsigned long long>(24 * items, 1ull << 26);
+            if (attempt == 0 && out_cap < est && level < NRT_MAX_INT) {  // children: ~10-100 per item
+                cudaFreeAsync(qout, st);
+                out_cap = est;
+                NRT_CUDA(cudaMallocAsync(&qout, out_cap * sizeof(CRay), st));
+                A.out = qout;
+                A.out_cap = out_cap;
+            }
             unsigned blocks = (unsigned)std::min<unsigned long long>((unsigned long long)sms * per_sm, (items + 3) / 4);
             if (blocks < 1) blocks = 1;
             cudaEventRecord(e0, st);
-            if (level == 0) k_env_tx<false><<<blocks, 128, 0, st>>>(P, A);
-            else k_env_prop<false><<<blocks, 128, 0, st>>>(P, A);
+            if (level == 0) {
+                if (counters) k_env_tx<true><<<blocks, 128, 0, st>>>(P, A);
+                else k_env_tx<false><<<blocks, 128, 0, st>>>(P, A);
+            } else if (counters) {
+                k_env_prop<true><<<blocks, 128, 0, st>>>(P, A);
+            } else {
+                k_env_prop<false><<<blocks, 128, 0, st>>>(P, A);
+            }
             ::nrt::count_launch();
             cudaEventRecord(e1, st);
             NRT_CUDA(cudaGetLastError());
@@ -2968,6 +3014,9 @@ nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out
             NRT_CUDA(cudaStreamSynchronize(st));
             float ms = 0.0f;
             cudaEventElapsedTime(&ms, e0, e1);
+            if (getenv("NRT_PHASES"))
+                fprintf(stderr, "[nrt] cone level %d attempt %d: %llu items, %.3f ms, children %llu/%llu, records %llu/%llu\n",
+                        level, attempt, items, ms, h[1], out_cap, h[0], raw_cap);
             if (h[0] <= raw_cap && h[1] <= out_cap) {
                 tot += ms;
                 break;
@@ -2995,9 +3044,10 @@ nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out
         qout = nullptr;
         NRT_CUDA(cudaMallocAsync(&qout, out_cap * sizeof(CRay), st));
     }
-    unsigned long long h[4];
+    unsigned long long h[5];
     NRT_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
     NRT_CUDA(cudaStreamSynchronize(st));
+    *terms_out = h[4];
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     for (void* p : {(void*)d_ie, (void*)d_pcs, (void*)d_vs, (void*)d_vi, (void*)d_m, (void*)ctr, (void*)qin, (void*)qout})
