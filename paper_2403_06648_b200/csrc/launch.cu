@@ -835,6 +835,36 @@ __device__ __forceinline__ void sdf_accum(const TP& P, unsigned k0, unsigned k1,
     if (CNT && lane == 0) cnt.tests += k1 - k0;  // Gaussian terms (the SDF mode's unit of work)
     const bool u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
     for (unsigned kb = k0; kb < k1; kb += 64) {
+        if (k1 - kb <= 32) {
+            // a single (last) chunk: one point per lane; tree levels 16, 8, 4 as a multi-value
+            // butterfly (quantity bits = lane bits 4, 3, 2), levels 2, 1 plain, then one shuffle
+            // moves quantity q to lanes with (lane >> 1) & 7 == q, the layout of `acc`
+            const unsigned k = kb + lane;
+            const unsigned kc = k < k1 ? k : k1 - 1;
+            const float4 A = __ldg(&P.sdf_pts[2 * kc]), B = __ldg(&P.sdf_pts[2 * kc + 1]);
+            const float d0 = A.x - x0, d1 = A.y - x1, d2 = A.z - x2;
+            const float q = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, d0 * d0));
+            const float w = k < k1 ? sdf_expf(-(q * P.sdf_inv)) : 0.0f;
+            const float v[8] = {w, w * A.x, w * A.y, w * A.z, w * B.x, w * B.y, w * B.z, 0.0f};
+            const bool u16 = lane & 16;
+            float a[4], b2[2];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float snd = u16 ? v[c] : v[c + 4], kp = u16 ? v[c + 4] : v[c];
+                a[c] = kp + __shfl_xor_sync(0xffffffffu, snd, 16);
+            }
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const float snd = u8 ? a[c] : a[c + 2], kp = u8 ? a[c + 2] : a[c];
+                b2[c] = kp + __shfl_xor_sync(0xffffffffu, snd, 8);
+            }
+            float t = (u4 ? b2[1] : b2[0]) + __shfl_xor_sync(0xffffffffu, u4 ? b2[0] : b2[1], 4);
+            t = t + __shfl_xor_sync(0xffffffffu, t, 2);
+            t = t + __shfl_xor_sync(0xffffffffu, t, 1);
+            const unsigned src = (((lane >> 3) & 1u) << 4) | (((lane >> 2) & 1u) << 3) | (((lane >> 1) & 1u) << 2);
+            acc = acc + __shfl_sync(0xffffffffu, t, src);
+            break;
+        }
         float v[8];
         v[7] = 0.0f;
 #pragma unroll

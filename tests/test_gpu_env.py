@@ -95,3 +95,24 @@ def test_env_errors(N):
     sc = N.build_case_scene(case)
     with pytest.raises(N.NrtError):
         N.launch_case(sc, case, tracer=1, intersect=0)
+
+
+@pytest.mark.parametrize("name,parts", [("C4", 512), ("C5", 2048)])
+def test_env_fullsize_sharded_subset_bit_exact(N, O, name, parts):
+    """Full-size scenes (1e7 surfels; C4: 85 RX with diffraction, C5: 879 RX): the transmission
+    shard i == 0 (mod parts) and its whole cone-traced subtree (rank 0 of world = parts) equals
+    the oracle's part 0 — records (kappa = 2^30 keeps every one), raw and validation-ray counts."""
+    case = G.case(name, max_refl=2)
+    case.sdf = dict(SDF)
+    case.kappa = 1 << 30
+    sc = N.build_case_scene(case)
+    p = N.launch_case(sc, case, tracer=1, rank=0, world=parts, stage=1)
+    got, info = p.export(), p.info()
+    O.env_lib()
+    O._FORK["env"] = O.EnvScene(case)
+    raw, rays = O._env_worker((case, 0, parts))
+    O._FORK.pop("env", None)
+    ref = O.dedupe(raw, case.kappa)
+    assert info["n_raw"] == len(raw) and info["bounces"] == rays, (info["n_raw"], len(raw), info["bounces"], rays)
+    assert_same_records(got, ref, f"NEXT-2 {name} shard 0/{parts}")
+    assert len(got) > 0

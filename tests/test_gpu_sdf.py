@@ -145,3 +145,18 @@ def test_sdf_errors(N):
     sc = N.build_case_scene(case)
     with pytest.raises(N.NrtError):
         N.launch_case(sc, case, sdf_t_sdf=0.0)
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_fullsize_sdf_sampled_hit_sequences(N, O, name):
+    """The reconstructed-room configs (1e7 surfels, 1e7 / 1e8-ray lattices) with the SDF
+    intersection: sampled rays' per-segment hits equal the oracle's tier-0 SDF tracer."""
+    case = sdf_case(name)
+    sc = N.build_case_scene(case)
+    ids = np.sort(np.random.default_rng(7).choice(case.n_rays, 12, replace=False)).astype(np.uint64)
+    d = N.case_desc(case)
+    d.pop("kappa"), d.pop("dphi_deg"), d.pop("edge_bin")
+    gpu = N.nrt_debug_trace_rays(sc, case.tx, case.n_rays, case.max_refl, ids, **d)
+    _, hits, _ = O.trace_rays(case, ids)
+    assert np.array_equal(gpu, hits)
+    assert (gpu[:, 1] >= 0).sum() > 3
