@@ -473,7 +473,7 @@ def main():
         achieved = fl / (ms_trace / 1000.0) / 1e12
         roof_trace = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
                       "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
-                      "traffic": measured_traffic(case.name + "_sdf"),
+                      "traffic": measured_traffic(case.name + ("_env" if getattr(case, "tracer", 0) else "_sdf")),
                       "kernel": ("k_env_tx + k_env_prop (cone tracing; SDF validation rays, one warp per "
                                  "ray)" if getattr(case, "tracer", 0) else
                                  "k_trace_sdf (primary bounces; one warp per segment)"),
@@ -507,7 +507,7 @@ def main():
         fl = FLOPS_SDF_TERM * cnt["mls_value"]
         ach = fl / (ms_refine / 1000.0) / 1e12 if ms_refine else 0.0
         roof_refine = {"bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                       "frac": ach / FP32_PEAK_TFLOPS, "traffic": None,
+                       "frac": ach / FP32_PEAK_TFLOPS, "traffic": measured_traffic(case.name + "_gd"),
                        "kernel": "k_refine_gd (the paper's GD, one warp per path)",
                        "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz",
                        "flops_per_launch": fl, "gaussian_terms": cnt["mls_value"],
