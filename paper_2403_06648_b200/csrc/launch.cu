@@ -59,13 +59,19 @@ struct RayCold {
     Hist h;
 };
 
+// per-ray hot state, one 64 B record (two full sectors): TRACE reads it whole, SHADE rewrites
+// it whole (no partial-sector read-modify-writes); the hit goes into l1.xy once the segment's
+// departure normals are no longer needed
+struct __align__(64) RayHot {
+    float4 o;   // origin xyz, prev surfel id / cell (int bits)
+    float4 d;   // direction
+    float4 l0;  // departure-sheet normal 0
+    float4 l1;  // departure-sheet normal 1; after TRACE: (best_t, best id bits, -, -)
+};
+
 struct Wave {
     void* slab;      // one workspace block holding all arrays below
-    float4* o;       // [cap] origin xyz, prev surfel id (int bits)
-    float4* d;       // [cap] direction
-    float4* l0;      // [cap] departure-sheet normal 0
-    float4* l1;      // [cap] departure-sheet normal 1
-    float2* hit;     // [cap] (best_t, best id bits)
+    RayHot* ray;     // [cap]
     float4* hitn;    // [cap] SDF mode: (unit MLS normal at the hit, AABB cell bits)
     RayCold* cold;   // [cap]
     unsigned* alive[2];       // ping-pong live lists
@@ -588,14 +594,15 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace(TP P, Wave W, int
                     done = true;
                 } else {
                     ray = alive[j];
-                    const float4 o = W.o[ray], d = W.d[ray], a = W.l0[ray], c = W.l1[ray];
+                    const RayHot R = W.ray[ray];
+                    const float4 o = R.o, d = R.d, a = R.l0, c = R.l1;
                     s.o = make_float3(o.x, o.y, o.z);
                     s.prev = __float_as_int(o.w);
                     s.d = make_float3(d.x, d.y, d.z);
                     s.l0 = make_float3(a.x, a.y, a.z);
                     s.l1 = make_float3(c.x, c.y, c.z);
                     ++bounces;
-                    if (!seg_begin<CNT>(P, s, cnt)) W.hit[ray] = make_float2(INFINITY, __int_as_float(-1));
+                    if (!seg_begin<CNT>(P, s, cnt)) *(float2*)&W.ray[ray].l1 = make_float2(INFINITY, __int_as_float(-1));
                     else have = true;
                 }
             }
@@ -607,7 +614,8 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace(TP P, Wave W, int
             const unsigned long long j = NRT_TRACE_FETCH(&W.ctr[b]);
             if (j >= n) break;
             ray = alive[j];
-            const float4 o = W.o[ray], d = W.d[ray], a = W.l0[ray], c = W.l1[ray];
+            const RayHot R = W.ray[ray];
+            const float4 o = R.o, d = R.d, a = R.l0, c = R.l1;
             s.o = make_float3(o.x, o.y, o.z);
             s.prev = __float_as_int(o.w);
             s.d = make_float3(d.x, d.y, d.z);
@@ -615,7 +623,7 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace(TP P, Wave W, int
             s.l1 = make_float3(c.x, c.y, c.z);
             ++bounces;
             if (!seg_begin<CNT>(P, s, cnt)) {
-                W.hit[ray] = make_float2(INFINITY, __int_as_float(-1));
+                *(float2*)&W.ray[ray].l1 = make_float2(INFINITY, __int_as_float(-1));
                 continue;
             }
             have = true;
@@ -640,7 +648,7 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace(TP P, Wave W, int
         }
         const float te = fminf(s.tmx, fminf(s.tmy, s.tmz));
         if (s.best_t < te - P.pad || !grid_move<CNT>(P, s, cnt)) {
-            W.hit[ray] = make_float2(s.best_t, __int_as_float(s.best));
+            *(float2*)&W.ray[ray].l1 = make_float2(s.best_t, __int_as_float(s.best));
             have = false;
         }
     }
@@ -708,7 +716,8 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace_coop(TP P, Wave W
                     break;
                 }
                 ray = alive[j];
-                const float4 o = W.o[ray], d = W.d[ray], a = W.l0[ray], c = W.l1[ray];
+                const RayHot R = W.ray[ray];
+                const float4 o = R.o, d = R.d, a = R.l0, c = R.l1;
                 sray[wid][0][lane] = o;
                 sray[wid][1][lane] = d;
                 sray[wid][2][lane] = a;
@@ -718,7 +727,7 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace_coop(TP P, Wave W
                 s.d = make_float3(d.x, d.y, d.z);
                 ++bounces;
                 if (!seg_begin<CNT>(P, s, cnt)) {
-                    W.hit[ray] = make_float2(INFINITY, __int_as_float(-1));
+                    *(float2*)&W.ray[ray].l1 = make_float2(INFINITY, __int_as_float(-1));
                     continue;
                 }
                 have = true;
@@ -728,7 +737,7 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace_coop(TP P, Wave W
             const float bt = bk == ~0ull ? INFINITY : __uint_as_float((unsigned)(bk >> 32));
             const float te = fminf(s.tmx, fminf(s.tmy, s.tmz));
             if (bt < te - P.pad || !grid_move<CNT>(P, s, cnt)) {
-                W.hit[ray] = make_float2(bt, __int_as_float(bk == ~0ull ? -1 : (int)(unsigned)bk));
+                *(float2*)&W.ray[ray].l1 = make_float2(bt, __int_as_float(bk == ~0ull ? -1 : (int)(unsigned)bk));
                 have = false;
                 continue;
             }
@@ -1239,7 +1248,8 @@ __global__ void __launch_bounds__(128, NRT_SDF_MINB) k_trace_sdf(TP P, Wave W, i
         if (jj >= n) break;
         const unsigned ray = alive[jj];
         if (lane == 0) ++bounces;
-        const float4 o4 = W.o[ray], d4 = W.d[ray], a4 = W.l0[ray], c4 = W.l1[ray];
+        const RayHot R = W.ray[ray];
+        const float4 o4 = R.o, d4 = R.d, a4 = R.l0, c4 = R.l1;
         const float3 o = make_float3(o4.x, o4.y, o4.z), d = make_float3(d4.x, d4.y, d4.z);
         const float3 l0 = make_float3(a4.x, a4.y, a4.z), l1 = make_float3(c4.x, c4.y, c4.z);
         const unsigned prev = __float_as_uint(o4.w);  // cell of the previous hit (~0: none)
@@ -1249,7 +1259,7 @@ __global__ void __launch_bounds__(128, NRT_SDF_MINB) k_trace_sdf(TP P, Wave W, i
         int pid;
         sdf_hit_attr<CNT>(P, best, best_t, o, d, hn, pid, cnt);
         if (lane == 0) {
-            W.hit[ray] = make_float2(best >= 0 ? best_t : INFINITY, __int_as_float(pid));
+            *(float2*)&W.ray[ray].l1 = make_float2(best >= 0 ? best_t : INFINITY, __int_as_float(pid));
             W.hitn[ray] = hn;
         }
     }
@@ -1981,9 +1991,9 @@ __global__ void __launch_bounds__(128) k_shade(TP P, Wave W, int b) {
         float4 o4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f), d4 = o4;
         float2 hit = make_float2(-1.0f, __int_as_float(-1));
         if (on) {
-            o4 = W.o[ray];
-            d4 = W.d[ray];
-            hit = W.hit[ray];
+            o4 = W.ray[ray].o;
+            d4 = W.ray[ray].d;
+            hit = *(const float2*)&W.ray[ray].l1;
         }
         const float3 o = make_float3(o4.x, o4.y, o4.z), d = make_float3(d4.x, d4.y, d4.z);
         const float th = hit.x;
@@ -2020,10 +2030,12 @@ __global__ void __launch_bounds__(128) k_shade(TP P, Wave W, int b) {
             const float k2 = 2.0f * dot3(d, nn);
             const float3 x = make_float3(d.x - k2 * nn.x, d.y - k2 * nn.y, d.z - k2 * nn.z);
             const float l = sqrtf(dot3(x, x));
-            W.d[ray] = make_float4(x.x / l, x.y / l, x.z / l, 0.0f);
-            W.o[ray] = make_float4(hp.x, hp.y, hp.z, P.sdf ? nv.w : __int_as_float(sid));  // prev: surfel / cell
-            W.l0[ray] = make_float4(nn.x, nn.y, nn.z, 0.0f);
-            W.l1[ray] = make_float4(nn.x, nn.y, nn.z, 0.0f);
+            RayHot R;
+            R.d = make_float4(x.x / l, x.y / l, x.z / l, 0.0f);
+            R.o = make_float4(hp.x, hp.y, hp.z, P.sdf ? nv.w : __int_as_float(sid));  // prev: surfel / cell
+            R.l0 = make_float4(nn.x, nn.y, nn.z, 0.0f);
+            R.l1 = make_float4(nn.x, nn.y, nn.z, 0.0f);
+            W.ray[ray] = R;
             c.L = L + th;
             c.Ls = Ls + th;
             c.seg = c.seg + 1;
@@ -2062,10 +2074,12 @@ __global__ void k_gen_primary(TP P, Wave W, uint64_t n_shard, uint64_t j0, const
         const uint64_t jr = perm ? (uint64_t)perm[j] : j;
         const uint64_t i = (uint64_t)P.rank + (j0 + jr) * (uint64_t)P.world;
         const float3 d = fib_dir(i, P.n_rays);
-        W.o[j] = make_float4(P.tx, P.ty, P.tz, __int_as_float(-1));
-        W.d[j] = make_float4(d.x, d.y, d.z, 0.0f);
-        W.l0[j] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        W.l1[j] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        RayHot R;
+        R.o = make_float4(P.tx, P.ty, P.tz, __int_as_float(-1));
+        R.d = make_float4(d.x, d.y, d.z, 0.0f);
+        R.l0 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        R.l1 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        W.ray[j] = R;
         RayCold& c = W.cold[j];
         c.L = 0.0f;
         c.Ls = 0.0f;
@@ -2091,10 +2105,12 @@ __global__ void k_gen_ids(TP P, Wave W, const uint64_t* ids, uint64_t n) {
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
          j += (uint64_t)gridDim.x * blockDim.x) {
         const float3 d = fib_dir(ids[j], P.n_rays);
-        W.o[j] = make_float4(P.tx, P.ty, P.tz, __int_as_float(-1));
-        W.d[j] = make_float4(d.x, d.y, d.z, 0.0f);
-        W.l0[j] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        W.l1[j] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        RayHot R;
+        R.o = make_float4(P.tx, P.ty, P.tz, __int_as_float(-1));
+        R.d = make_float4(d.x, d.y, d.z, 0.0f);
+        R.l0 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        R.l1 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        W.ray[j] = R;
         RayCold& c = W.cold[j];
         c.L = 0.0f;
         c.Ls = 0.0f;
@@ -2170,10 +2186,12 @@ __global__ void k_gen_fans(TP P, Wave W, const nrt_event_rec* ev, int64_t n_ev,
             const double x2 = cp * (double)E.t0[k] + sp * (double)E.n0[k];
             dir[k] = (float)(x2 * g.st + (double)E.e[k] * g.ct);
         }
-        W.o[f] = make_float4(o.x, o.y, o.z, __int_as_float(-1));
-        W.d[f] = make_float4(dir[0], dir[1], dir[2], 0.0f);
-        W.l0[f] = make_float4(E.n0[0], E.n0[1], E.n0[2], 0.0f);
-        W.l1[f] = make_float4(E.n1[0], E.n1[1], E.n1[2], 0.0f);
+        RayHot R;
+        R.o = make_float4(o.x, o.y, o.z, __int_as_float(-1));
+        R.d = make_float4(dir[0], dir[1], dir[2], 0.0f);
+        R.l0 = make_float4(E.n0[0], E.n0[1], E.n0[2], 0.0f);
+        R.l1 = make_float4(E.n1[0], E.n1[1], E.n1[2], 0.0f);
+        W.ray[f] = R;
         c.L = e.L;
         c.Ls = 0.0f;
         c.seg = 0;
@@ -2412,17 +2430,17 @@ static bool reorder_on(nrt_scene s) {
 static nrt_status alloc_wave(Wave& W, uint64_t cap, int dev, bool sdf, cudaStream_t st) {
     if (cap < 1) cap = 1;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-    const size_t b_o = al(cap * sizeof(float4)), b_h = al(cap * sizeof(float2)),
+    const size_t b_r = al(cap * sizeof(RayHot)), b_o = al(cap * sizeof(float4)),
                  b_c = al(cap * sizeof(RayCold)), b_a = al(cap * sizeof(unsigned));
     size_t b_t = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b_t, (unsigned*)nullptr, (unsigned*)nullptr,
                                     (unsigned*)nullptr, (unsigned*)nullptr, (int)cap, 0, 32, st);
     b_t = al(b_t);
-    const size_t total = 4 * b_o + b_h + b_c + 2 * b_a + 3 * b_a + b_t + (sdf ? b_o : 0);
+    const size_t total = b_r + b_c + 2 * b_a + 3 * b_a + b_t + (sdf ? b_o : 0);
     char* p = (char*)ws_get(dev, total, st);
     if (!p) return set_error(NRT_E_NOMEM, "wavefront workspace of %zu bytes", total);
     {
-        char* q = p + 4 * b_o + b_h + b_c + 2 * b_a;
+        char* q = p + b_r + b_c + 2 * b_a;
         W.okey[0] = (unsigned*)q;
         W.okey[1] = (unsigned*)(q + b_a);
         W.oval = (unsigned*)(q + 2 * b_a);
@@ -2432,14 +2450,10 @@ static nrt_status alloc_wave(Wave& W, uint64_t cap, int dev, bool sdf, cudaStrea
         W.skey = nullptr;  // per-bounce coherence reorder: see reorder_on()
     }
     W.slab = p;
-    W.o = (float4*)p;
-    W.d = (float4*)(p + b_o);
-    W.l0 = (float4*)(p + 2 * b_o);
-    W.l1 = (float4*)(p + 3 * b_o);
-    W.hit = (float2*)(p + 4 * b_o);
-    W.cold = (RayCold*)(p + 4 * b_o + b_h);
-    W.alive[0] = (unsigned*)(p + 4 * b_o + b_h + b_c);
-    W.alive[1] = (unsigned*)(p + 4 * b_o + b_h + b_c + b_a);
+    W.ray = (RayHot*)p;
+    W.cold = (RayCold*)(p + b_r);
+    W.alive[0] = (unsigned*)(p + b_r + b_c);
+    W.alive[1] = (unsigned*)(p + b_r + b_c + b_a);
     return NRT_OK;
 }
 // returns the slab to the workspace cache once no queued kernel still reads it
