@@ -1967,7 +1967,10 @@ __global__ void k_pad_keys(unsigned* keys, const unsigned long long* n_alive, ui
 // SHADE: captures, edge events, reflection; compacts the live list for bounce b+1.
 // Receivers (few) and edge cull spheres are staged in shared memory and looped over with a
 // warp-uniform trip count (one broadcast read per receiver/edge for the whole warp).
-__global__ void __launch_bounds__(128) k_shade(TP P, Wave W, int b) {
+#ifndef NRT_SHADE_MINB
+#define NRT_SHADE_MINB 5  // k_shade: min resident blocks/SM (register cap)
+#endif
+__global__ void __launch_bounds__(128, NRT_SHADE_MINB) k_shade(TP P, Wave W, int b) {
     extern __shared__ float4 sh[];
     float4* srx = sh;
     float4* sed = sh + P.shade_rx;
@@ -2481,10 +2484,19 @@ static nrt_status run_bounces(const TP& P, Wave& W, uint64_t cap, int iters, int
                                           : persistent_blocks(k_trace_sdf<false>, dev))
                               : (counters ? persistent_blocks(NRT_K_TRACE<true>, dev)
                                           : persistent_blocks(NRT_K_TRACE<false>, dev));
-    const unsigned sb = (unsigned)sm_count(dev) * 8;
     const size_t shade_smem = (size_t)(P.shade_rx + P.shade_edges) * sizeof(float4);
     if (shade_smem > 48 * 1024)
         NRT_CUDA(cudaFuncSetAttribute(k_shade, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shade_smem));
+    // SHADE: exactly one wave of resident blocks (its loop strides over the live list; a second,
+    // partial wave only lengthened the tail); NRT_SHADE_BLOCKS overrides (blocks per SM)
+    unsigned sb;
+    {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_shade, 128, shade_smem);
+        if (const char* e = getenv("NRT_SHADE_BLOCKS")) per_sm = atoi(e);
+        if (per_sm < 1) per_sm = 1;
+        sb = (unsigned)sm_count(dev) * (unsigned)per_sm;
+    }
     cudaEvent_t ev[3 * kMaxIter + 3];
     for (int i = 0; i < 3 * iters; ++i) cudaEventCreate(&ev[i]);
     unsigned long long last[3] = {0, 0, 0};
