@@ -809,6 +809,15 @@ __device__ __forceinline__ unsigned order_key(const TP& P, float3 h, float3 d) {
 // =======================================================================================
 // NEXT-1: the paper's point-set SDF intersection (DESIGN R40-R45, §6.4)
 // =======================================================================================
+// IEEE a / b with an exact shortcut for a zero dividend (+-0 with the quotient's sign): the
+// hardware division's fast path rejects zero dividends (FCHK), and axis-aligned normals and
+// ray origins on AABB faces make them common.  Bitwise the result of a / b.
+__device__ __forceinline__ float div0(float a, float b) {
+    const bool z = a == 0.0f;
+    const float q = (z ? 1.0f : a) / b;  // branch-free: a zero dividend divides 1 instead
+    return z ? __int_as_float((__float_as_int(a) ^ __float_as_int(b)) & 0x80000000) : q;
+}
+
 // R41: FP32 exp for x <= 0, the definition's fixed operation order (identical to the oracle's:
 // Cody-Waite split and Horner steps as single-rounding FMAs); 0 below -87 (branch-free)
 __device__ __forceinline__ float sdf_expf(float x) {
@@ -917,10 +926,10 @@ __device__ __forceinline__ bool sdf_eval(const TP& P, unsigned k0, unsigned k1, 
     const float p0 = __shfl_sync(0xffffffffu, acc, 2), p1 = __shfl_sync(0xffffffffu, acc, 4),
                 p2 = __shfl_sync(0xffffffffu, acc, 6), n0 = __shfl_sync(0xffffffffu, acc, 8),
                 n1 = __shfl_sync(0xffffffffu, acc, 10), n2 = __shfl_sync(0xffffffffu, acc, 12);
-    const float b0 = p0 / W, b1 = p1 / W, b2 = p2 / W;
-    nb0 = n0 / W;
-    nb1 = n1 / W;
-    nb2 = n2 / W;
+    const float b0 = div0(p0, W), b1 = div0(p1, W), b2 = div0(p2, W);
+    nb0 = div0(n0, W);
+    nb1 = div0(n1, W);
+    nb2 = div0(n2, W);
     const float e0 = x0 - b0, e1 = x1 - b1, e2 = x2 - b2;
     f = (e0 * nb0 + e1 * nb1) + e2 * nb2;
     return true;
@@ -957,12 +966,12 @@ __device__ __forceinline__ bool sdf_normal27(const TP& P, unsigned cell, float x
     if (!(W > 0.0f)) return false;
     const float a0 = __shfl_sync(0xffffffffu, acc, 8), a1 = __shfl_sync(0xffffffffu, acc, 10),
                 a2 = __shfl_sync(0xffffffffu, acc, 12);
-    const float b0 = a0 / W, b1 = a1 / W, b2 = a2 / W;
+    const float b0 = div0(a0, W), b1 = div0(a1, W), b2 = div0(a2, W);
     const float l = sqrtf((b0 * b0 + b1 * b1) + b2 * b2);
     if (!(l > 0.0f)) return false;
-    n0 = b0 / l;
-    n1 = b1 / l;
-    n2 = b2 / l;
+    n0 = div0(b0, l);
+    n1 = div0(b1, l);
+    n2 = div0(b2, l);
     return true;
 }
 
@@ -1035,7 +1044,7 @@ __device__ __forceinline__ bool sdf_excluded(const TP& P, const float3 o, const 
     if (!(fabsf(f) <= P.tau)) return false;
     const float l = sqrtf((nb0 * nb0 + nb1 * nb1) + nb2 * nb2);
     if (!(l > 0.0f)) return false;
-    const float u0 = nb0 / l, u1 = nb1 / l, u2 = nb2 / l;
+    const float u0 = div0(nb0, l), u1 = div0(nb1, l), u2 = div0(nb2, l);
     if (fabsf((u0 * l0.x + u1 * l0.y) + u2 * l0.z) >= P.cos_ex) return true;
     return fabsf((u0 * l1.x + u1 * l1.y) + u2 * l1.z) >= P.cos_ex;
 }
@@ -1201,9 +1210,9 @@ __device__ __forceinline__ void sdf_hit_attr(const TP& P, const int best, const 
         if (sdf_eval<CNT>(P, k0, k1, x0, x1, x2, f, nb0, nb1, nb2, cnt)) {
             const float l = sqrtf((nb0 * nb0 + nb1 * nb1) + nb2 * nb2);
             if (l > 0.0f) {
-                hn.x = nb0 / l;
-                hn.y = nb1 / l;
-                hn.z = nb2 / l;
+                hn.x = div0(nb0, l);
+                hn.y = div0(nb1, l);
+                hn.z = div0(nb2, l);
             }
         }
         // warp argmin of (q, k): per lane ascending k with strict <, then lexicographic
@@ -1304,9 +1313,9 @@ __device__ __forceinline__ void gd_basis(const float* n, float* u, float* v) {
     const float a0 = ax == 0 ? 1.0f : 0.0f, a1 = ax == 1 ? 1.0f : 0.0f, a2 = ax == 2 ? 1.0f : 0.0f;
     const float c0 = n[1] * a2 - n[2] * a1, c1 = n[2] * a0 - n[0] * a2, c2 = n[0] * a1 - n[1] * a0;
     const float l = sqrtf((c0 * c0 + c1 * c1) + c2 * c2);
-    u[0] = c0 / l;
-    u[1] = c1 / l;
-    u[2] = c2 / l;
+    u[0] = div0(c0, l);
+    u[1] = div0(c1, l);
+    u[2] = div0(c2, l);
     v[0] = n[1] * u[2] - n[2] * u[1];
     v[1] = n[2] * u[0] - n[0] * u[2];
     v[2] = n[0] * u[1] - n[1] * u[0];
@@ -3013,8 +3022,10 @@ nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     float tot = 0.0f;
+    double ratio = 24.0;
     for (int level = 0; level <= NRT_MAX_INT; ++level) {
         if (level > 0 && n_in == 0) break;
+        const unsigned long long items_done = level == 0 ? (unsigned long long)n_ie : n_in;
         unsigned long long h[4];
         NRT_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
         NRT_CUDA(cudaStreamSynchronize(st));
@@ -3044,7 +3055,9 @@ nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out
                 A.raw = raw;
                 A.raw_cap = raw_cap;
             }
-            const unsigned long long est = std::min<unsigned long long>(24 * items, 1ull << 26);
+            // children of this level: the previous level's ratio (x 1.25), 24 at the start
+            const unsigned long long est = std::min<unsigned long long>(
+                (unsigned long long)(1.25 * ratio * (double)items) + 4096, 1ull << 26);
             if (attempt == 0 && out_cap < est && level < NRT_MAX_INT) {  // children: ~10-100 per item
                 cudaFreeAsync(qout, st);
                 out_cap = est;
@@ -3094,6 +3107,7 @@ nrt_status launch_env(nrt_scene s, const LaunchArgs& a, nrt_coarse_rec** raw_out
             }
         }
         // the children become the next level's input
+        if (items_done > 0 && h[1] > 0) ratio = (double)h[1] / (double)items_done;
         n_in = h[1];
         if (qin) cudaFreeAsync(qin, st);
         qin = qout;
