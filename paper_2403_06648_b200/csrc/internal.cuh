@@ -112,13 +112,20 @@ struct DevEdge {
     float b_[3];     // the input end point b (refinement works in FP64 from a and b)
 };
 
-struct Hist {
+// a ray's interaction history: a 32 B header and one 32 B sector per interaction, so that the
+// per-segment append is one full-sector write
+struct __align__(32) HEnt {
+    int32_t label;
+    uint32_t prim;
+    float v[3];
+    int32_t pad_[3];
+};
+struct __align__(32) Hist {
     int32_t n, n_diff;
     uint32_t kinds;
-    int32_t label[NRT_MAX_INT];
-    uint32_t prim[NRT_MAX_INT];
-    float v[NRT_MAX_INT][3];
     float s_edge;
+    int32_t pad_[4];
+    HEnt e[NRT_MAX_INT];
 };
 
 }  // namespace nrt

@@ -50,12 +50,14 @@ constexpr int kShadeEdges = 1024;  // edge tables up to this size are staged in 
 #define NRT_SHADE_RX 32  // receiver sets up to this size are staged in smem (else receiver grid)
 #endif
 
-// per-ray state that only the shade kernel touches
-struct RayCold {
+// per-ray state that only the shade kernel touches: a 64 B header (two sectors, read as
+// vectors), then the history (its header sector and one sector per interaction)
+struct __align__(32) RayCold {
     float L, Ls, kR, R0;
     int32_t seg, budget, flags;  // flags: bit0 edge captures on, bit1 after a diffraction
     int32_t pad_;
     uint64_t rid;
+    uint64_t pad2_[3];
     Hist h;
 };
 
@@ -183,11 +185,11 @@ __device__ void write_record(const TP& P, const Hist& h, int rx, float L, uint64
 #pragma unroll
     for (int k = 0; k < NRT_MAX_INT; ++k) {
         bool on = k < h.n;
-        c.label[k] = on ? h.label[k] : 0;
-        c.prim[k] = on ? h.prim[k] : 0u;
-        c.v[k][0] = on ? h.v[k][0] : 0.0f;
-        c.v[k][1] = on ? h.v[k][1] : 0.0f;
-        c.v[k][2] = on ? h.v[k][2] : 0.0f;
+        c.label[k] = on ? h.e[k].label : 0;
+        c.prim[k] = on ? h.e[k].prim : 0u;
+        c.v[k][0] = on ? h.e[k].v[0] : 0.0f;
+        c.v[k][1] = on ? h.e[k].v[1] : 0.0f;
+        c.v[k][2] = on ? h.e[k].v[2] : 0.0f;
     }
     c.s_edge = h.s_edge;
     c.L = L;
@@ -316,11 +318,11 @@ __device__ __forceinline__ void edge_event(const TP& P, const Hist& h, float3 o,
 #pragma unroll
     for (int k = 0; k < NRT_MAX_INT; ++k) {
         bool on = k < h.n;
-        e.label[k] = on ? h.label[k] : 0;
-        e.prim[k] = on ? h.prim[k] : 0u;
-        e.v[k][0] = on ? h.v[k][0] : 0.0f;
-        e.v[k][1] = on ? h.v[k][1] : 0.0f;
-        e.v[k][2] = on ? h.v[k][2] : 0.0f;
+        e.label[k] = on ? h.e[k].label : 0;
+        e.prim[k] = on ? h.e[k].prim : 0u;
+        e.v[k][0] = on ? h.e[k].v[0] : 0.0f;
+        e.v[k][1] = on ? h.e[k].v[1] : 0.0f;
+        e.v[k][2] = on ? h.e[k].v[2] : 0.0f;
     }
     e.s_edge = h.s_edge;
     e.edge = (uint32_t)j;
@@ -2033,11 +2035,14 @@ __global__ void __launch_bounds__(128, NRT_SHADE_MINB) k_shade(TP P, Wave W, int
             const float4 nv = P.sdf ? W.hitn[ray] : __ldg(&P.sn[sid]);  // SDF: MLS normal (R44)
             const float3 nn = make_float3(nv.x, nv.y, nv.z);
             const int hn = c.h.n;
-            c.h.label[hn] = __ldg(&P.label[sid]);
-            c.h.prim[hn] = (uint32_t)sid;
-            c.h.v[hn][0] = hp.x;
-            c.h.v[hn][1] = hp.y;
-            c.h.v[hn][2] = hp.z;
+            HEnt en;
+            en.label = __ldg(&P.label[sid]);
+            en.prim = (uint32_t)sid;
+            en.v[0] = hp.x;
+            en.v[1] = hp.y;
+            en.v[2] = hp.z;
+            en.pad_[0] = en.pad_[1] = en.pad_[2] = 0;
+            c.h.e[hn] = en;  // one full 32 B sector
             c.h.n = hn + 1;
             const float k2 = 2.0f * dot3(d, nn);
             const float3 x = make_float3(d.x - k2 * nn.x, d.y - k2 * nn.y, d.z - k2 * nn.z);
@@ -2174,17 +2179,17 @@ __global__ void k_gen_fans(TP P, Wave W, const nrt_event_rec* ev, int64_t n_ev,
         h.n_diff = e.n_diff;
         h.kinds = e.kinds;
         for (int k = 0; k < NRT_MAX_INT; ++k) {
-            h.label[k] = e.label[k];
-            h.prim[k] = e.prim[k];
-            h.v[k][0] = e.v[k][0];
-            h.v[k][1] = e.v[k][1];
-            h.v[k][2] = e.v[k][2];
+            h.e[k].label = e.label[k];
+            h.e[k].prim = e.prim[k];
+            h.e[k].v[0] = e.v[k][0];
+            h.e[k].v[1] = e.v[k][1];
+            h.e[k].v[2] = e.v[k][2];
         }
-        h.label[h.n] = E.label;
-        h.prim[h.n] = e.edge;
-        h.v[h.n][0] = o.x;
-        h.v[h.n][1] = o.y;
-        h.v[h.n][2] = o.z;
+        h.e[h.n].label = E.label;
+        h.e[h.n].prim = e.edge;
+        h.e[h.n].v[0] = o.x;
+        h.e[h.n].v[1] = o.y;
+        h.e[h.n].v[2] = o.z;
         h.kinds |= 1u << h.n;
         h.n++;
         h.n_diff++;
