@@ -1109,7 +1109,8 @@ __device__ void write_refined(const RP& P, const Path& D, const nrt_coarse_rec& 
 // =======================================================================================
 constexpr int kWPB = 4;  // independent warps (paths) per block
 #ifndef NRT_WMINB
-#define NRT_WMINB 4  // resident blocks per SM the register budget is sized for (4 x 4 = 16 warps)
+#define NRT_WMINB 5  // resident blocks per SM the register budget is sized for (5 x 4 = 20 warps;
+                     // 96 registers with a few spills: C5 refine 705 -> 677 ms vs 4 / 128, 6 / 80 worse)
 #endif
 
 struct WS {  // one warp's path state in shared memory (J and A follow all WS, sized by m_max)

@@ -182,3 +182,19 @@ def test_select_partitions(N):
     diff = coarse.export()["n_diff"] > 0
     assert p1.tobytes() == full[~diff].tobytes()
     assert p2.tobytes() == full[diff].tobytes()
+
+
+def test_warp_and_block_kernels_agree(N, monkeypatch):
+    """The two refinement kernels (warp per path, the throughput regime the C4/C5 bench runs;
+    block of 12 warps per path, the latency regime) on the same C2 coarse set: every record
+    equal, bit for bit (they share the device functions and take trials in the same order)."""
+    case = G.case("C2", sigma=0.010)
+    sc = N.build_case_scene(case)
+    coarse = N.launch_case(sc, case)
+    monkeypatch.setenv("NRT_REFINE_IMPL", "block")
+    blk = refine_gpu(N, case, sc, coarse)
+    monkeypatch.setenv("NRT_REFINE_IMPL", "warp")
+    wrp = refine_gpu(N, case, sc, coarse)
+    assert len(blk) == len(wrp) > 1000
+    same = np.array([a.tobytes() == b.tobytes() for a, b in zip(blk, wrp)])
+    assert same.all(), (int((~same).sum()), np.nonzero(~same)[0][:5])
