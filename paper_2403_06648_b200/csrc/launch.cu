@@ -1052,7 +1052,11 @@ __device__ __forceinline__ bool sdf_excluded(const TP& P, const float3 o, const 
 }
 
 #ifndef NRT_SDF_MINB
-#define NRT_SDF_MINB 4  // k_trace_sdf: min resident blocks/SM (register cap 128)
+#define NRT_SDF_MINB 8  // k_trace_sdf, k_env_*: min resident blocks/SM (64 registers; A/B on C4 /
+                        // C2 / C2 cone tracing, 4 / 6 / 8 / 10 / 12: 8 best, -9 / -14 / -15 % vs 4)
+#endif
+#ifndef NRT_GD_MINB
+#define NRT_GD_MINB 4   // k_refine_gd (latency-bound per path: registers over occupancy)
 #endif
 // TRACE (SDF mode): one WARP per segment.  A 3D-DDA over the AABB traversal grid (Chebyshev
 // jumps over empty cells), executed uniformly by the warp; in a non-empty cell the lanes slab-
@@ -1359,7 +1363,7 @@ __device__ __forceinline__ int gd_trace(const TP& P, const GdVert* V, int j, con
 }
 
 template <bool CNT>
-__global__ void __launch_bounds__(128, NRT_SDF_MINB) k_refine_gd(TP P, GdArgs A) {
+__global__ void __launch_bounds__(128, NRT_GD_MINB) k_refine_gd(TP P, GdArgs A) {
     __shared__ GdVert sv[4][NRT_MAX_INT];
     const unsigned lane = threadIdx.x & 31;
     GdVert* V = sv[threadIdx.x >> 5];

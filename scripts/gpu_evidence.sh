@@ -21,3 +21,8 @@ timeout 900 python bench.py --config C2 --tracer env --steps 5 --warmup 3 > gpur
 echo "bench C2 env rc=$?" | tee -a gpurun_out/$TAG.status
 timeout 900 python bench.py --config C2 --intersect sdf --refine gd --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/$TAG.bench_C2_sdf_gd.json 2> gpurun_out/$TAG.bench_C2_sdf_gd.err
 echo "bench C2 sdf gd rc=$?" | tee -a gpurun_out/$TAG.status
+# launch lists (per-kernel time + DRAM bytes) of one C5 step and of the NEXT kernels
+timeout 1800 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/$TAG.launches_C5.csv python scripts/prof_step.py C5 2 > /dev/null 2>&1
+echo "launch list C5 rc=$?" | tee -a gpurun_out/$TAG.status
+PYTHONPATH=. timeout 1800 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv -k regex:"k_trace_sdf|k_env_tx|k_env_prop|k_refine_gd" --log-file gpurun_out/$TAG.launches_next.csv python scripts/prof_next.py > /dev/null 2>&1
+echo "launch list next rc=$?" | tee -a gpurun_out/$TAG.status
