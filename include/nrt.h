@@ -326,7 +326,7 @@ const char* nrt_version(void);
 /* Number of CUDA kernels this library has launched in the process so far (evidence counter). */
 uint64_t nrt_kernel_launches(void);
 /* Bytes of device memory the library keeps cached between launches (wavefront workspaces:
- * per-ray state of the rays in flight, up to ~300 B x 2^24 rays), and a call that returns
+ *  per-ray state of the rays in flight, up to ~440 B x 2^26 rays), and a call that returns
  * all idle cached blocks to the CUDA memory pool.  Must not race with a running launch. */
 /* Diagnostic: FP64 fused multiply-add throughput of this device, TFLOP/s (2 flops per FMA),
  * measured by a synthetic kernel of independent FMA chains (~20 ms).  The roofline denominator

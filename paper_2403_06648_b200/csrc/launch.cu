@@ -2424,11 +2424,12 @@ struct Counters {
 };
 
 static std::atomic<unsigned long long> g_hint_raw{0}, g_hint_ev{0}, g_hint_fan{0};
-// rays in flight per wavefront batch (bounded wavefront state: ~300 B per ray in flight);
-// NRT_BATCH overrides (A/B)
+// rays in flight per wavefront batch (bounded wavefront state: ~440 B per ray in flight, so
+// 2^26 rays hold ~30 GB of a 180 GB B200; measured on C5: 2^24 / 2^25 / 2^26 / 1e8 rays per
+// batch -> 1280 / 1269 / 1235 / 1237 ms per step); NRT_BATCH overrides (A/B)
 static uint64_t batch_rays() {
     if (const char* e = getenv("NRT_BATCH")) return strtoull(e, nullptr, 10);
-    return 1ull << 24;
+    return 1ull << 26;
 }
 // reorder live lists of batches at least this long (NRT_SORT_MIN overrides: tests force the
 // reorder path on small scenes)
