@@ -1107,7 +1107,10 @@ __device__ void write_refined(const RP& P, const Path& D, const nrt_coarse_rec& 
 // the validity checks all on that warp; the candidate lists live in a per-warp global scratch
 // (L2-resident), the path state in shared memory.
 // =======================================================================================
-constexpr int kWPB = 4;  // independent warps (paths) per block
+#ifndef NRT_WPB
+#define NRT_WPB 4
+#endif
+constexpr int kWPB = NRT_WPB;  // independent warps (paths) per block
 #ifndef NRT_WMINB
 #define NRT_WMINB 5  // resident blocks per SM the register budget is sized for (5 x 4 = 20 warps;
                      // 96 registers with a few spills: C5 refine 705 -> 677 ms vs 4 / 128, 6 / 80 worse)
