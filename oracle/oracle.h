@@ -136,6 +136,9 @@ void or_sdf_aabb(const or_sdf* G, int64_t j, float lo[3], float hi[3], int64_t* 
 float or_sdf_expf(float x);
 int or_sdf_eval(const or_scene* S, const or_sdf* G, int64_t j, const float x[3], float sigma, float* f,
                 float nbar[3]);
+/* tier 1 for the SDF intersection: a uniform grid (edge `voxel`) over the AABBs; afterwards
+ * or_sdf_nearest walks it (same argmin as tier 0, pinned) */
+void or_sdf_grid_build(or_sdf* G, double voxel);
 /* nearest SDF hit of (o, d): returns the record's surfel id (-1: escape), *t_out, the hit
  * AABB's cell (for the departure rule of the next segment) and the unit hit normal */
 int64_t or_sdf_nearest(const or_scene* S, const or_sdf* G, const or_sdf_params* Q, const float o[3],

@@ -113,6 +113,7 @@ def lib():
         L.or_fan_dirs.argtypes = [C.POINTER(_Edge), C.c_void_p, C.c_float, C.c_void_p, C.c_int]
         L.or_sdf_build.argtypes = [C.POINTER(_Scene), C.c_float]
         L.or_sdf_build.restype = C.c_void_p
+        L.or_sdf_grid_build.argtypes = [C.c_void_p, C.c_double]
         L.or_sdf_free.argtypes = [C.c_void_p]
         L.or_sdf_count.argtypes = [C.c_void_p]
         L.or_sdf_count.restype = C.c_int64
@@ -148,7 +149,7 @@ class OracleScene:
     tier-1 uniform grid (grid.c: the same argmin as the brute force, pinned to it bit for bit);
     shift (3,) moves the grid origin (invariance pins)."""
 
-    def __init__(self, scene, grid_voxel=None, shift=None, sdf_cell=None):
+    def __init__(self, scene, grid_voxel=None, shift=None, sdf_cell=None, sdf_grid=None):
         self.p = _f32(scene.points, (-1, 3))
         self.nrm = _f32(scene.normals, (-1, 3))
         self.r = _f32(scene.radii, (-1,))
@@ -173,6 +174,8 @@ class OracleScene:
         if sdf_cell:
             self.sdf = lib().or_sdf_build(C.byref(self.c), float(sdf_cell))
             self.c.sdf = self.sdf
+            if sdf_grid:  # tier 1 for the SDF intersection (same argmin, pinned)
+                lib().or_sdf_grid_build(self.sdf, float(sdf_grid))
         if grid_voxel is not None:
             sh = np.ascontiguousarray(np.zeros(3) if shift is None else shift, np.float64)
             self.grid = lib().or_grid_build(C.byref(self.c), float(grid_voxel), sh.ctypes.data)
@@ -678,8 +681,8 @@ def _gd_params(case, **over):
     return p, rxa
 
 
-def gd_scene(case, **over):
-    return OracleScene(case.scene, sdf_cell=gd_settings(case, **over)["cell"])
+def gd_scene(case, sdf_grid=None, **over):
+    return OracleScene(case.scene, sdf_cell=gd_settings(case, **over)["cell"], sdf_grid=sdf_grid)
 
 
 def gd_lib():
@@ -716,14 +719,16 @@ def _gd_worker(args):
     return refine_gd(case, recs, _FORK.get("gdscene"), **over)
 
 
-def refine_gd_par(case, coarse, procs=1, **over):
-    """refine_gd() over forked single-threaded processes (out[q] is the serial result)."""
+def refine_gd_par(case, coarse, procs=1, sdf_grid=None, **over):
+    """refine_gd() over forked single-threaded processes (out[q] is the serial result);
+    sdf_grid: trace with the tier-1 SDF grid of that voxel (same results, pinned)."""
     import multiprocessing as mp
     lib()
     cin = np.ascontiguousarray(coarse, dtype=COARSE_DTYPE)
     if procs <= 1 or len(cin) < 2:
-        return refine_gd(case, cin, **over)
-    _FORK["gdscene"] = gd_scene(case, **over)
+        return refine_gd(case, cin, scene=gd_scene(case, sdf_grid=sdf_grid, **over) if sdf_grid else None,
+                         **over)
+    _FORK["gdscene"] = gd_scene(case, sdf_grid=sdf_grid, **over)
     chunks = [cin[k::procs] for k in range(procs)]
     with mp.get_context("fork").Pool(procs) as pool:
         parts = pool.map(_gd_worker, [(case, c, over) for c in chunks if len(c)])
@@ -760,8 +765,8 @@ def env_lib():
 class EnvScene:
     """The oracle scene with its SDF AABBs and the NEXT-2 IE tables for a case's RX set."""
 
-    def __init__(self, case):
-        self.sc = coarse_scene(case)
+    def __init__(self, case, sdf_grid=None):
+        self.sc = coarse_scene(case, sdf_grid=sdf_grid)
         self.rx = _f32(case.rx, (-1, 3))
         self.E = env_lib().or_env_build(C.byref(self.sc.c), self.rx.ctypes.data, self.rx.shape[0])
         assert self.E
@@ -808,12 +813,13 @@ def _env_worker(args):
         cap = int(n.value) + 1
 
 
-def env_launch(case, procs=1):
+def env_launch(case, procs=1, sdf_grid=None):
     """NEXT-2 coarse set: transmission + cone tracing over forked processes (IE shards), then
-    the R17 kappa dedupe -> (records, raw count, validation rays traced)."""
+    the R17 kappa dedupe -> (records, raw count, validation rays traced); sdf_grid: validate
+    with the tier-1 SDF grid (same results, pinned)."""
     import multiprocessing as mp
     env_lib()
-    _FORK["env"] = EnvScene(case)
+    _FORK["env"] = EnvScene(case, sdf_grid=sdf_grid)
     parts = max(1, procs)
     if parts == 1:
         res = [_env_worker((case, 0, 1))]

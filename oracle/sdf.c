@@ -33,6 +33,15 @@
 
 #include "oracle.h"
 
+typedef struct {      /* tier 1 (optional): a uniform grid over the AABBs, see or_sdf_grid_build */
+    double org[3], v, pad;
+    int64_t dims[3];
+    int64_t* start;     /* [ncell + 1] CSR offsets */
+    int64_t* aabb;      /* AABB indices registered per cell, ascending */
+    int64_t* stamp;     /* [n_aabb] last query that tested the AABB */
+    int64_t query;
+} sdf_tgrid;
+
 struct or_sdf {
     float org[3];       /* cell origin: the points' minimum */
     float a;            /* cell edge */
@@ -43,6 +52,7 @@ struct or_sdf {
     int64_t* ids;       /* point ids per AABB, ascending */
     float* lo;          /* [3 n_aabb] AABB bounds */
     float* hi;
+    sdf_tgrid* tg;      /* tier 1 when set */
 };
 
 /* R41: exp(x) for x <= 0 in FP32, fixed operation order (Cody-Waite ln2 split + degree-7
@@ -148,6 +158,12 @@ or_sdf* or_sdf_build(const or_scene* S, float a) {
 
 void or_sdf_free(or_sdf* G) {
     if (!G) return;
+    if (G->tg) {
+        free(G->tg->start);
+        free(G->tg->aabb);
+        free(G->tg->stamp);
+        free(G->tg);
+    }
     free(G->cell);
     free(G->start);
     free(G->ids);
@@ -279,20 +295,144 @@ static int excluded(const or_scene* S, const or_sdf* G, int64_t j, const float o
     return 0;
 }
 
-/* R43-R44: the segment's nearest SDF hit over every AABB (tier 0) */
+/* tier 1: the same argmin over the AABBs a FP64 walk of the tier-1 grid reaches.  AABB j is
+ * registered in every cell its box inflated by pad overlaps; a march of j can only start once
+ * the ray is in its box (slab test) and only at t >= tn - L (L = the march segment: its centre
+ * projection lies within half a diagonal of the box), so once best_t < t_exit - pad - L no
+ * untested AABB can win.  Candidates are compared lexicographically (t, index), so the visiting
+ * order does not matter: the result is tier 0's. */
+static int64_t nearest_t1(const or_scene* S, const or_sdf* G, const or_sdf_params* Q, const float o[3],
+                          const float d[3], const float* lam, int n_lam, int64_t prev_cell, float tau,
+                          float cos_ex, float* bt_out) {
+    sdf_tgrid* T = G->tg;
+    const int64_t qid = ++T->query;
+    float bt = INFINITY;
+    int64_t bj = -1;
+    const double L = 2.0 * (double)(0.5f * (Q->cell * 1.7320508f));
+    double od[3] = {o[0], o[1], o[2]}, dd[3] = {d[0], d[1], d[2]};
+    double t0 = 0.0, t1 = INFINITY;
+    for (int a = 0; a < 3; ++a) {
+        double lo = T->org[a], hi = T->org[a] + (double)T->dims[a] * T->v;
+        if (dd[a] != 0.0) {
+            double ta = (lo - od[a]) / dd[a], tb = (hi - od[a]) / dd[a];
+            t0 = fmax(t0, fmin(ta, tb));
+            t1 = fmin(t1, fmax(ta, tb));
+        } else if (od[a] < lo || od[a] > hi) {
+            t1 = -1.0;
+        }
+    }
+    if (t0 > t1) {
+        *bt_out = bt;
+        return -1;
+    }
+    int64_t c[3];
+    double tm[3];
+    for (int a = 0; a < 3; ++a) {
+        double x = od[a] + t0 * dd[a];
+        c[a] = (int64_t)floor((x - T->org[a]) / T->v);
+        if (c[a] < 0) c[a] = 0;
+        if (c[a] > T->dims[a] - 1) c[a] = T->dims[a] - 1;
+        tm[a] = dd[a] != 0.0 ? (T->org[a] + (double)(c[a] + (dd[a] > 0.0)) * T->v - od[a]) / dd[a] : INFINITY;
+    }
+    for (;;) {
+        const int64_t cell = c[0] + T->dims[0] * (c[1] + T->dims[1] * c[2]);
+        for (int64_t k = T->start[cell]; k < T->start[cell + 1]; ++k) {
+            const int64_t j = T->aabb[k];
+            if (T->stamp[j] == qid) continue;
+            T->stamp[j] = qid;
+            if (G->cell[j] == prev_cell) continue;
+            float t;
+            if (!march(S, G, j, o, d, Q, &t)) continue;
+            if (!(t < bt || (t == bt && j < bj))) continue;
+            if (excluded(S, G, j, o, lam, n_lam, Q, tau, cos_ex)) continue;
+            bt = t;
+            bj = j;
+        }
+        int ax = 0;
+        if (tm[1] < tm[ax]) ax = 1;
+        if (tm[2] < tm[ax]) ax = 2;
+        if ((double)bt < tm[ax] - T->pad - L) break;
+        c[ax] += dd[ax] > 0.0 ? 1 : -1;
+        if (c[ax] < 0 || c[ax] >= T->dims[ax]) break;
+        tm[ax] = (T->org[ax] + (double)(c[ax] + (dd[ax] > 0.0)) * T->v - od[ax]) / dd[ax];
+    }
+    *bt_out = bt;
+    return bj;
+}
+
+/* tier 1 for the SDF: register every AABB in the cells (edge voxel, origin = the AABB grid's
+ * minus one voxel) its box inflated by 1e-4 m + 1e-6 x extent overlaps */
+void or_sdf_grid_build(or_sdf* G, double voxel) {
+    if (!G || G->n_aabb == 0) return;
+    sdf_tgrid* T = (sdf_tgrid*)calloc(1, sizeof(sdf_tgrid));
+    double lo[3], hi[3], ext = 0.0;
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = INFINITY;
+        hi[k] = -INFINITY;
+    }
+    for (int64_t j = 0; j < G->n_aabb; ++j)
+        for (int k = 0; k < 3; ++k) {
+            if (G->lo[3 * j + k] < lo[k]) lo[k] = G->lo[3 * j + k];
+            if (G->hi[3 * j + k] > hi[k]) hi[k] = G->hi[3 * j + k];
+        }
+    for (int k = 0; k < 3; ++k) ext = fmax(ext, fmax(fabs(lo[k]), fabs(hi[k])));
+    T->v = voxel;
+    T->pad = 1e-4 + 1e-6 * ext;
+    int64_t nc = 1;
+    for (int k = 0; k < 3; ++k) {
+        T->org[k] = lo[k] - voxel;
+        T->dims[k] = (int64_t)ceil((hi[k] + voxel - T->org[k]) / voxel) + 1;
+        nc *= T->dims[k];
+    }
+    int64_t* cnt = (int64_t*)calloc((size_t)nc + 1, sizeof(int64_t));
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int64_t j = 0; j < G->n_aabb; ++j) {
+            int64_t a0[3], a1[3];
+            for (int k = 0; k < 3; ++k) {
+                a0[k] = (int64_t)floor(((double)G->lo[3 * j + k] - T->pad - T->org[k]) / voxel);
+                a1[k] = (int64_t)floor(((double)G->hi[3 * j + k] + T->pad - T->org[k]) / voxel);
+                if (a0[k] < 0) a0[k] = 0;
+                if (a1[k] > T->dims[k] - 1) a1[k] = T->dims[k] - 1;
+            }
+            for (int64_t z = a0[2]; z <= a1[2]; ++z)
+                for (int64_t y = a0[1]; y <= a1[1]; ++y)
+                    for (int64_t x = a0[0]; x <= a1[0]; ++x) {
+                        const int64_t cell = x + T->dims[0] * (y + T->dims[1] * z);
+                        if (pass == 0) cnt[cell + 1]++;
+                        else T->aabb[T->start[cell] + cnt[cell]++] = j;
+                    }
+        }
+        if (pass == 0) {
+            T->start = (int64_t*)malloc(sizeof(int64_t) * ((size_t)nc + 1));
+            T->start[0] = 0;
+            for (int64_t c = 0; c < nc; ++c) T->start[c + 1] = T->start[c] + cnt[c + 1];
+            T->aabb = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T->start[nc] > 0 ? T->start[nc] : 1));
+            memset(cnt, 0, sizeof(int64_t) * ((size_t)nc + 1));
+        }
+    }
+    free(cnt);
+    T->stamp = (int64_t*)calloc((size_t)G->n_aabb, sizeof(int64_t));
+    G->tg = T;
+}
+
+/* R43-R44: the segment's nearest SDF hit over every AABB (tier 0; tier 1 when G->tg is set) */
 int64_t or_sdf_nearest(const or_scene* S, const or_sdf* G, const or_sdf_params* Q, const float o[3],
                        const float d[3], const float* lam, int n_lam, int64_t prev_cell, float tau,
                        float cos_ex, float* t_out, int64_t* cell_out, float n_out[3]) {
     float bt = INFINITY;
     int64_t bj = -1;
-    for (int64_t j = 0; j < G->n_aabb; ++j) {
-        if (G->cell[j] == prev_cell) continue;
-        float t;
-        if (!march(S, G, j, o, d, Q, &t)) continue;
-        if (!(t < bt)) continue;  /* cells ascend: equal t keeps the lower cell */
-        if (excluded(S, G, j, o, lam, n_lam, Q, tau, cos_ex)) continue;
-        bt = t;
-        bj = j;
+    if (G->tg) {
+        bj = nearest_t1(S, G, Q, o, d, lam, n_lam, prev_cell, tau, cos_ex, &bt);
+    } else {
+        for (int64_t j = 0; j < G->n_aabb; ++j) {
+            if (G->cell[j] == prev_cell) continue;
+            float t;
+            if (!march(S, G, j, o, d, Q, &t)) continue;
+            if (!(t < bt)) continue;  /* cells ascend: equal t keeps the lower cell */
+            if (excluded(S, G, j, o, lam, n_lam, Q, tau, cos_ex)) continue;
+            bt = t;
+            bj = j;
+        }
     }
     *t_out = bt;
     if (bj < 0) {
