@@ -116,3 +116,17 @@ def test_env_fullsize_sharded_subset_bit_exact(N, O, name, parts):
     assert info["n_raw"] == len(raw) and info["bounces"] == rays, (info["n_raw"], len(raw), info["bounces"], rays)
     assert_same_records(got, ref, f"NEXT-2 {name} shard 0/{parts}")
     assert len(got) > 0
+
+
+def test_env_full_c2_bit_exact(N, O):
+    """The paper's setting on the whole C2 scene: <= 3 reflections, <= 1 diffraction, kappa 100
+    (1.3e7 validation rays): set, raw and validation-ray counts equal the oracle's (tier-1 SDF
+    grid)."""
+    case = G.case("C2", sigma=0.010, max_refl=3, max_diff=1)
+    case.sdf = dict(SDF)
+    case.kappa = 100
+    got, info = run(N, case)
+    ref, n_raw, nrays = O.env_launch(case, procs=NPROC, sdf_grid=0.125)
+    assert info["n_raw"] == n_raw and info["bounces"] == nrays, (info["n_raw"], n_raw, info["bounces"], nrays)
+    assert_same_records(got, ref, "NEXT-2 full C2")
+    assert len(got) > 10_000

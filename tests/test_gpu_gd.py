@@ -126,3 +126,15 @@ def test_gd_errors(N):
     co = N.launch_case(sc, case)
     with pytest.raises(N.NrtError):
         N.nrt_refine_ex(sc, co, select=1, **N.gd_desc(case))
+
+
+def test_gd_full_c2_sdf_set_bit_exact(N, O):
+    """Every path of the whole C2 SDF coarse set (1864) refined by the paper's GD (rho = 2000):
+    all records equal the oracle's (tier-1 SDF grid)."""
+    case = G.case("C2", sigma=0.010)
+    case.sdf = dict(SDF)
+    coarse, got, _ = run_gd(N, case)
+    assert len(coarse) > 1000
+    ref = O.refine_gd_par(case, coarse, procs=NPROC, sdf_grid=0.125)
+    compare(got, ref, "GD full C2")
+    assert (got["status"] == 0).sum() > 500

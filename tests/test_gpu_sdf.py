@@ -160,3 +160,14 @@ def test_fullsize_sdf_sampled_hit_sequences(N, O, name):
     _, hits, _ = O.trace_rays(case, ids)
     assert np.array_equal(gpu, hits)
     assert (gpu[:, 1] >= 0).sum() > 3
+
+
+def test_full_c2_sdf_set_bit_exact(N, O):
+    """The whole C2 SDF launch (1e6 surfels, 1e6 rays, diffraction: 5.5e6 segments) equals the
+    oracle's whole set (tier-1 SDF grid, pinned to tier 0), raw and bounce counts included."""
+    case = sdf_case("C2", sigma=0.010)
+    got, info, _ = run(N, case)
+    ref, n_raw, nb = O.launch_phased(case, procs=NPROC, scene=O.coarse_scene(case, sdf_grid=0.125))
+    assert info["bounces"] == nb and info["n_raw"] == n_raw
+    assert_same_records(got, ref, "SDF full C2")
+    assert len(got) > 1000
