@@ -249,12 +249,12 @@ def oracle_scene(case):
     """The oracle's scene: tier-1 grid (disk hit), or the tier-0 SDF tracer (case.sdf)."""
     from oracle import oracle as O
     if getattr(case, "sdf", None):
-        return O.OracleScene(case.scene, sdf_cell=case.sdf["cell"])
+        return O.OracleScene(case.scene, sdf_cell=case.sdf["cell"], sdf_grid=0.125)
     return O.OracleScene(case.scene, grid_voxel=oracle_voxel(case))
 
 
 def oracle_kind(case):
-    return ("tier-0 SDF oracle (oracle/sdf.c, every AABB per segment)" if getattr(case, "sdf", None)
+    return ("tier-1 SDF oracle (oracle/sdf.c, own 12.5 cm grid over the AABBs)" if getattr(case, "sdf", None)
             else "tier-1 grid oracle")
 
 
@@ -303,14 +303,14 @@ def _env_chunk(args):
     return O._env_worker((case, part, parts))[1]
 
 
-def cpu_baseline_env(case, parts=512):
+def cpu_baseline_env(case, parts=128):
     """NEXT-2: the oracle (env.c, tier-0 SDF validation) on this host's cores over the first P of
     `parts` transmission shards (IE i == k mod parts): validation rays per second."""
     import multiprocessing as mp
     from oracle import oracle as O
     O.env_lib()
     P = os.cpu_count() or 1
-    O._FORK["env"] = O.EnvScene(case)
+    O._FORK["env"] = O.EnvScene(case, sdf_grid=0.125)
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(P) as pool:
@@ -319,7 +319,7 @@ def cpu_baseline_env(case, parts=512):
     O._FORK.pop("env", None)
     return {"value": sum(res) / wall, "unit": UNIT, "cores": P, "kind": "oracle",
             "sample": f"transmission shards 0..{min(P, parts) - 1} of {parts} of {case.name} (NEXT-2 "
-                      f"oracle, tier-0 SDF validation rays and their cone-traced subtrees), {wall:.1f} s "
+                      f"oracle, tier-1 SDF validation rays and their cone-traced subtrees), {wall:.1f} s "
                       f"wall on {P} processes"}
 
 
