@@ -246,7 +246,7 @@ def oracle_voxel(case):
 
 
 def oracle_scene(case):
-    """The oracle's scene: tier-1 grid (disk hit), or the tier-0 SDF tracer (case.sdf)."""
+    """The oracle's scene: tier-1 grid (disk hit), or the tier-1 SDF tracer (case.sdf)."""
     from oracle import oracle as O
     if getattr(case, "sdf", None):
         return O.OracleScene(case.scene, sdf_cell=case.sdf["cell"], sdf_grid=0.125)
@@ -304,7 +304,7 @@ def _env_chunk(args):
 
 
 def cpu_baseline_env(case, parts=128):
-    """NEXT-2: the oracle (env.c, tier-0 SDF validation) on this host's cores over the first P of
+    """NEXT-2: the oracle (env.c, tier-1 SDF validation) on this host's cores over the first P of
     `parts` transmission shards (IE i == k mod parts): validation rays per second."""
     import multiprocessing as mp
     from oracle import oracle as O
