@@ -171,3 +171,30 @@ def test_full_c2_sdf_set_bit_exact(N, O):
     assert info["bounces"] == nb and info["n_raw"] == n_raw
     assert_same_records(got, ref, "SDF full C2")
     assert len(got) > 1000
+
+
+@pytest.mark.parametrize("name,rays", [("C4", 60_000), ("C5", 60_000)])
+def test_fullsize_sdf_sharded_subset(N, O, name, rays):
+    """A shard of the full-size C4 / C5 lattice (1e7 surfels; 1e7 / 1e8 rays) with the SDF
+    intersection through the production path (stage 1): every raw record (kappa = 2^30), the
+    events and the bounce count equal the oracle's (tier-1 SDF grid)."""
+    import multiprocessing as mp
+    case = sdf_case(name)
+    case.kappa = 1 << 30
+    world = case.n_rays // rays
+    rank = world // 5
+    sc = N.build_case_scene(case, device_arrays=True)
+    p = N.launch_case(sc, case, rank=rank, world=world, stage=1)
+    got, info, ev = p.export(), p.info(), p.export_events()
+    O._FORK["case"], O._FORK["max_diff"] = case, None
+    O._FORK["scene"] = O.coarse_scene(case, sdf_grid=0.125)
+    with mp.get_context("fork").Pool(NPROC) as pool:
+        parts = pool.map(O._primary_worker, [(rank + q * world, NPROC * world) for q in range(NPROC)])
+    O._FORK.pop("scene")
+    raw = np.concatenate([x[0] for x in parts])
+    ref_ev = O.event_dedupe(np.concatenate([x[1] for x in parts]))
+    ref = O.dedupe(raw, case.kappa)
+    assert info["bounces"] == sum(x[2] for x in parts)
+    assert len(got) == len(ref) and got.tobytes() == ref.tobytes()
+    assert len(ev) == len(ref_ev) and ev.tobytes() == ref_ev.tobytes()
+    assert len(got) > 0
