@@ -258,10 +258,11 @@ def oracle_kind(case):
             else "tier-1 grid oracle")
 
 
-def _oracle_chunk(args):
-    case, ids = args
+def _oracle_chunk(ids):
+    """One forked worker's rays; the case and the oracle scene come from the fork (pickling the
+    1e7-surfel case per task cost seconds per step)."""
     from oracle import oracle as O
-    _, _, nb = O.trace_rays(case, ids, scene=O._FORK.get("scene"))
+    _, _, nb = O.trace_rays(O._FORK["case"], ids, scene=O._FORK.get("scene"))
     return nb
 
 
@@ -273,21 +274,22 @@ def cpu_baseline(case, seconds=15.0):
     O.lib()
     P = os.cpu_count() or 1
     O._FORK["scene"] = oracle_scene(case)
+    O._FORK["case"] = case
     ids = np.arange(0, case.n_rays, max(1, case.n_rays // 997), dtype=np.uint64)
     t0 = time.perf_counter()
-    nb0 = _oracle_chunk((case, ids[:64]))
+    nb0 = _oracle_chunk(ids[:64])
     per_bounce = max(1e-9, (time.perf_counter() - t0) / max(1, nb0))
     n_rays = max(P, int(seconds * P / (per_bounce * (case.max_refl + 1))))
     sample = np.linspace(0, case.n_rays - 1, n_rays).astype(np.uint64)
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(P) as pool:
-        res = pool.map(_oracle_chunk, [(case, sample[k::P]) for k in range(P)])
+        res = pool.map(_oracle_chunk, [sample[k::P] for k in range(P)])
     wall = time.perf_counter() - t0
     bounces = sum(res)
     one = sample[: max(1, len(sample) // (4 * P))]
     t1 = time.perf_counter()
-    nb1 = _oracle_chunk((case, one))
+    nb1 = _oracle_chunk(one)
     one_core = nb1 / max(1e-9, time.perf_counter() - t1)
     O._FORK.pop("scene", None)
     return {"value": bounces / wall, "unit": UNIT, "cores": P, "kind": "oracle",
@@ -298,9 +300,9 @@ def cpu_baseline(case, seconds=15.0):
 
 
 def _env_chunk(args):
-    case, part, parts = args
+    part, parts = args
     from oracle import oracle as O
-    return O._env_worker((case, part, parts))[1]
+    return O._env_worker((O._FORK["case"], part, parts))[1]
 
 
 def cpu_baseline_env(case, parts=128):
@@ -311,10 +313,11 @@ def cpu_baseline_env(case, parts=128):
     O.env_lib()
     P = os.cpu_count() or 1
     O._FORK["env"] = O.EnvScene(case, sdf_grid=0.125)
+    O._FORK["case"] = case
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(P) as pool:
-        res = pool.map(_env_chunk, [(case, k, parts) for k in range(min(P, parts))])
+        res = pool.map(_env_chunk, [(k, parts) for k in range(min(P, parts))])
     wall = time.perf_counter() - t0
     O._FORK.pop("env", None)
     return {"value": sum(res) / wall, "unit": UNIT, "cores": P, "kind": "oracle",
@@ -354,7 +357,8 @@ def run_reference(args, case):
     import multiprocessing as mp
     P = os.cpu_count() or 1
     O._FORK["scene"] = oracle_scene(case)
-    rays_per_step = (64 if getattr(case, "sdf", None) else 512) * P
+    O._FORK["case"] = case
+    rays_per_step = (512 if getattr(case, "sdf", None) else 4096) * P
     times, bounces = [], []
     ctx = mp.get_context("fork")
     with ctx.Pool(P) as pool:
@@ -362,7 +366,7 @@ def run_reference(args, case):
             sample = (np.arange(rays_per_step, dtype=np.uint64) * (case.n_rays // rays_per_step)
                       + k).astype(np.uint64)
             t0 = time.perf_counter()
-            res = pool.map(_oracle_chunk, [(case, sample[j::P]) for j in range(P)])
+            res = pool.map(_oracle_chunk, [sample[j::P] for j in range(P)])
             dt = time.perf_counter() - t0
             if k >= args.warmup:
                 times.append(dt)
