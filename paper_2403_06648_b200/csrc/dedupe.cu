@@ -18,8 +18,6 @@ __global__ void k_coarse_keys(const nrt_coarse_rec* r, int64_t n, uint64_t* hi, 
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const nrt_coarse_rec& c = r[i];
-    const uint64_t* l = nullptr;
-    (void)l;
     uint64_t L[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) L[k] = (uint64_t)(uint32_t)c.label[k] & 0xfffull;

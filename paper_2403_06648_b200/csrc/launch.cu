@@ -157,7 +157,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-__device__ __forceinline__ unsigned long long lane_inc(unsigned long long* ctr) {
+[[maybe_unused]] __device__ __forceinline__ unsigned long long lane_inc(unsigned long long* ctr) {
     return atomicAdd(ctr, 1ull);
 }
 #ifndef NRT_TRACE_MINB
@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace(TP P, Wave W, int
 // HIT predicate (R7-R9) of one record against one segment, as a packed lexicographic key
 // (t bits << 32 | id): t > 0 here, so the unsigned order of the key is the (t, id) order, and
 // the nearest hit is the minimum key (~0 = no hit).  Same arithmetic as test_record.
-__device__ __forceinline__ unsigned long long hit_key(const TP& P, const float4 o, const float4 d,
+[[maybe_unused]] __device__ __forceinline__ unsigned long long hit_key(const TP& P, const float4 o, const float4 d,
                                                       const float4 l0, const float4 l1,
                                                       const float4 A, const float4 B) {
     const int id = __float_as_int(B.w);

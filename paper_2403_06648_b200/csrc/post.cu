@@ -11,6 +11,7 @@
 //      in delay order, lanes over the group's earlier kept paths) — the same decisions as the
 //      sequential walk over the whole delay-ordered list.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <cmath>
 
@@ -288,7 +289,7 @@ nrt_status postprocess(nrt_scene s, nrt_paths in, const nrt_post_desc* d, nrt_pa
     ::nrt::count_launch();
     int64_t ng = 0;
     {
-        cub::CountingInputIterator<unsigned> cnt(0);
+        thrust::counting_iterator<unsigned> cnt(0);
         size_t tb = 0;
         cub::DeviceSelect::Flagged(nullptr, tb, cnt, head, gstart, d_ng, m, st);
         char* tmp = nullptr;
@@ -310,7 +311,7 @@ nrt_status postprocess(nrt_scene s, nrt_paths in, const nrt_post_desc* d, nrt_pa
     NRT_TRY(B.get(&d_nk, 1));
     int64_t nk = 0;
     {
-        cub::CountingInputIterator<unsigned> cnt(0);
+        thrust::counting_iterator<unsigned> cnt(0);
         size_t tb = 0;
         cub::DeviceSelect::Flagged(nullptr, tb, cnt, keep_t, sel, d_nk, m, st);
         char* tmp = nullptr;
