@@ -170,6 +170,10 @@ __device__ __forceinline__ float rcp_approx(float x) {
 #ifndef NRT_TRACE_FETCH
 #define NRT_TRACE_FETCH lane_inc
 #endif
+#ifndef NRT_TRACE_UNROLL
+#define NRT_TRACE_UNROLL 3  // records loaded per k_trace iteration before testing them (C5 A/B,
+                            // 1 / 2 / 3 / 4 / 6 / 8: trace 430 / 375 / 359 / 379 / 535 / 676 ms)
+#endif
 #ifndef NRT_TRACE_REFILL
 #define NRT_TRACE_REFILL 8  // 1: each lane refills alone; k > 1: warp refills k+ idle lanes together
 #endif
@@ -632,20 +636,19 @@ __global__ void __launch_bounds__(128, NRT_TRACE_MINB) k_trace(TP P, Wave W, int
         }
 #endif
         if (s.k < s.kend) {
-            // four records per iteration, all loads issued before any test; indices past the
-            // cell end repeat the last record (the (t, id) argmin is idempotent)
+            // NRT_TRACE_UNROLL records per iteration, all loads issued before any test; indices
+            // past the cell end repeat the last record (the (t, id) argmin is idempotent)
             const unsigned last = s.kend - 1;
-            const unsigned k0 = s.k, k1 = min(k0 + 1, last), k2 = min(k0 + 2, last),
-                           k3 = min(k0 + 3, last);
-            const float4 A0 = __ldg(&P.rec[2 * k0]), B0 = __ldg(&P.rec[2 * k0 + 1]);
-            const float4 A1 = __ldg(&P.rec[2 * k1]), B1 = __ldg(&P.rec[2 * k1 + 1]);
-            const float4 A2 = __ldg(&P.rec[2 * k2]), B2 = __ldg(&P.rec[2 * k2 + 1]);
-            const float4 A3 = __ldg(&P.rec[2 * k3]), B3 = __ldg(&P.rec[2 * k3 + 1]);
-            test_record(P, s, A0, B0);
-            test_record(P, s, A1, B1);
-            test_record(P, s, A2, B2);
-            test_record(P, s, A3, B3);
-            s.k = min(k0 + 4, s.kend);
+            float4 A[NRT_TRACE_UNROLL], B[NRT_TRACE_UNROLL];
+#pragma unroll
+            for (int u = 0; u < NRT_TRACE_UNROLL; ++u) {
+                const unsigned ku = min(s.k + u, last);
+                A[u] = __ldg(&P.rec[2 * ku]);
+                B[u] = __ldg(&P.rec[2 * ku + 1]);
+            }
+#pragma unroll
+            for (int u = 0; u < NRT_TRACE_UNROLL; ++u) test_record(P, s, A[u], B[u]);
+            s.k = min(s.k + NRT_TRACE_UNROLL, s.kend);
             continue;
         }
         const float te = fminf(s.tmx, fminf(s.tmy, s.tmz));
