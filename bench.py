@@ -69,10 +69,20 @@ class Clocks:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                 "--format=csv,noheader,nounits", "-lms", os.environ.get("NRT_CLOCKS_MS", "200")],
+                stdout=self.f,
                 stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+        # keep nvidia-smi's start-up (NVML init) out of the timed region: start timing after its
+        # first sample (interval: the profiling recipe's 200 ms; NRT_CLOCKS_MS overrides)
+        t0 = time.time()
+        while self.p is not None and time.time() - t0 < 10.0:
+            self.f.flush()
+            if os.path.getsize(self.path) > 0:
+                time.sleep(0.3)
+                break
+            time.sleep(0.05)
         return self
 
     def __exit__(self, *a):
