@@ -1916,7 +1916,11 @@ nrt_status refine(nrt_scene s, nrt_paths coarse, const nrt_refine_desc* d, nrt_p
     int per_sm = 0;
     if (warp_impl) {
         NRT_CUDA(cudaFuncSetAttribute(k_refine_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w));
+        if (const char* cv = getenv("NRT_REFINE_CARVEOUT"))  // A/B: shared-memory share of L1 (%)
+            cudaFuncSetAttribute(k_refine_w, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_w, 32 * kWPB, smem_w);
+        if (getenv("NRT_REFINE_CARVEOUT"))
+            fprintf(stderr, "nrt: k_refine_w smem %zu B per block, %d blocks/SM\n", smem_w, per_sm);
     } else {
         NRT_CUDA(cudaFuncSetAttribute(k_refine_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_b, 32 * NW, smem_b);
